@@ -1,0 +1,335 @@
+/* kvgpu — B200 (sm_100a) engine for the Concur / kvadmit simulator hot path.
+ *
+ * This is the drop-in C boundary for the reference's hot path
+ *   kvadmit::run_simulation(Population, Policy, CostParams, EngineParams)
+ *   (/root/reference/proj/src/engine.hpp:75-78, engine.cpp:446-456)
+ * and for the cache-policy seam it drives per event
+ *   kvadmit::CacheTree (/root/reference/proj/src/cache_tree.hpp:94-198).
+ *
+ * Conventions follow the reference C ABI (/root/reference/proj/include/kvadmit/kvadmit.h):
+ *   - every fallible call returns a status, 0 = success            (kvadmit.h:33-40)
+ *   - kvg_last_error() is a thread-local message, never NULL        (kvadmit.h:44-45)
+ *   - opaque handles are freed with their *_free function           (kvadmit.h:56-64)
+ *   - exceptions never cross the ABI                                (capi.cpp:47-65)
+ * Only plain C types cross this boundary (no torch / CUDA types). A handle is
+ * bound to one CUDA device; separate handles may be driven from separate host
+ * threads (one per GPU). Calls on one handle must be externally serialized.
+ */
+#ifndef KVGPU_KVGPU_H_
+#define KVGPU_KVGPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#define KVG_API __attribute__((visibility("default")))
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Mirrors kva_status (kvadmit.h:33-40) plus KVG_ERR_CUDA. */
+typedef enum kvg_status {
+  KVG_OK = 0,
+  KVG_ERR_CONFIG = 1,           /* bad configuration, argument, or request */
+  KVG_ERR_IO = 2,               /* filesystem failure */
+  KVG_ERR_HORIZON = 3,          /* a simulation exceeded its horizon guard */
+  KVG_ERR_STATE = 4,            /* invariant violation or API misuse */
+  KVG_ERR_MISSING_BASELINE = 5, /* kept for parity with kva_status */
+  KVG_ERR_CUDA = 6              /* CUDA runtime failure or no device */
+} kvg_status;
+
+KVG_API const char* kvg_version(void);
+/* Message for the most recent failure in this thread; never NULL. */
+KVG_API const char* kvg_last_error(void);
+
+/* ------------------------------------------------------------------ */
+/* Inputs. Field meanings follow the reference structs cited per type. */
+/* ------------------------------------------------------------------ */
+
+/* workload.hpp:29-44 (Distribution). */
+enum { KVG_DIST_CONSTANT = 0, KVG_DIST_UNIFORM = 1, KVG_DIST_LOGNORMAL = 2 };
+typedef struct kvg_distribution {
+  uint32_t kind; /* KVG_DIST_* */
+  uint32_t _pad;
+  double a; /* constant value | uniform min | lognormal mean */
+  double b; /* uniform max | lognormal sigma */
+} kvg_distribution;
+
+/* workload.hpp:102-113 (WorkloadConfig). */
+typedef struct kvg_workload_config {
+  uint32_t agents;
+  uint32_t shared_prompt; /* bool */
+  uint64_t prompt_tokens;
+  uint32_t steps;
+  uint32_t _pad;
+  kvg_distribution gen_tokens;
+  kvg_distribution obs_tokens;
+  kvg_distribution tool_latency;
+  double tool_probability;
+} kvg_workload_config;
+
+/* workload.hpp:60-66 (StepPlan). */
+typedef struct kvg_step_plan {
+  uint64_t gen_tokens;
+  uint64_t obs_tokens;
+  double tool_latency;
+  uint32_t has_tool; /* bool */
+  uint32_t _pad;
+} kvg_step_plan;
+
+/* workload.hpp:115-128 (Population). Agent a's context is never materialised:
+ * token p of agent a is p (p < prompt_tokens, shared prompt) or
+ * ((a+1)<<32)|(p - shared_len) otherwise (workload.cpp:139-142, 167-171). */
+typedef struct kvg_population {
+  uint32_t agents;
+  uint32_t steps; /* plans per agent (WorkloadConfig.steps) */
+  uint64_t prompt_tokens;
+  uint32_t shared_prompt; /* bool */
+  uint32_t _pad;
+  uint64_t shared_prompt_tokens; /* 0 when prompts are private */
+  uint64_t stream_hash;          /* FNV-1a over sampled values */
+  uint64_t peak_aggregate_tokens;
+  kvg_step_plan* plans; /* agents*steps, row-major by agent */
+} kvg_population;
+
+/* controller.hpp:29-42 (ControllerConfig) and :49-62 (Policy). */
+enum {
+  KVG_POLICY_UNCONTROLLED = 0,
+  KVG_POLICY_REQUEST_CAP = 1,
+  KVG_POLICY_AGENT_CAP = 2,
+  KVG_POLICY_AIMD = 3
+};
+typedef struct kvg_controller_config {
+  double alpha, beta, u_low, u_high, h_thresh, w_min, w_max, initial_window,
+      control_interval, signal_smoothing;
+} kvg_controller_config;
+typedef struct kvg_policy {
+  uint32_t kind; /* KVG_POLICY_* */
+  uint32_t cap;
+  kvg_controller_config aimd;
+} kvg_policy;
+
+/* cost_model.hpp:26-36 (CostParams). */
+typedef struct kvg_cost_params {
+  double prefill_linear, prefill_quadratic, decode_base, decode_context,
+      bytes_per_token, pcie_bandwidth, transfer_sync_overhead;
+} kvg_cost_params;
+
+/* metrics.hpp:57-63 (PhaseParams) and engine.hpp:29-41 (EngineParams). */
+enum { KVG_EVICT_DISCARD = 0, KVG_EVICT_OFFLOAD = 1 };
+typedef struct kvg_phase_params {
+  double sat_threshold, hit_threshold;
+  int32_t hysteresis;
+  int32_t _pad;
+} kvg_phase_params;
+typedef struct kvg_engine_params {
+  uint64_t capacity;  /* device pool, pages */
+  uint64_t page_size; /* tokens per page */
+  uint32_t eviction;  /* KVG_EVICT_* */
+  uint32_t paranoid;  /* accepted for parity; device runs always self-check */
+  double hit_window_decay;
+  double horizon;
+  kvg_phase_params phases;
+} kvg_engine_params;
+
+/* One simulation = one reference run_simulation() call. */
+typedef struct kvg_sim_desc {
+  const kvg_population* population;
+  kvg_policy policy;
+  kvg_cost_params cost;
+  kvg_engine_params engine;
+} kvg_sim_desc;
+
+/* ------------------------------------------------------------------ */
+/* Outputs (metrics.hpp:27-43, 77-83; engine.hpp:45-69).               */
+/* ------------------------------------------------------------------ */
+
+/* TraceRecord (metrics.hpp:27-39) with the TickHits pair (engine.hpp:45-48). */
+typedef struct kvg_trace_row {
+  double time, usage, hit_rate, window;
+  uint64_t active, pending, decoded_cum, recompute_cum, transfers;
+  double hit_matched, hit_requested;
+} kvg_trace_row;
+
+/* AgentStats (workload.hpp:75-82) plus the completion record the north star
+ * asks for: simulated finish time and the event ordinal that finished it. */
+typedef struct kvg_agent_stats {
+  uint64_t generated_tokens, recompute_tokens, recompute_events, stall_events,
+      pause_events;
+  double wait_time;
+  double finish_time;
+  uint64_t finish_ordinal;
+} kvg_agent_stats;
+
+typedef struct kvg_ledger {
+  double prefill_fresh, prefill_recompute, decode, transfer, tool_wait;
+} kvg_ledger;
+
+enum { KVG_PHASE_WARMUP = 0, KVG_PHASE_MIDDLE = 1, KVG_PHASE_COOLDOWN = 2 };
+typedef struct kvg_phase_label {
+  uint32_t phase;
+  uint32_t _pad;
+  double start, end;
+} kvg_phase_label;
+
+/* SimulationResult scalars (engine.hpp:50-69) plus hot-path counters. */
+typedef struct kvg_sim_result {
+  int32_t status; /* kvg_status of this simulation */
+  uint32_t n_phases;
+  kvg_ledger ledger;
+  double makespan, device_busy, link_busy;
+  uint64_t decoded_tokens, recompute_tokens, recompute_events, stall_events,
+      offloaded_tokens, reloaded_tokens, discarded_tokens;
+  double total_wait_time;
+  uint64_t ticks;
+  uint64_t workload_hash;
+  /* hot-path counters (BASELINE.md §2 definitions) */
+  uint64_t agent_steps;  /* successful dispatch_member calls */
+  uint64_t lookups;      /* resolved prefix pages + terminating miss */
+  uint64_t events;       /* processed (non-skipped) events */
+  uint64_t evict_calls;  /* CacheTree::evict calls with needed > 0 */
+  uint64_t evicted_pages;
+  uint64_t cache_clock;  /* final CacheTree clock */
+  uint64_t pool_used;    /* final resident pages */
+  double hit_matched, hit_requested; /* final hit window */
+  kvg_phase_label phases[3];
+} kvg_sim_result;
+
+/* Optional per-simulation event log (parity testing). */
+enum {
+  KVG_LOG_MATCH = 1,   /* agent, clock, a = matched tokens, b = lookups   */
+  KVG_LOG_INSERT = 2,  /* agent, clock, a = ok,            b = stored     */
+  KVG_LOG_EVICT = 3,   /* clock,        a = needed,        b = reclaimed  */
+  KVG_LOG_VICTIM = 4,  /*               a = page key,      b = stamp      */
+  KVG_LOG_FINISH = 5,  /* agent,        a = time bits,     b = ordinal    */
+  KVG_LOG_DISCARD = 6  /* agent, clock, a = from page,     b = pages      */
+};
+typedef struct kvg_log_record {
+  uint32_t kind;
+  uint32_t agent;
+  uint64_t clock;
+  uint64_t a, b;
+} kvg_log_record;
+
+/* ------------------------------------------------------------------ */
+/* Host prologue: population build (workload.cpp:153-204).             */
+/* ------------------------------------------------------------------ */
+
+/* Fills *out; out->plans is allocated by the library and released with
+ * kvg_population_free. Identical to the reference sampling stream bit for
+ * bit (splitmix64 + libm Box-Muller, FNV-1a stream hash). */
+KVG_API kvg_status kvg_build_population(const kvg_workload_config* cfg,
+                                        uint64_t seed, kvg_population* out);
+KVG_API void kvg_population_free(kvg_population* pop);
+
+/* Reference calibration (cost_model.cpp:49-59) and defaults
+ * (controller.hpp:29-42, metrics.hpp:57-63, engine.hpp:29-41). */
+KVG_API void kvg_cost_params_init(kvg_cost_params* p);
+KVG_API void kvg_controller_config_init(kvg_controller_config* c);
+KVG_API void kvg_engine_params_init(kvg_engine_params* e);
+
+/* ------------------------------------------------------------------ */
+/* Batched simulation on one device.                                   */
+/* ------------------------------------------------------------------ */
+
+typedef struct kvg_batch kvg_batch;
+
+typedef struct kvg_batch_options {
+  uint32_t warps_per_sim; /* 0 = automatic (1 for small sims, up to 32)   */
+  uint32_t log_capacity;  /* per-sim event-log records; 0 disables logging */
+  uint64_t trace_capacity;/* per-sim trace rows; 0 = automatic (grows)     */
+} kvg_batch_options;
+
+KVG_API void kvg_batch_options_init(kvg_batch_options* o);
+
+/* Validates every descriptor (engine.cpp:446-452 semantics), copies the
+ * populations to device memory and sizes the per-simulation workspaces. */
+KVG_API kvg_status kvg_batch_create(int device, const kvg_sim_desc* sims,
+                                    size_t n, const kvg_batch_options* opt,
+                                    kvg_batch** out);
+/* Runs every simulation to completion on the device (blocking). Re-runnable:
+ * each call starts from the initial state. Returns KVG_ERR_HORIZON if any
+ * simulation hit its horizon (per-sim status in kvg_batch_result), with the
+ * partial results still readable, as run_simulation's partial_on_abort. */
+KVG_API kvg_status kvg_batch_run(kvg_batch* b);
+/* Device time of the last kvg_batch_run, milliseconds (CUDA events). */
+KVG_API kvg_status kvg_batch_last_ms(const kvg_batch* b, double* ms);
+/* Copies results device->host (done once per run, lazily). */
+KVG_API kvg_status kvg_batch_result(kvg_batch* b, size_t i,
+                                    kvg_sim_result* out);
+KVG_API kvg_status kvg_batch_trace(kvg_batch* b, size_t i, kvg_trace_row* rows,
+                                   size_t cap, size_t* n_rows);
+KVG_API kvg_status kvg_batch_agent_stats(kvg_batch* b, size_t i,
+                                         kvg_agent_stats* out, size_t cap,
+                                         size_t* n_agents);
+KVG_API kvg_status kvg_batch_log(kvg_batch* b, size_t i, kvg_log_record* out,
+                                 size_t cap, size_t* n_records);
+KVG_API void kvg_batch_free(kvg_batch* b);
+
+/* One-shot convenience: create, run, read scalar results, free. */
+KVG_API kvg_status kvg_run_batch(int device, const kvg_sim_desc* sims,
+                                 size_t n, kvg_sim_result* results);
+
+/* Phase classification of a trace (metrics.cpp:41-81), host-side. */
+KVG_API kvg_status kvg_classify_phases(const kvg_trace_row* rows, size_t n,
+                                       double makespan,
+                                       const kvg_phase_params* params,
+                                       kvg_phase_label* out, size_t cap,
+                                       size_t* n_out);
+
+/* ------------------------------------------------------------------ */
+/* Cache-policy seam: a device-resident paged prefix cache driven by a */
+/* batch of CacheTree-style operations (cache_tree.hpp:96-167).        */
+/* Sequences are owner-form: (agent, length) names the token sequence  */
+/* agent `agent` would hold at that length under the population token */
+/* scheme above, with the cache's shared prompt configuration.         */
+/* ------------------------------------------------------------------ */
+
+enum {
+  KVG_OP_MATCH = 1,   /* match_prefix(seq)          -> r0 = matched, r1 = host_matched */
+  KVG_OP_INSERT = 2,  /* insert(seq)                -> r0 = ok, r1 = inserted slots    */
+  KVG_OP_EVICT = 3,   /* evict(arg)                 -> r0 = reclaimed                  */
+  KVG_OP_PIN = 4,     /* pin(seq, arg tokens)                                          */
+  KVG_OP_UNPIN = 5,   /* unpin(seq, arg tokens)     -> status on underflow             */
+  KVG_OP_DISCARD = 6  /* discard_suffix(seq, arg)                                      */
+};
+typedef struct kvg_cache_op {
+  uint32_t kind;
+  uint32_t agent;
+  uint64_t len; /* sequence length in tokens */
+  uint64_t arg;
+} kvg_cache_op;
+typedef struct kvg_cache_op_result {
+  int32_t status;
+  uint32_t _pad;
+  uint64_t r0, r1;
+  uint64_t clock, used;
+  uint64_t victims_begin, victims_end; /* range into the victim list */
+} kvg_cache_op_result;
+typedef struct kvg_victim {
+  uint64_t key;   /* (owner << 32) | page index; owner 0 = shared prompt */
+  uint64_t stamp; /* last-access stamp at eviction */
+} kvg_victim;
+
+typedef struct kvg_cache kvg_cache;
+KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity,
+                                    uint64_t page_size, uint32_t eviction,
+                                    uint64_t prompt_tokens,
+                                    uint32_t shared_prompt, uint32_t max_agents,
+                                    kvg_cache** out);
+/* Executes ops in order on the device. Victims of each op are appended to
+ * the handle's victim list, ordered as the reference evicts them
+ * (stamp ascending, deeper page first). */
+KVG_API kvg_status kvg_cache_exec(kvg_cache* c, const kvg_cache_op* ops,
+                                  size_t n, kvg_cache_op_result* results);
+KVG_API kvg_status kvg_cache_victims(const kvg_cache* c, size_t begin,
+                                     size_t end, kvg_victim* out);
+KVG_API kvg_status kvg_cache_hit_window(const kvg_cache* c, double* matched,
+                                        double* requested);
+KVG_API void kvg_cache_free(kvg_cache* c);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* KVGPU_KVGPU_H_ */
