@@ -339,3 +339,21 @@ def c5_stress(policy: str = "aimd", seed: int = 5, agents: int = 65536,
 
 def scaled_capacity(peak_tokens: int, page: int = 16, ratio: float = 1.5) -> int:
     return int(math.floor(peak_tokens / page / ratio))
+
+
+def scenario_to_dict(s: Scenario) -> dict:
+    from dataclasses import asdict
+    return asdict(s)
+
+
+def scenario_from_dict(d: dict) -> Scenario:
+    s = Scenario(name=d["name"], seed=d["seed"], policy=d["policy"],
+                 compare=d.get("compare"), sweep=d.get("sweep"))
+    w = dict(d["workload"])
+    for k in ("gen_tokens", "obs_tokens", "tool_latency"):
+        w[k] = Distribution(**w[k])
+    s.workload = WorkloadConfig(**w)
+    s.engine = EngineParams(**d["engine"])
+    s.controller = ControllerConfig(**d["controller"])
+    s.cost = CostParams(**d["cost"])
+    return s

@@ -1,0 +1,117 @@
+// Device-side data layout of the B200 engine (shared by engine.cu and capi.cu).
+//
+// One simulation = one CTA (NW warps). Everything a simulation owns lives in
+// one HBM workspace carved by the host (capi.cu: plan_workspace):
+//
+//   table / alt   paged prefix cache: open-addressing hash of 32-page CHUNKS.
+//                 A bucket is 32 x 16 B slots = 512 B; lane l of a warp owns
+//                 slot l, so one bucket is one fully coalesced 128-bit-per-lane
+//                 probe. Slot = {u64 key = owner<<32 | page, u64 meta}.
+//   occ           dense list of claimed bucket indices (eviction scans this,
+//                 not the whole table).
+//   agents        AgentDev records (hot agent state + its single pending event).
+//   pend / paus   controller FIFO rings; active set is a linked list in AgentDev.
+//   ready/batch   dispatch scratch.
+//   trace / log   outputs (trace rows per control tick; optional event log).
+#pragma once
+#include <stdint.h>
+
+#include "../../include/kvgpu.h"
+
+namespace kvg {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+
+constexpr int kChunk = 32;                   // pages per bucket
+constexpr u64 kEmptyKey = ~0ull;             // unclaimed bucket marker
+constexpr u64 kResident = 1ull << 63;        // meta: page is device resident
+constexpr int kPinShift = 40;                // meta: pins in bits 40..61
+constexpr u64 kPinMask = (1ull << 22) - 1;
+constexpr u64 kStampMask = (1ull << 40) - 1; // meta: stamp in bits 0..39
+
+struct Slot {
+  u64 key;
+  u64 meta;
+};
+
+enum AgentState : uint8_t { S_PENDING, S_AWAIT, S_GEN, S_TOOL, S_PAUSED, S_DONE };
+enum EventKind : uint8_t { EV_NONE = 0, EV_GEN = 1, EV_TOOL = 2, EV_XFER = 3 };
+
+struct AgentDev {     // 96 B
+  double ev_time;     // pending event (valid when ev_kind != EV_NONE)
+  u64 ev_ord;
+  u64 ctx;            // context length in tokens
+  u64 high_water;
+  u64 pinned;         // pinned_len (tokens)
+  double ready_since;
+  u64 f_gen, f_rec, f_obs;  // InFlight (engine.cpp:71-77)
+  double f_tool;
+  u32 step;
+  uint8_t state, ev_kind, f_has_tool, in_active;
+  u32 next, prev;     // active-list links (insertion order)
+};
+
+struct Member {       // one dispatched batch member (engine.cpp:293-299)
+  u32 id, pad;
+  double t, f, r, d;
+};
+
+// Per-simulation device descriptor (inputs, workspace pointers, outputs).
+struct SimDev {
+  // ---- inputs
+  const kvg_step_plan* plans;
+  u32 n_agents, n_steps;
+  u64 prompt_tokens;
+  u64 shared_len;     // Population::shared_prompt_tokens
+  u64 shared_pages;   // pages wholly inside a shared prompt (owner 0)
+  u64 workload_hash;
+  kvg_policy policy;
+  kvg_cost_params cost;
+  kvg_engine_params engine;
+  // ---- workspace
+  Slot* table;
+  Slot* alt;
+  u32* occ;
+  u32* alt_occ;
+  u32 bucket_mask;    // buckets - 1 (power of two)
+  u32 pad0;
+  AgentDev* agents;
+  u32* pend;
+  u32* paus;
+  u32* ready;
+  Member* batch;
+  // ---- outputs
+  kvg_agent_stats* stats;
+  kvg_trace_row* trace;
+  u64 trace_cap;
+  kvg_log_record* log;
+  u64 log_cap;
+  kvg_sim_result* result;
+  u64* counts;        // [0] = trace rows produced, [1] = log records produced
+};
+
+// Cache-op (CacheTree seam) executor descriptor.
+struct CacheDev {
+  u64 capacity, page_size, shared_pages;
+  Slot* table;
+  Slot* alt;
+  u32* occ;
+  u32* alt_occ;
+  u32 bucket_mask;
+  u32 n_ops;
+  const kvg_cache_op* ops;
+  kvg_cache_op_result* results;
+  kvg_victim* victims;  // appended per op (unordered within an op; host sorts)
+  u64 victim_cap;
+  u64* state;           // persistent scalars across exec calls (see CacheState)
+};
+
+// Persistent cache scalars for the cache-op executor.
+struct CacheState {
+  u64 used, clock, pinned_pages, occ_n, discarded, n_victims;
+  double hit_m, hit_r;
+  u64 swapped;  // table/alt swapped by a rebuild (parity of rebuilds)
+};
+
+}  // namespace kvg

@@ -1,0 +1,279 @@
+"""Python mirror of the reference hot-path seam, over the C ABI (libkvgpu.so).
+
+    run_simulation(population, policy, cost, params)   ~ engine.hpp:75-78
+    build_population(workload, seed)                   ~ workload.hpp:128
+    Batch([...]).run()                                  ~ run_rows (experiment.cpp:75-108)
+    DeviceCache(...)                                    ~ CacheTree (cache_tree.hpp:94-198)
+
+The library is the product: there is no CPU fallback. Loading fails loudly if
+libkvgpu.so is missing, and every compute call fails with KVG_ERR_CUDA when no
+GPU is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+from .config import Scenario
+
+_lib = None
+
+
+class EngineError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[{abi.STATUS_NAMES.get(status, status)}] {msg}")
+        self.status = status
+
+
+class HorizonError(EngineError):
+    """Simulated time exceeded the horizon (errors.hpp:33-36); partial results kept."""
+
+
+def lib():
+    """Loads libkvgpu.so (build it with `python -m paper_2601_22705_b200.build`)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(abi.LIB_PATH):
+        raise ImportError(f"{abi.LIB_PATH} is missing: the B200 engine has no CPU fallback; "
+                          "run `python -m paper_2601_22705_b200.build`")
+    L = C.CDLL(abi.LIB_PATH)
+    P = C.POINTER
+    L.kvg_version.restype = C.c_char_p
+    L.kvg_last_error.restype = C.c_char_p
+    L.kvg_build_population.argtypes = [P(abi.WorkloadConfig), C.c_uint64, P(abi.Population)]
+    L.kvg_population_free.argtypes = [P(abi.Population)]
+    L.kvg_population_free.restype = None
+    L.kvg_cost_params_init.argtypes = [P(abi.CostParams)]
+    L.kvg_controller_config_init.argtypes = [P(abi.ControllerConfig)]
+    L.kvg_engine_params_init.argtypes = [P(abi.EngineParams)]
+    L.kvg_batch_options_init.argtypes = [P(abi.BatchOptions)]
+    L.kvg_batch_create.argtypes = [C.c_int, P(abi.SimDesc), C.c_size_t, P(abi.BatchOptions),
+                                   P(C.c_void_p)]
+    L.kvg_batch_run.argtypes = [C.c_void_p]
+    L.kvg_batch_last_ms.argtypes = [C.c_void_p, P(C.c_double)]
+    L.kvg_batch_result.argtypes = [C.c_void_p, C.c_size_t, P(abi.SimResult)]
+    L.kvg_batch_trace.argtypes = [C.c_void_p, C.c_size_t, P(abi.TraceRow), C.c_size_t,
+                                  P(C.c_size_t)]
+    L.kvg_batch_agent_stats.argtypes = [C.c_void_p, C.c_size_t, P(abi.AgentStats), C.c_size_t,
+                                        P(C.c_size_t)]
+    L.kvg_batch_log.argtypes = [C.c_void_p, C.c_size_t, P(abi.LogRecord), C.c_size_t,
+                                P(C.c_size_t)]
+    L.kvg_batch_free.argtypes = [C.c_void_p]
+    L.kvg_batch_free.restype = None
+    L.kvg_run_batch.argtypes = [C.c_int, P(abi.SimDesc), C.c_size_t, P(abi.SimResult)]
+    L.kvg_classify_phases.argtypes = [P(abi.TraceRow), C.c_size_t, C.c_double,
+                                      P(abi.PhaseParams), P(abi.PhaseLabel), C.c_size_t,
+                                      P(C.c_size_t)]
+    L.kvg_cache_create.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64,
+                                   C.c_uint32, C.c_uint32, P(C.c_void_p)]
+    L.kvg_cache_exec.argtypes = [C.c_void_p, P(abi.CacheOp), C.c_size_t, P(abi.CacheOpResult)]
+    L.kvg_cache_victims.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, P(abi.Victim)]
+    L.kvg_cache_hit_window.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double)]
+    L.kvg_cache_free.argtypes = [C.c_void_p]
+    L.kvg_cache_free.restype = None
+    _lib = L
+    return L
+
+
+def _check(status: int, allow_horizon: bool = False):
+    if status == abi.KVG_OK or (allow_horizon and status == abi.KVG_ERR_HORIZON):
+        return status
+    msg = lib().kvg_last_error().decode()
+    if status == abi.KVG_ERR_HORIZON:
+        raise HorizonError(status, msg)
+    raise EngineError(status, msg)
+
+
+class Population:
+    """Owning wrapper of kvg_population built by the library (bit-identical to
+    the reference's build_population, workload.cpp:153-204)."""
+
+    def __init__(self, workload, seed: int):
+        self.c = abi.Population()
+        wl = workload.to_abi() if hasattr(workload, "to_abi") else workload
+        _check(lib().kvg_build_population(C.byref(wl), int(seed), C.byref(self.c)))
+
+    @property
+    def stream_hash(self) -> int:
+        return self.c.stream_hash
+
+    @property
+    def peak_aggregate_tokens(self) -> int:
+        return self.c.peak_aggregate_tokens
+
+    def plans(self) -> np.ndarray:
+        n = self.c.agents * self.c.steps
+        if n == 0:
+            return np.zeros((0,), dtype=np.uint8)
+        buf = C.cast(self.c.plans, C.POINTER(C.c_uint8 * (n * C.sizeof(abi.StepPlan)))).contents
+        return np.frombuffer(buf, dtype=np.uint8).copy()
+
+    def __del__(self):
+        if _lib is not None and getattr(self, "c", None) is not None and self.c.plans:
+            _lib.kvg_population_free(C.byref(self.c))
+
+
+def build_population(workload, seed: int) -> Population:
+    return Population(workload, seed)
+
+
+@dataclass
+class SimSpec:
+    """One simulation: a population plus policy / cost / engine parameters."""
+    population: Population
+    policy: abi.Policy
+    cost: abi.CostParams
+    engine: abi.EngineParams
+
+    @staticmethod
+    def from_scenario(s: Scenario, policy_text: str | None = None,
+                      population: Population | None = None) -> "SimSpec":
+        pol, eng = s.resolved(policy_text)
+        pop = population if population is not None else Population(s.workload, s.seed)
+        return SimSpec(pop, pol, s.cost.to_abi(), eng.to_abi())
+
+
+class Batch:
+    """A set of independent simulations executed on one GPU in one launch."""
+
+    def __init__(self, specs: list[SimSpec], device: int = 0, warps_per_sim: int = 0,
+                 log_capacity: int = 0, trace_capacity: int = 0):
+        self.specs = specs
+        self.descs = (abi.SimDesc * max(1, len(specs)))()
+        for i, sp in enumerate(specs):
+            self.descs[i] = abi.SimDesc(population=C.pointer(sp.population.c), policy=sp.policy,
+                                        cost=sp.cost, engine=sp.engine)
+        opt = abi.BatchOptions(warps_per_sim=warps_per_sim, log_capacity=log_capacity,
+                               trace_capacity=trace_capacity)
+        h = C.c_void_p()
+        _check(lib().kvg_batch_create(device, self.descs, len(specs), C.byref(opt), C.byref(h)))
+        self.h = h
+        self.n = len(specs)
+
+    def run(self, allow_horizon: bool = True) -> int:
+        return _check(lib().kvg_batch_run(self.h), allow_horizon=allow_horizon)
+
+    def last_ms(self) -> float:
+        v = C.c_double()
+        _check(lib().kvg_batch_last_ms(self.h, C.byref(v)))
+        return v.value
+
+    def result(self, i: int) -> dict:
+        r = abi.SimResult()
+        _check(lib().kvg_batch_result(self.h, i, C.byref(r)))
+        return abi.struct_to_dict(r)
+
+    def results_raw(self) -> list[abi.SimResult]:
+        out = []
+        for i in range(self.n):
+            r = abi.SimResult()
+            _check(lib().kvg_batch_result(self.h, i, C.byref(r)))
+            out.append(r)
+        return out
+
+    def trace(self, i: int) -> list[dict]:
+        n = C.c_size_t()
+        _check(lib().kvg_batch_trace(self.h, i, None, 0, C.byref(n)))
+        rows = (abi.TraceRow * max(1, n.value))()
+        _check(lib().kvg_batch_trace(self.h, i, rows, n.value, C.byref(n)))
+        return [abi.struct_to_dict(rows[k]) for k in range(n.value)]
+
+    def trace_array(self, i: int) -> np.ndarray:
+        n = C.c_size_t()
+        _check(lib().kvg_batch_trace(self.h, i, None, 0, C.byref(n)))
+        rows = (abi.TraceRow * max(1, n.value))()
+        _check(lib().kvg_batch_trace(self.h, i, rows, n.value, C.byref(n)))
+        return np.ctypeslib.as_array(rows)[: n.value]
+
+    def agent_stats(self, i: int) -> list[dict]:
+        na = self.specs[i].population.c.agents
+        out = (abi.AgentStats * max(1, na))()
+        n = C.c_size_t()
+        _check(lib().kvg_batch_agent_stats(self.h, i, out, na, C.byref(n)))
+        return [abi.struct_to_dict(out[k]) for k in range(na)]
+
+    def log(self, i: int) -> list[tuple]:
+        n = C.c_size_t()
+        _check(lib().kvg_batch_log(self.h, i, None, 0, C.byref(n)))
+        recs = (abi.LogRecord * max(1, n.value))()
+        _check(lib().kvg_batch_log(self.h, i, recs, n.value, C.byref(n)))
+        return [(r.kind, r.agent, r.clock, r.a, r.b) for r in recs[: n.value]]
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().kvg_batch_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_simulation(population: Population, policy: abi.Policy, cost: abi.CostParams,
+                   params: abi.EngineParams, device: int = 0) -> dict:
+    """Mirror of kvadmit::run_simulation: one simulation, full result.
+    Raises HorizonError (with .partial) when the horizon guard trips."""
+    b = Batch([SimSpec(population, policy, cost, params)], device=device)
+    st = b.run(allow_horizon=True)
+    out = dict(result=b.result(0), trace=b.trace(0), agents=b.agent_stats(0))
+    b.close()
+    if st == abi.KVG_ERR_HORIZON:
+        e = HorizonError(st, "simulated time exceeded the horizon")
+        e.partial = out
+        raise e
+    return out
+
+
+class DeviceCache:
+    """Device-resident paged prefix cache driven through CacheTree-style ops."""
+
+    def __init__(self, capacity: int, page_size: int = 1, prompt_tokens: int = 0,
+                 shared_prompt: bool = False, max_agents: int = 64, device: int = 0):
+        h = C.c_void_p()
+        _check(lib().kvg_cache_create(device, capacity, page_size, abi.EVICT_DISCARD,
+                                      prompt_tokens, int(shared_prompt), max_agents,
+                                      C.byref(h)))
+        self.h = h
+
+    def execute(self, ops: list[tuple]) -> list[dict]:
+        """ops: (kind, agent, len, arg). Returns per-op results incl. victims
+        ordered as the reference evicts them."""
+        n = len(ops)
+        arr = (abi.CacheOp * max(1, n))()
+        for i, (k, a, ln, arg) in enumerate(ops):
+            arr[i] = abi.CacheOp(kind=k, agent=a, len=ln, arg=arg)
+        res = (abi.CacheOpResult * max(1, n))()
+        _check(lib().kvg_cache_exec(self.h, arr, n, res))
+        out = []
+        for i in range(n):
+            r = res[i]
+            nv = r.victims_end - r.victims_begin
+            vic = (abi.Victim * max(1, nv))()
+            if nv:
+                _check(lib().kvg_cache_victims(self.h, r.victims_begin, r.victims_end, vic))
+            out.append(dict(status=r.status, r0=r.r0, r1=r.r1, clock=r.clock, used=r.used,
+                            victims=[vic[j].key for j in range(nv)]))
+        return out
+
+    def hit_window(self):
+        m, r = C.c_double(), C.c_double()
+        _check(lib().kvg_cache_hit_window(self.h, C.byref(m), C.byref(r)))
+        return m.value, r.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().kvg_cache_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

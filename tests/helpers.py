@@ -166,3 +166,9 @@ def oracle_run(s: Scenario, policy_text: str | None = None, digests: bool = Fals
                 agents=_rows(agents, s.workload.agents),
                 digests=np.ctypeslib.as_array(dig)[:nd.value].copy() if digests else None,
                 log=[(r.kind, r.agent, r.clock, r.a, r.b) for r in lg[:nl.value]] if log else None)
+
+
+def load_presets() -> dict:
+    import json
+    with open(os.path.join(GOLDEN, "scenarios.json")) as fh:
+        return json.load(fh)
