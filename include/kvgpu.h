@@ -192,6 +192,12 @@ typedef struct kvg_sim_result {
   uint64_t cache_clock;  /* final CacheTree clock */
   uint64_t pool_used;    /* final resident pages */
   double hit_matched, hit_requested; /* final hit window */
+  /* algorithmic-traffic counters (BASELINE.md §2 roofline definitions) */
+  uint64_t hit_pages;       /* pages resolved by lookups (stamp refreshed)   */
+  uint64_t created_pages;   /* pages inserted                                 */
+  uint64_t refreshed_pages; /* resident pages refreshed by successful inserts */
+  uint64_t evict_scanned;   /* resident pages scanned by eviction selects     */
+  uint64_t agent_events;    /* agent state-machine advances                   */
   kvg_phase_label phases[3];
 } kvg_sim_result;
 
@@ -252,8 +258,11 @@ KVG_API kvg_status kvg_batch_create(int device, const kvg_sim_desc* sims,
  * simulation hit its horizon (per-sim status in kvg_batch_result), with the
  * partial results still readable, as run_simulation's partial_on_abort. */
 KVG_API kvg_status kvg_batch_run(kvg_batch* b);
-/* Device time of the last kvg_batch_run, milliseconds (CUDA events). */
+/* Device time of the last kvg_batch_run, milliseconds (CUDA events on the
+ * launching stream): whole step (workspace init + kernels) and kernels only. */
 KVG_API kvg_status kvg_batch_last_ms(const kvg_batch* b, double* ms);
+KVG_API kvg_status kvg_batch_timing(const kvg_batch* b, double* step_ms,
+                                    double* kernel_ms);
 /* Copies results device->host (done once per run, lazily). */
 KVG_API kvg_status kvg_batch_result(kvg_batch* b, size_t i,
                                     kvg_sim_result* out);

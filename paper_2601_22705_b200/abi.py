@@ -115,6 +115,8 @@ class SimResult(C.Structure):
                 ("evict_calls", u64), ("evicted_pages", u64),
                 ("cache_clock", u64), ("pool_used", u64),
                 ("hit_matched", f64), ("hit_requested", f64),
+                ("hit_pages", u64), ("created_pages", u64), ("refreshed_pages", u64),
+                ("evict_scanned", u64), ("agent_events", u64),
                 ("phases", PhaseLabel * 3)]
 
 
@@ -170,3 +172,17 @@ def struct_to_dict(s) -> dict:
             v = [struct_to_dict(x) if isinstance(x, C.Structure) else x for x in v]
         out[name] = v
     return out
+
+
+def bucket_count(capacity: int, agents: int) -> int:
+    """Mirror of capi.cu bucket_count: 4x worst-case live 32-page chunks, pow2."""
+    live = (capacity + 31) // 32 + agents + 2
+    b = 1
+    while b < 4 * live:
+        b <<= 1
+    return max(64, b)
+
+
+def table_bytes(capacity: int, agents: int) -> int:
+    """Primary + alternate hash tables of one simulation (512 B per bucket)."""
+    return 2 * bucket_count(capacity, agents) * 32 * 16

@@ -69,7 +69,7 @@ struct Region {
 struct kvg_batch {
   int device = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evk = nullptr;
   kvg_batch_options opt{};
   size_t n = 0;
   std::vector<kvg_sim_desc> desc;
@@ -92,7 +92,7 @@ struct kvg_batch {
   std::vector<kvg_sim_result> h_results;
   std::vector<u64> h_counts;
   bool fetched = false;
-  double last_ms = 0;
+  double last_ms = 0, last_kernel_ms = 0;
   bool ran = false;
 
   ~kvg_batch() { release(); }
@@ -202,6 +202,7 @@ kvg_status launch(kvg_batch* b) {
   CUDA_TRY(cudaEventRecord(b->ev0, b->stream));
   CUDA_TRY(cudaMemsetAsync(b->arena + b->tables_off, 0xff, b->tables_bytes, b->stream));
   CUDA_TRY(cudaMemsetAsync(b->d_counts, 0, b->n * 3 * sizeof(u64), b->stream));
+  CUDA_TRY(cudaEventRecord(b->evk, b->stream));
   if (b->n_small > 0)
     kvg::engine_kernel_small<<<static_cast<unsigned>(b->n_small), 32, 0, b->stream>>>(b->d_sims);
   // big sims: one launch per distinct warp count (positions are grouped)
@@ -219,6 +220,8 @@ kvg_status launch(kvg_batch* b) {
   float ms = 0;
   CUDA_TRY(cudaEventElapsedTime(&ms, b->ev0, b->ev1));
   b->last_ms = ms;
+  CUDA_TRY(cudaEventElapsedTime(&ms, b->evk, b->ev1));
+  b->last_kernel_ms = ms;
   return KVG_OK;
 }
 
@@ -294,6 +297,7 @@ KVG_API kvg_status kvg_batch_create(int device, const kvg_sim_desc* sims, size_t
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&b->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&b->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&b->ev1);
+  if (e == cudaSuccess) e = cudaEventCreate(&b->evk);
   if (e != cudaSuccess) {
     delete b;
     return (kvg_status)set_error(KVG_ERR_CUDA, cudaGetErrorString(e));
@@ -345,6 +349,13 @@ KVG_API kvg_status kvg_batch_run(kvg_batch* b) {
 KVG_API kvg_status kvg_batch_last_ms(const kvg_batch* b, double* ms) {
   if (b == nullptr || ms == nullptr) return (kvg_status)set_error(KVG_ERR_CONFIG, "null argument");
   *ms = b->last_ms;
+  return KVG_OK;
+}
+
+KVG_API kvg_status kvg_batch_timing(const kvg_batch* b, double* step_ms, double* kernel_ms) {
+  if (b == nullptr) return (kvg_status)set_error(KVG_ERR_CONFIG, "null batch");
+  if (step_ms) *step_ms = b->last_ms;
+  if (kernel_ms) *kernel_ms = b->last_kernel_ms;
   return KVG_OK;
 }
 
@@ -427,6 +438,7 @@ KVG_API void kvg_batch_free(kvg_batch* b) {
   cudaSetDevice(b->device);
   if (b->ev0) cudaEventDestroy(b->ev0);
   if (b->ev1) cudaEventDestroy(b->ev1);
+  if (b->evk) cudaEventDestroy(b->evk);
   b->release();
   if (b->stream) cudaStreamDestroy(b->stream);
   delete b;

@@ -43,6 +43,7 @@ struct Lead {
   // cache scalars (cache_tree.hpp:187-197)
   u64 used, cclock, pinned_pages, discarded, lookups, agent_steps, events, evict_calls,
       evicted;
+  u64 hit_pages, created_pages, refreshed_pages, evict_scanned, agent_events;
   double hit_m, hit_r;
   // controller (controller.hpp:117-126)
   double window, su, sh;
@@ -350,6 +351,11 @@ __device__ void finalize(const SimDev& D, Lead& L) {
   r->pool_used = L.used;
   r->hit_matched = L.hit_m;
   r->hit_requested = L.hit_r;
+  r->hit_pages = L.hit_pages;
+  r->created_pages = L.created_pages;
+  r->refreshed_pages = L.refreshed_pages;
+  r->evict_scanned = L.evict_scanned;
+  r->agent_events = L.agent_events;
   D.counts[0] = L.n_trace;
   D.counts[1] = L.n_log;
   D.counts[2] = static_cast<u64>(L.err);
@@ -367,6 +373,7 @@ __device__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.n_ready = 0;
   L.used = L.cclock = L.pinned_pages = L.discarded = L.lookups = 0;
   L.agent_steps = L.events = L.evict_calls = L.evicted = 0;
+  L.hit_pages = L.created_pages = L.refreshed_pages = L.evict_scanned = L.agent_events = 0;
   L.hit_m = L.hit_r = 0.0;
   L.n = D.n_agents;
   L.steps = D.n_steps;
@@ -496,6 +503,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           return;
         }
         L.ev_agent = agent;
+        ++L.agent_events;
         AgentDev& a = D.agents[agent];
         if (kind == EV_GEN) {  // on_generation_complete (engine.cpp:184-222)
           L.makespan = L.makespan < L.clock ? L.clock : L.makespan;
@@ -573,6 +581,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         L.pinned_pages += op.pin_up;
         const u64 matched = f * L.ps;
         L.lookups += f + (f < L.m_nctx ? 1 : 0);
+        L.hit_pages += f;
         L.hit_m += static_cast<double>(matched);
         L.hit_r += static_cast<double>(L.m_ctx0);
         log_rec(D, L, KVG_LOG_MATCH, L.m_id, matched, 0);
@@ -609,6 +618,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         }
         L.m_k = k;
         L.m_e = e;
+        L.evict_scanned += L.used;
         op.kind = OP_EVICT;
         op.k = k;
         op.evictable = e;
@@ -654,6 +664,8 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         if (op.err) fail(L, op.err);
         L.used += op.created;
         L.pinned_pages += op.pin_up;
+        L.created_pages += op.created;
+        if (L.m_nafter > 0) L.refreshed_pages += L.m_f;
         AgentDev& a = D.agents[L.m_id];
         const u64 stored = a.ctx - a.ctx % L.ps;
         const u64 matched = L.m_f * L.ps;

@@ -56,6 +56,7 @@ def lib():
                                    P(C.c_void_p)]
     L.kvg_batch_run.argtypes = [C.c_void_p]
     L.kvg_batch_last_ms.argtypes = [C.c_void_p, P(C.c_double)]
+    L.kvg_batch_timing.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double)]
     L.kvg_batch_result.argtypes = [C.c_void_p, C.c_size_t, P(abi.SimResult)]
     L.kvg_batch_trace.argtypes = [C.c_void_p, C.c_size_t, P(abi.TraceRow), C.c_size_t,
                                   P(C.c_size_t)]
@@ -162,6 +163,12 @@ class Batch:
         v = C.c_double()
         _check(lib().kvg_batch_last_ms(self.h, C.byref(v)))
         return v.value
+
+    def timing(self) -> tuple[float, float]:
+        """(step_ms, kernel_ms) of the last run, CUDA events on the launch stream."""
+        a, k = C.c_double(), C.c_double()
+        _check(lib().kvg_batch_timing(self.h, C.byref(a), C.byref(k)))
+        return a.value, k.value
 
     def result(self, i: int) -> dict:
         r = abi.SimResult()
