@@ -84,7 +84,8 @@ struct kvg_batch {
   size_t arena_bytes = 0;
   u64 tables_off = 0, tables_bytes = 0;
   std::vector<u64> off_plans, off_table, off_alt, off_occ, off_altocc, off_agents, off_pend,
-      off_paus, off_ready, off_batch, off_stats, off_trace, off_log;
+      off_paus, off_ready, off_batch, off_stats, off_trace, off_log, off_heap, off_rbits,
+      off_rl1, off_pinh, off_hist;
   kvg::SimDev* d_sims = nullptr;
   kvg_sim_result* d_results = nullptr;
   u64* d_counts = nullptr;
@@ -118,7 +119,8 @@ kvg_status layout_and_upload(kvg_batch* b) {
   resize(b->off_plans); resize(b->off_table); resize(b->off_alt); resize(b->off_occ);
   resize(b->off_altocc); resize(b->off_agents); resize(b->off_pend); resize(b->off_paus);
   resize(b->off_ready); resize(b->off_batch); resize(b->off_stats); resize(b->off_trace);
-  resize(b->off_log);
+  resize(b->off_log); resize(b->off_heap); resize(b->off_rbits); resize(b->off_rl1);
+  resize(b->off_pinh); resize(b->off_hist);
   // Region order: primary tables first so one memset initialises them all.
   u64 cur = 0;
   b->tables_off = 0;
@@ -144,6 +146,13 @@ kvg_status layout_and_upload(kvg_batch* b) {
     b->off_stats[i] = cur; cur += align_up(std::max<u64>(1, na) * sizeof(kvg_agent_stats));
     b->off_trace[i] = cur; cur += align_up(std::max<u64>(1, b->trace_cap[i]) * sizeof(kvg_trace_row));
     b->off_log[i] = cur; cur += align_up(std::max<u64>(1, b->log_cap[i]) * sizeof(kvg_log_record));
+    const u64 nwords = (na + 31) / 32;
+    b->off_heap[i] = cur; cur += align_up(std::max<u64>(1, na) * sizeof(kvg::HeapEnt));
+    b->off_rbits[i] = cur; cur += align_up(std::max<u64>(1, nwords) * sizeof(u32));
+    b->off_rl1[i] = cur; cur += align_up(std::max<u64>(1, (nwords + 31) / 32) * sizeof(u32));
+    const u64 sp = pop->shared_prompt ? pop->prompt_tokens / b->desc[i].engine.page_size : 0;
+    b->off_pinh[i] = cur; cur += align_up((sp + 1) * sizeof(u32) + (sp / 32 + 1) * sizeof(u32));
+    b->off_hist[i] = cur; cur += align_up(2 * 512 * sizeof(u32));
   }
   b->arena_bytes = cur;
   CUDA_TRY(cudaSetDevice(b->device));
@@ -179,6 +188,12 @@ kvg_status layout_and_upload(kvg_batch* b) {
     s.paus = reinterpret_cast<u32*>(base + b->off_paus[i]);
     s.ready = reinterpret_cast<u32*>(base + b->off_ready[i]);
     s.batch = reinterpret_cast<kvg::Member*>(base + b->off_batch[i]);
+    s.heap = reinterpret_cast<kvg::HeapEnt*>(base + b->off_heap[i]);
+    s.rbits = reinterpret_cast<u32*>(base + b->off_rbits[i]);
+    s.rl1 = reinterpret_cast<u32*>(base + b->off_rl1[i]);
+    s.pin_hist = reinterpret_cast<u32*>(base + b->off_pinh[i]);
+    s.pin_lvl = s.pin_hist + (s.shared_pages + 1);
+    s.hist = reinterpret_cast<u32*>(base + b->off_hist[i]);
     s.stats = reinterpret_cast<kvg_agent_stats*>(base + b->off_stats[i]);
     s.trace = reinterpret_cast<kvg_trace_row*>(base + b->off_trace[i]);
     s.trace_cap = b->trace_cap[i];
@@ -256,6 +271,16 @@ KVG_API kvg_status kvg_batch_create(int device, const kvg_sim_desc* sims, size_t
     std::string why;
     if (!kvg_host::validate_sim(sims[i], &why))
       return (kvg_status)set_error(KVG_ERR_CONFIG, "sim " + std::to_string(i) + ": " + why);
+    const kvg_population* pop = sims[i].population;
+    if (pop->agents >= (1u << kvg::kAgentBits))
+      return (kvg_status)set_error(KVG_ERR_CONFIG, "sim " + std::to_string(i) +
+                                                       ": more than 2^20-1 agents");
+    if (pop->steps > 65535)
+      return (kvg_status)set_error(KVG_ERR_CONFIG, "sim " + std::to_string(i) +
+                                                       ": more than 65535 steps per agent");
+    if (max_context_pages(pop, 1) >= (1ull << 32))
+      return (kvg_status)set_error(KVG_ERR_CONFIG, "sim " + std::to_string(i) +
+                                                       ": contexts beyond 2^32 tokens");
   }
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
@@ -503,7 +528,8 @@ KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity, uint64_t page
   const u64 tb = c->buckets * kvg::kChunk * sizeof(kvg::Slot);
   const u64 ob = align_up(c->buckets * sizeof(u32));
   c->victim_cap = 1 << 20;
-  const u64 bytes = 2 * tb + 2 * ob + align_up(sizeof(kvg::CacheState)) + sizeof(kvg::CacheDev) + 256;
+  const u64 bytes = 2 * tb + 2 * ob + align_up(sizeof(kvg::CacheState)) +
+                    align_up(sizeof(kvg::CacheDev)) + 2 * 512 * sizeof(u32) + 256;
   CUDA_TRY(cudaMalloc(&c->mem, bytes));
   CUDA_TRY(cudaMalloc(&c->d_victims, c->victim_cap * sizeof(kvg_victim)));
   CUDA_TRY(cudaMemset(c->mem, 0xff, 2 * tb));
@@ -517,10 +543,13 @@ KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity, uint64_t page
   c->h.alt_occ = reinterpret_cast<u32*>(p + 2 * tb + ob);
   c->d_state = reinterpret_cast<kvg::CacheState*>(p + 2 * tb + 2 * ob);
   c->d = reinterpret_cast<kvg::CacheDev*>(p + 2 * tb + 2 * ob + align_up(sizeof(kvg::CacheState)));
+  static_assert(sizeof(kvg::CacheDev) % 8 == 0, "layout");
   c->h.bucket_mask = static_cast<u32>(c->buckets - 1);
   c->h.victims = c->d_victims;
   c->h.victim_cap = c->victim_cap;
   c->h.state = reinterpret_cast<u64*>(c->d_state);
+  c->h.hist = reinterpret_cast<u32*>(p + 2 * tb + 2 * ob + align_up(sizeof(kvg::CacheState)) +
+                                     align_up(sizeof(kvg::CacheDev)));
   CUDA_TRY(cudaMemset(c->d_state, 0, sizeof(kvg::CacheState)));
   *out = c;
   return KVG_OK;

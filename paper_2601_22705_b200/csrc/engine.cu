@@ -16,8 +16,9 @@
 //              pin / create / free over an agent's page range (kernel 1),
 //      EVICT   shared-memory radix select over page last-use stamps plus a
 //              scatter that frees the chosen pages (kernel 2),
-//      ARGMIN  next agent event (per-agent event slots),
 //      REBUILD rehash of live buckets into the alternate table.
+//    The event heap, ready set and pin bookkeeping are leader-only O(log n) /
+//    O(1) structures (leader.cuh), so ticks and admissions never need the CTA.
 //  * tick signals (kernel 3) and the agent state machine (kernel 4) are
 //    leader-side O(1) steps fused into the same persistent kernel, because the
 //    reference's strictly sequential event order (engine.cpp:98-136) leaves no
@@ -65,10 +66,8 @@ enum OpKind : int {
   OP_EXIT,
   OP_RANGE,      // per-page work over an agent's page range
   OP_EVICT,      // radix select + scatter free
-  OP_ARGMIN,     // next agent event
   OP_REBUILD,    // rehash live buckets into the alternate table
   OP_SCANFREE,   // free pages by (owner, min index) over the whole table
-  OP_READY,      // ordered compaction of ready agents
 };
 
 enum RangeFlags : u32 {
@@ -103,6 +102,9 @@ struct Op {
   u32 flags;
   int pin_delta;
   int log_victims;      // 1: append victims to the log / victim list
+  int implicit_pins;    // engine mode: pins derived from per-agent pinned prefixes
+  u64 pin_max;          // engine mode: shared-prompt pages [0, pin_max) are pinned
+  const AgentDev* agents;
   u64 p0, p1;
   u64 stamp;
   u64 k;                // EVICT: pages needed
@@ -140,24 +142,20 @@ struct Op {
   unsigned long long* vic_n;
 };
 
-struct Red {  // warp-level reduction scratch
-  double t[32];
-  u64 o[32];
-  u32 a[32];
-};
-
 constexpr int kBins = 512;
 
+// Radix-select histogram. Lives in per-simulation global scratch (L2): it is
+// touched only by eviction selects, and keeping it out of shared memory leaves
+// the SM's unified L1 to the leader's hot agent records.
 struct Hist {
-  unsigned int cnt[kBins];
-  unsigned int dmax[kBins];
+  unsigned int* cnt;   // [kBins]
+  unsigned int* dmax;  // [kBins]
 };
 
-// Probe for chunk `tag`. Returns true and this lane's slot when present;
-// otherwise *bucket is the first empty bucket on the probe path.
-__device__ __forceinline__ bool probe(const Op& op, u64 tag, int lane, u32* bucket,
-                                      Slot* mine) {
-  u32 b = static_cast<u32>(hash64(tag)) & op.mask;
+// Continues a linear probe for chunk `tag` from bucket `b`. Returns true and
+// this lane's slot when present; otherwise *bucket is the first empty bucket.
+__device__ __forceinline__ bool probe_from(const Op& op, u64 tag, u32 b, int lane, u32* bucket,
+                                           Slot* mine) {
   for (;;) {
     Slot s = ld_slot(&op.table[(size_t)b * kChunk + lane]);
     u64 k0 = __shfl_sync(FULL, s.key, 0);
@@ -201,9 +199,73 @@ __device__ u32 claim(Op& op, Slot* table, u32* occ, unsigned int* occ_n, u32 mas
   }
 }
 
+struct RangeAcc {
+  unsigned int created, freed, up, down, resident;
+  u64 miss;
+  int err;
+};
+
+// Per-lane work on one 32-page chunk whose bucket probe already completed.
+__device__ __forceinline__ void range_chunk(Op& op, u64 tag, u64 lo, u64 hi, u32 b, Slot s,
+                                            bool found, int lane, RangeAcc& acc) {
+  const u32 flags = op.flags;
+  const int delta = op.pin_delta;
+  const u64 page = (tag & 0xffffffffull) + lane;
+  const bool in = page >= lo && page < hi;
+  if (!found && (flags & RF_CREATE) && __any_sync(FULL, in)) {
+    b = claim(op, op.table, op.occ, &op.occ_n, op.mask, tag, b, lane);
+    found = true;
+    s = Slot{tag + lane, 0};
+  }
+  if (!in) return;
+  const bool res = found && (s.meta & kResident);
+  Slot* slot = found ? &op.table[(size_t)b * kChunk + lane] : nullptr;
+  if (!res) {
+    if (flags & RF_CREATE) {
+      const u64 pins = delta > 0 ? static_cast<u64>(delta) : 0;
+      st_meta(slot, m_make(op.stamp, pins));
+      ++acc.created;
+      if (pins) ++acc.up;
+    } else {
+      acc.miss = page < acc.miss ? page : acc.miss;
+      if (flags & RF_STRICT) acc.err = E_PIN_MISSING;
+    }
+    return;
+  }
+  ++acc.resident;
+  const u64 m = s.meta;
+  if (flags & RF_FREE) {
+    if (!op.implicit_pins && m_pins(m) != 0) {
+      acc.err = E_DISCARD_PINNED;
+      return;
+    }
+    st_meta(slot, 0ull);
+    ++acc.freed;
+    return;
+  }
+  const u64 stamp = (flags & RF_STAMP) ? op.stamp : m_stamp(m);
+  long long pins = static_cast<long long>(m_pins(m));
+  if (flags & RF_PIN) {
+    long long np = pins + delta;
+    if (np < 0) {
+      acc.err = E_UNPIN_UNDERFLOW;
+      np = 0;
+    }
+    if (pins == 0 && np > 0) ++acc.up;
+    if (pins > 0 && np == 0) ++acc.down;
+    pins = np;
+  }
+  const u64 nm = m_make(stamp, static_cast<u64>(pins));
+  if (nm != m) st_meta(slot, nm);
+}
+
 // RANGE: agent `op.agent`, pages [p0, p1). Pages below shared_pages belong to
 // the shared prompt (owner 0), the rest to owner agent+1 (workload.cpp:167-171).
-// One 32-page chunk per warp iteration: one 512 B coalesced probe.
+// Each warp owns every nw-th 32-page chunk and keeps kProbeDepth bucket probes
+// in flight (one 512 B coalesced load each) before consuming any of them, so a
+// context of C chunks costs ~C/(nw*kProbeDepth) DRAM round trips, not C.
+constexpr int kProbeDepth = 8;
+
 __device__ void coop_range(Op& op, int warp, int lane, int nw) {
   const u64 p0 = op.p0, p1 = op.p1;
   if (p0 >= p1) return;
@@ -212,96 +274,111 @@ __device__ void coop_range(Op& op, int warp, int lane, int nw) {
   const u64 q_lo = p0 > S ? p0 : S, q_hi = p1;
   const u64 n_sh = s_lo < s_hi ? ((s_hi - 1) >> 5) - (s_lo >> 5) + 1 : 0;
   const u64 n_pr = q_lo < q_hi ? ((q_hi - 1) >> 5) - (q_lo >> 5) + 1 : 0;
-  const u32 flags = op.flags;
-  const int delta = op.pin_delta;
+  const u64 total = n_sh + n_pr;
   const u64 owner_priv = static_cast<u64>(op.agent) + 1;
-  unsigned int created = 0, freed = 0, up = 0, down = 0, resident = 0;
-  u64 miss = ~0ull;
-  int err = E_NONE;
-  for (u64 it = warp; it < n_sh + n_pr; it += nw) {
-    u64 owner, chunk, lo, hi;
-    if (it < n_sh) {
-      owner = 0; chunk = (s_lo >> 5) + it; lo = s_lo; hi = s_hi;
-    } else {
-      owner = owner_priv; chunk = (q_lo >> 5) + (it - n_sh); lo = q_lo; hi = q_hi;
+  RangeAcc acc{0, 0, 0, 0, 0, ~0ull, E_NONE};
+  auto tag_of = [&](u64 it) -> u64 {
+    return it < n_sh ? ((s_lo >> 5) + it) << 5
+                     : (owner_priv << 32) | (((q_lo >> 5) + (it - n_sh)) << 5);
+  };
+  for (u64 base = warp; base < total; base += static_cast<u64>(nw) * kProbeDepth) {
+    Slot s[kProbeDepth];
+    u32 b[kProbeDepth];
+#pragma unroll
+    for (int g = 0; g < kProbeDepth; ++g) {
+      const u64 it = base + static_cast<u64>(g) * nw;
+      if (it < total) {
+        b[g] = static_cast<u32>(hash64(tag_of(it))) & op.mask;
+        s[g] = ld_slot(&op.table[(size_t)b[g] * kChunk + lane]);
+      }
     }
-    const u64 tag = (owner << 32) | (chunk << 5);
-    const u64 page = (chunk << 5) + lane;
-    const bool in = page >= lo && page < hi;
-    u32 b;
-    Slot s{0, 0};
-    bool found = probe(op, tag, lane, &b, &s);
-    if (!found && (flags & RF_CREATE) && __any_sync(FULL, in)) {
-      b = claim(op, op.table, op.occ, &op.occ_n, op.mask, tag, b, lane);
-      found = true;
-      s = Slot{tag + lane, 0};
-    }
-    if (!in) continue;
-    const bool res = found && (s.meta & kResident);
-    Slot* slot = found ? &op.table[(size_t)b * kChunk + lane] : nullptr;
-    if (!res) {
-      if (flags & RF_CREATE) {
-        u64 pins = delta > 0 ? static_cast<u64>(delta) : 0;
-        st_meta(slot, m_make(op.stamp, pins));
-        ++created;
-        if (pins) ++up;
+#pragma unroll
+    for (int g = 0; g < kProbeDepth; ++g) {
+      const u64 it = base + static_cast<u64>(g) * nw;
+      if (it >= total) break;
+      const u64 tag = tag_of(it);
+      const u64 k0 = __shfl_sync(FULL, s[g].key, 0);
+      bool found;
+      if (k0 == tag) {
+        found = true;
+      } else if (k0 == kEmptyKey) {
+        found = false;
       } else {
-        miss = page < miss ? page : miss;
-        if (flags & RF_STRICT) err = E_PIN_MISSING;
+        found = probe_from(op, tag, (b[g] + 1) & op.mask, lane, &b[g], &s[g]);
       }
-      continue;
+      const bool shared = it < n_sh;
+      range_chunk(op, tag, shared ? s_lo : q_lo, shared ? s_hi : q_hi, b[g], s[g], found, lane,
+                  acc);
     }
-    ++resident;
-    u64 m = s.meta;
-    if (flags & RF_FREE) {
-      if (m_pins(m) != 0) {
-        err = E_DISCARD_PINNED;
-        continue;
-      }
-      st_meta(slot, 0ull);
-      ++freed;
-      continue;
-    }
-    u64 stamp = (flags & RF_STAMP) ? op.stamp : m_stamp(m);
-    long long pins = static_cast<long long>(m_pins(m));
-    if (flags & RF_PIN) {
-      long long np = pins + delta;
-      if (np < 0) {
-        err = E_UNPIN_UNDERFLOW;
-        np = 0;
-      }
-      if (pins == 0 && np > 0) ++up;
-      if (pins > 0 && np == 0) ++down;
-      pins = np;
-    }
-    u64 nm = m_make(stamp, static_cast<u64>(pins));
-    if (nm != m) st_meta(slot, nm);
   }
   // warp reductions, then one shared atomic per warp
   for (int o = 16; o > 0; o >>= 1) {
-    created += __shfl_down_sync(FULL, created, o);
-    freed += __shfl_down_sync(FULL, freed, o);
-    up += __shfl_down_sync(FULL, up, o);
-    down += __shfl_down_sync(FULL, down, o);
-    resident += __shfl_down_sync(FULL, resident, o);
-    u64 om = __shfl_down_sync(FULL, miss, o);
-    miss = om < miss ? om : miss;
-    int oe = __shfl_down_sync(FULL, err, o);
-    err = oe > err ? oe : err;
+    acc.created += __shfl_down_sync(FULL, acc.created, o);
+    acc.freed += __shfl_down_sync(FULL, acc.freed, o);
+    acc.up += __shfl_down_sync(FULL, acc.up, o);
+    acc.down += __shfl_down_sync(FULL, acc.down, o);
+    acc.resident += __shfl_down_sync(FULL, acc.resident, o);
+    const u64 om = __shfl_down_sync(FULL, acc.miss, o);
+    acc.miss = om < acc.miss ? om : acc.miss;
+    const int oe = __shfl_down_sync(FULL, acc.err, o);
+    acc.err = oe > acc.err ? oe : acc.err;
   }
   if (lane == 0) {
-    if (created) atomicAdd(&op.created, created);
-    if (freed) atomicAdd(&op.freed, freed);
-    if (up) atomicAdd(&op.pin_up, up);
-    if (down) atomicAdd(&op.pin_down, down);
-    if (resident) atomicAdd(&op.resident, resident);
-    if (miss != ~0ull) atomicMin(&op.first_miss, miss);
-    if (err) atomicMax(&op.err, err);
+    if (acc.created) atomicAdd(&op.created, acc.created);
+    if (acc.freed) atomicAdd(&op.freed, acc.freed);
+    if (acc.up) atomicAdd(&op.pin_up, acc.up);
+    if (acc.down) atomicAdd(&op.pin_down, acc.down);
+    if (acc.resident) atomicAdd(&op.resident, acc.resident);
+    if (acc.miss != ~0ull) atomicMin(&op.first_miss, acc.miss);
+    if (acc.err) atomicMax(&op.err, acc.err);
   }
 }
 
-__device__ __forceinline__ bool is_candidate(u64 m) {
-  return (m & kResident) && m_pins(m) == 0;
+// Visits every claimed bucket (the dense occupancy list), kScanDepth buckets in
+// flight per warp; f(bucket, slot, pin_threshold) runs per lane. With implicit
+// pins (engine mode) the bucket owner's pinned prefix length is fetched in the
+// same wave: page (owner, idx) is pinned iff idx < threshold.
+constexpr int kScanDepth = 4;
+
+template <typename F>
+__device__ __forceinline__ void scan_buckets(const Op& op, int warp, int lane, int nw, F&& f) {
+  const unsigned int n_occ = op.occ_n;
+  for (u32 base = warp; base < n_occ; base += static_cast<u32>(nw) * kScanDepth) {
+    u32 bk[kScanDepth];
+    Slot s[kScanDepth];
+    u64 thr[kScanDepth];
+#pragma unroll
+    for (int g = 0; g < kScanDepth; ++g) {
+      const u32 i = base + g * nw;
+      bk[g] = i < n_occ ? __ldcg(&op.occ[i]) : 0u;
+    }
+#pragma unroll
+    for (int g = 0; g < kScanDepth; ++g) {
+      const u32 i = base + g * nw;
+      if (i < n_occ) s[g] = ld_slot(&op.table[(size_t)bk[g] * kChunk + lane]);
+    }
+#pragma unroll
+    for (int g = 0; g < kScanDepth; ++g) {
+      const u32 i = base + g * nw;
+      thr[g] = 0;
+      if (i < n_occ && op.implicit_pins) {
+        const u64 owner = __shfl_sync(FULL, s[g].key, 0) >> 32;
+        thr[g] = owner == 0 ? op.pin_max : __ldcg(&op.agents[owner - 1].pinned_pg);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < kScanDepth; ++g) {
+      const u32 i = base + g * nw;
+      if (i < n_occ) f(bk[g], s[g], thr[g]);
+    }
+  }
+}
+
+// Eviction candidate: resident and unpinned (cache_tree.cpp:230-234 per page).
+__device__ __forceinline__ bool is_candidate(const Op& op, const Slot& s, u64 thr) {
+  if (!(s.meta & kResident)) return false;
+  if (op.implicit_pins) return (s.key & 0xffffffffull) >= thr;
+  return m_pins(s.meta) == 0;
 }
 
 __device__ __forceinline__ void emit_victim(Op& op, u64 key, u64 stamp, u32 agent) {
@@ -324,7 +401,7 @@ __device__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int lane, u64* rank
   const u32 base = lane * per;
   u32 local = 0;
   for (u32 i = 0; i < per; ++i)
-    if (base + i < nbins) local += h.cnt[base + i];
+    if (base + i < nbins) local += __ldcg(&h.cnt[base + i]);
   u32 incl = local;
   for (int o = 1; o < 32; o <<= 1) {
     u32 v = __shfl_up_sync(FULL, incl, o);
@@ -343,7 +420,7 @@ __device__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int lane, u64* rank
   if (lane == L) {
     u32 i = 0;
     for (; i + 1 < per; ++i) {
-      const u32 c = h.cnt[base + i];
+      const u32 c = __ldcg(&h.cnt[base + i]);
       if (cum + c >= need) break;
       cum += c;
     }
@@ -361,8 +438,9 @@ __device__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int lane, u64* rank
 
 // EVICT (cache_tree.cpp:270-319, per-page form SURVEY.md A.2): free the
 // op.k smallest (stamp asc, page index desc) resident unpinned pages.
-// Radix select over stamps (9-bit digits, smem histogram), exact stamp T and
-// the deepest-j cut inside it, then one scatter pass.
+// Radix select over stamps (9-bit digits, shared-memory histogram with
+// warp-aggregated atomics), exact threshold stamp T and the deepest-j cut
+// inside it (equal stamps lie on one root path), then one scatter pass.
 __device__ void coop_evict(Op& op, Hist& h, int tid, int warp, int lane, int nw) {
   const int nt = nw * 32;
   if (tid == 0) {
@@ -382,17 +460,14 @@ __device__ void coop_evict(Op& op, Hist& h, int tid, int warp, int lane, int nw)
       const bool last = shift == 0;
       const u32 nbins = 1u << d;
       for (u32 i = tid; i < nbins; i += nt) {
-        h.cnt[i] = 0;
-        h.dmax[i] = 0;
+        __stcg(&h.cnt[i], 0u);
+        __stcg(&h.dmax[i], 0u);
       }
       __syncthreads();
       const u64 prefix = op.prefix;
-      const unsigned int n_occ = op.occ_n;
-      for (u32 i = warp; i < n_occ; i += nw) {
-        const u32 b = __ldcg(&op.occ[i]);
-        const Slot s = ld_slot(&op.table[(size_t)b * kChunk + lane]);
+      scan_buckets(op, warp, lane, nw, [&](u32, const Slot& s, u64 thr) {
         const u64 st = m_stamp(s.meta);
-        const bool act = is_candidate(s.meta) && (st >> lo_bits) == prefix;
+        const bool act = is_candidate(op, s, thr) && (st >> lo_bits) == prefix;
         const u32 bin = act ? static_cast<u32>((st >> shift) & (nbins - 1)) : 0xffffffffu;
         const unsigned peers = __match_any_sync(FULL, bin);
         if (act) {
@@ -404,12 +479,12 @@ __device__ void coop_evict(Op& op, Hist& h, int tid, int warp, int lane, int nw)
             if (lane == leader) atomicMax(&h.dmax[bin], mx);
           }
         }
-      }
+      });
       __syncthreads();
       if (warp == 0) {
         u64 rank = 0;
         const u32 bin = select_bin(op, h, nbins, d, lane, &rank);
-        if (last && lane == 0) op.cut_depth = static_cast<u64>(h.dmax[bin]) + 1 - rank;
+        if (last && lane == 0) op.cut_depth = static_cast<u64>(__ldcg(&h.dmax[bin])) + 1 - rank;
       }
       __syncthreads();
       lo_bits = shift;
@@ -419,20 +494,16 @@ __device__ void coop_evict(Op& op, Hist& h, int tid, int warp, int lane, int nw)
   }
   // scatter-free pass
   unsigned int freed = 0;
-  const unsigned int n_occ = op.occ_n;
-  for (u32 i = warp; i < n_occ; i += nw) {
-    const u32 b = __ldcg(&op.occ[i]);
-    Slot* slot = &op.table[(size_t)b * kChunk + lane];
-    const Slot s = ld_slot(slot);
-    if (!is_candidate(s.meta)) continue;
+  scan_buckets(op, warp, lane, nw, [&](u32 b, const Slot& s, u64 thr) {
+    if (!is_candidate(op, s, thr)) return;
     const u64 st = m_stamp(s.meta);
     const u64 depth = s.key & 0xffffffffu;
     if (all || st < T || (st == T && depth >= cut)) {
-      st_meta(slot, 0ull);
+      st_meta(&op.table[(size_t)b * kChunk + lane], 0ull);
       ++freed;
       if (op.log_victims) emit_victim(op, s.key, st, op.agent);
     }
-  }
+  });
   for (int o = 16; o > 0; o >>= 1) freed += __shfl_down_sync(FULL, freed, o);
   if (lane == 0 && freed) atomicAdd(&op.freed, freed);
 }
@@ -442,22 +513,18 @@ __device__ void coop_evict(Op& op, Hist& h, int tid, int warp, int lane, int nw)
 __device__ void coop_scanfree(Op& op, int warp, int lane, int nw) {
   unsigned int freed = 0;
   int err = 0;
-  const unsigned int n_occ = op.occ_n;
-  for (u32 i = warp; i < n_occ; i += nw) {
-    const u32 b = __ldcg(&op.occ[i]);
-    Slot* slot = &op.table[(size_t)b * kChunk + lane];
-    const Slot s = ld_slot(slot);
-    if (!(s.meta & kResident)) continue;
+  scan_buckets(op, warp, lane, nw, [&](u32 b, const Slot& s, u64) {
+    if (!(s.meta & kResident)) return;
     const u64 owner = s.key >> 32, idx = s.key & 0xffffffffu;
-    if (idx < op.p0) continue;
-    if (op.owner_filter != ~0ull && owner != op.owner_filter) continue;
+    if (idx < op.p0) return;
+    if (op.owner_filter != ~0ull && owner != op.owner_filter) return;
     if (m_pins(s.meta)) {
       err = E_DISCARD_PINNED;
-      continue;
+      return;
     }
-    st_meta(slot, 0ull);
+    st_meta(&op.table[(size_t)b * kChunk + lane], 0ull);
     ++freed;
-  }
+  });
   for (int o = 16; o > 0; o >>= 1) {
     freed += __shfl_down_sync(FULL, freed, o);
     int oe = __shfl_down_sync(FULL, err, o);
@@ -470,7 +537,7 @@ __device__ void coop_scanfree(Op& op, int warp, int lane, int nw) {
 }
 
 // REBUILD: copy buckets holding at least one resident page into the
-// alternate table (pre-cleared), then the caller swaps tables.
+// alternate table (pre-cleared here), then swap tables.
 __device__ void coop_rebuild(Op& op, int tid, int warp, int lane, int nw) {
   const int nt = nw * 32;
   const size_t nslots = (static_cast<size_t>(op.mask) + 1) * kChunk;
@@ -500,75 +567,6 @@ __device__ void coop_rebuild(Op& op, int tid, int warp, int lane, int nw) {
     op.alt_occ = o;
     op.occ_n = op.alt_n;
   }
-}
-
-// ARGMIN over per-agent pending events by (time, ordinal).
-__device__ void coop_argmin(Op& op, Red& red, const AgentDev* ag, u32 n, int tid,
-                            int warp, int lane, int nw) {
-  const int nt = nw * 32;
-  double bt = 0;
-  u64 bo = ~0ull;
-  u32 ba = 0xffffffffu;
-  for (u32 i = tid; i < n; i += nt) {
-    const AgentDev* a = &ag[i];
-    uint8_t kind = *reinterpret_cast<const volatile uint8_t*>(&a->ev_kind);
-    if (kind == EV_NONE) continue;
-    double t = __ldcg(&a->ev_time);
-    u64 o = __ldcg(&a->ev_ord);
-    if (ba == 0xffffffffu || t < bt || (t == bt && o < bo)) {
-      bt = t; bo = o; ba = i;
-    }
-  }
-  for (int off = 16; off > 0; off >>= 1) {
-    double ot = __shfl_down_sync(FULL, bt, off);
-    u64 oo = __shfl_down_sync(FULL, bo, off);
-    u32 oa = __shfl_down_sync(FULL, ba, off);
-    if (oa != 0xffffffffu && (ba == 0xffffffffu || ot < bt || (ot == bt && oo < bo))) {
-      bt = ot; bo = oo; ba = oa;
-    }
-  }
-  if (lane == 0) {
-    red.t[warp] = bt;
-    red.o[warp] = bo;
-    red.a[warp] = ba;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double t = 0;
-    u64 o = ~0ull;
-    u32 a = 0xffffffffu;
-    for (int w = 0; w < nw; ++w) {
-      if (red.a[w] == 0xffffffffu) continue;
-      if (a == 0xffffffffu || red.t[w] < t || (red.t[w] == t && red.o[w] < o)) {
-        t = red.t[w]; o = red.o[w]; a = red.a[w];
-      }
-    }
-    op.amin_t = t;
-    op.amin_o = o;
-    op.amin_a = a;
-    op.amin_any = a != 0xffffffffu;
-  }
-}
-
-// READY: ids of active agents awaiting admission, ascending (engine.cpp:306-310).
-__device__ void coop_ready(Op& op, const AgentDev* ag, u32 n, u32* out, int tid, int warp,
-                           int lane, int nw) {
-  // one warp walks the agents in id order with ballots; others idle (n is
-  // small relative to the work of the dispatch that follows)
-  if (warp != 0) return;
-  u32 count = 0;
-  for (u32 base = 0; base < n; base += 32) {
-    u32 i = base + lane;
-    bool r = false;
-    if (i < n) {
-      const volatile AgentDev* a = &ag[i];
-      r = a->in_active && a->state == S_AWAIT;
-    }
-    unsigned m = __ballot_sync(FULL, r);
-    if (r) out[count + __popc(m & ((1u << lane) - 1))] = i;
-    count += __popc(m);
-  }
-  if (lane == 0) op.created = count;
 }
 
 }  // namespace kvg

@@ -38,19 +38,30 @@ struct Slot {
 enum AgentState : uint8_t { S_PENDING, S_AWAIT, S_GEN, S_TOOL, S_PAUSED, S_DONE };
 enum EventKind : uint8_t { EV_NONE = 0, EV_GEN = 1, EV_TOOL = 2, EV_XFER = 3 };
 
-struct AgentDev {     // 96 B
-  double ev_time;     // pending event (valid when ev_kind != EV_NONE)
-  u64 ev_ord;
+struct AgentDev {     // 64 B: two agents per 128 B line
   u64 ctx;            // context length in tokens
   u64 high_water;
-  u64 pinned;         // pinned_len (tokens)
   double ready_since;
-  u64 f_gen, f_rec, f_obs;  // InFlight (engine.cpp:71-77)
-  double f_tool;
-  u32 step;
+  double f_tool;      // InFlight (engine.cpp:71-77)
+  u32 pinned_pg;      // pinned_len / page_size: pages [0, pinned_pg) of this
+                      // agent's path carry its pin (implicit per-page pins)
+  u32 f_gen, f_rec, f_obs;
+  u32 act_seq;        // admission order: active_ is insertion ordered
+                      // (controller.hpp:122); larger = newer
+  u32 pad0;
+  uint16_t step;
   uint8_t state, ev_kind, f_has_tool, in_active;
-  u32 next, prev;     // active-list links (insertion order)
+  uint8_t ready;      // mirror of this agent's bit in the ready bitmap
+  uint8_t pad;
 };
+static_assert(sizeof(AgentDev) == 64, "AgentDev must stay 64 B");
+
+// Event heap entry: (time, ordinal) lexicographic; key = ordinal << 20 | agent.
+struct HeapEnt {
+  double t;
+  u64 k;
+};
+constexpr int kAgentBits = 20;  // <= 1,048,575 agents per simulation
 
 struct Member {       // one dispatched batch member (engine.cpp:293-299)
   u32 id, pad;
@@ -79,8 +90,14 @@ struct SimDev {
   AgentDev* agents;
   u32* pend;
   u32* paus;
-  u32* ready;
+  u32* ready;         // unused (kept for layout stability)
   Member* batch;
+  HeapEnt* heap;      // agent events (leader-only binary heap)
+  u32* rbits;         // ready bitmap: in_active && AwaitingAdmission
+  u32* rl1;           // second level: non-empty words of rbits
+  u32* pin_hist;      // [shared_pages+1]: agents per shared-pin depth
+  u32* pin_lvl;       // bitmap of non-empty pin_hist levels
+  u32* hist;          // [2 * 512]: eviction radix-select histogram scratch
   // ---- outputs
   kvg_agent_stats* stats;
   kvg_trace_row* trace;
@@ -105,6 +122,7 @@ struct CacheDev {
   kvg_victim* victims;  // appended per op (unordered within an op; host sorts)
   u64 victim_cap;
   u64* state;           // persistent scalars across exec calls (see CacheState)
+  u32* hist;            // [2 * 512] eviction histogram scratch
 };
 
 // Persistent cache scalars for the cache-op executor.

@@ -4,6 +4,18 @@
 // function below cites the reference lines it follows. Whenever page-level
 // work is needed it posts a cooperative op (engine.cu) and returns; the CTA
 // executes the op and thread 0 resumes at the continuation phase.
+//
+// Leader-only structures (no CTA involvement, L1-resident for small sims):
+//   * agent events: binary min-heap of (time, ordinal, agent) — equivalent to
+//     the reference's priority queue since an agent has at most one pending
+//     event; tick and admission are two scalar slots;
+//   * ready set: two-level bitmap of (active && AwaitingAdmission) agents,
+//     iterated in id order exactly like dispatch_batch's sorted vector;
+//   * pins: each agent holds at most one pin, on its own root prefix
+//     [0, pinned_len) (engine.cpp:340-342, 374-377). The pin count of private
+//     page (a, k) is [k < pinned_pg(a)] and of shared page k is
+//     #{a : pinned_pg(a) > k}; only the prefix max matters for eviction, kept
+//     with a histogram. No page-table pass is ever spent on pin/unpin.
 #pragma once
 
 namespace kvg {
@@ -11,21 +23,16 @@ namespace kvg {
 constexpr u32 NIL = 0xffffffffu;
 
 enum Phase : int {
-  PH_INIT = 0,
-  PH_EVENT,
-  PH_ARGMIN_DONE,
-  PH_ADM_READY,
+  PH_EVENT = 0,
   PH_MEMBER,
   PH_M_MATCHED,
   PH_M_INSERT,
   PH_M_EVICTED,
   PH_M_COMMIT,
-  PH_M_REBUILT,
   PH_M_CREATED,
   PH_M_FAIL,
   PH_M_RESTORED,
   PH_BATCH_END,
-  PH_GEN_UNPINNED,
   PH_GEN_DISCARDED,
   PH_DONE,
   PH_EXITED,
@@ -36,30 +43,28 @@ struct Lead {
   // event queue (engine.cpp:46-68, 139-154)
   double clock, gpu_busy, makespan, device_busy, tick_t, adm_t;
   u64 ord, tick_o, adm_o;
-  int tick_on, adm_on, amin_valid, amin_any;
-  double amin_t;
-  u64 amin_o;
-  u32 amin_a, finished, n_ready, ev_agent;
+  int tick_on, adm_on;
+  u32 hsize, finished, n_ready, ev_agent;
   // cache scalars (cache_tree.hpp:187-197)
-  u64 used, cclock, pinned_pages, discarded, lookups, agent_steps, events, evict_calls,
-      evicted;
+  u64 used, cclock, discarded, lookups, agent_steps, events, evict_calls, evicted;
+  u64 pin_max, pin_priv;  // implicit pins: shared prefix max, private pinned pages
   u64 hit_pages, created_pages, refreshed_pages, evict_scanned, agent_events;
   double hit_m, hit_r;
   // controller (controller.hpp:117-126)
   double window, su, sh;
   int have_s, gated;
   u64 ticks;
-  u32 act_head, act_tail, act_size, pend_head, pend_size, paus_head, paus_size, pad0;
+  u32 act_seq, act_size, pend_head, pend_size, paus_head, paus_size, nwords, pad2;
   // metrics
   u64 decoded_cum, rec_cum;
   kvg_ledger ledger;
   unsigned long long n_trace, n_log;
   // dispatch context
-  u32 nready, ready_i, batch_n, m_id;
+  u32 batch_n, m_id, m_next, pad1;
   u64 m_ctx0, m_f, m_nctx, m_nafter, m_now, m_k, m_e;
   // config snapshot
   double interval, decay, horizon, capacity_d;
-  u64 capacity, ps, shared_len;
+  u64 capacity, ps, shared_len, S;
   u32 n, steps, kind, cap;
   kvg_controller_config cfg;
 };
@@ -90,30 +95,64 @@ __device__ __forceinline__ void fail(Lead& L, int code) {
   L.status = KVG_ERR_STATE;
 }
 
-// AgentRecord::set_state (workload.cpp:130-137) + ready-count upkeep.
+// ready bitmap: bit a <=> agent a is active and AwaitingAdmission
+__device__ __forceinline__ void ready_sync(const SimDev& D, Lead& L, AgentDev& a, u32 id) {
+  const uint8_t want = a.in_active && a.state == S_AWAIT;
+  if (want == a.ready) return;
+  a.ready = want;
+  const u32 w = id >> 5, bit = 1u << (id & 31);
+  u32 v = D.rbits[w];
+  if (want) {
+    if (v == 0) D.rl1[w >> 5] |= 1u << (w & 31);
+    D.rbits[w] = v | bit;
+    ++L.n_ready;
+  } else {
+    v &= ~bit;
+    D.rbits[w] = v;
+    if (v == 0) D.rl1[w >> 5] &= ~(1u << (w & 31));
+    --L.n_ready;
+  }
+}
+
+// smallest ready agent id >= from, or NIL
+__device__ __forceinline__ u32 ready_next(const SimDev& D, const Lead& L, u32 from) {
+  if (from >= L.n) return NIL;
+  const u32 w = from >> 5;
+  const u32 bits = D.rbits[w] & (~0u << (from & 31));
+  if (bits) return (w << 5) + __ffs(bits) - 1;
+  for (u32 w1 = w + 1; w1 < L.nwords;) {
+    const u32 m = D.rl1[w1 >> 5] & (~0u << (w1 & 31));
+    if (m) {
+      const u32 ww = ((w1 >> 5) << 5) + __ffs(m) - 1;
+      return (ww << 5) + __ffs(D.rbits[ww]) - 1;
+    }
+    w1 = ((w1 >> 5) + 1) << 5;
+  }
+  return NIL;
+}
+
+// AgentRecord::set_state (workload.cpp:130-137)
 __device__ __forceinline__ void set_state(const SimDev& D, Lead& L, u32 id, uint8_t s) {
   AgentDev& a = D.agents[id];
   if (!legal_edge(a.state, s)) {
     fail(L, E_ILLEGAL_TRANSITION);
     return;
   }
-  if (a.in_active) {
-    if (a.state == S_AWAIT) --L.n_ready;
-    if (s == S_AWAIT) ++L.n_ready;
-  }
   a.state = s;
+  ready_sync(D, L, a, id);
 }
 
+// active_ is an insertion-ordered vector in the reference (controller.hpp:122).
+// Only its size and "the newest member at a step boundary" (the pause victim,
+// controller.cpp:130-136) are ever needed, so membership is a flag plus an
+// admission sequence number; the victim is the ready agent (active and
+// AwaitingAdmission = at_boundary) with the largest sequence number.
 __device__ __forceinline__ void act_push(const SimDev& D, Lead& L, u32 id) {
   AgentDev& a = D.agents[id];
   a.in_active = 1;
-  a.next = NIL;
-  a.prev = L.act_tail;
-  if (L.act_tail != NIL) D.agents[L.act_tail].next = id;
-  else L.act_head = id;
-  L.act_tail = id;
+  a.act_seq = ++L.act_seq;
   ++L.act_size;
-  if (a.state == S_AWAIT) ++L.n_ready;
+  ready_sync(D, L, a, id);
 }
 
 __device__ __forceinline__ bool act_erase(const SimDev& D, Lead& L, u32 id) {
@@ -122,39 +161,82 @@ __device__ __forceinline__ bool act_erase(const SimDev& D, Lead& L, u32 id) {
     fail(L, E_NOT_ACTIVE);
     return false;
   }
-  if (a.prev != NIL) D.agents[a.prev].next = a.next;
-  else L.act_head = a.next;
-  if (a.next != NIL) D.agents[a.next].prev = a.prev;
-  else L.act_tail = a.prev;
   a.in_active = 0;
   --L.act_size;
-  if (a.state == S_AWAIT) --L.n_ready;
+  ready_sync(D, L, a, id);
   return true;
 }
 
+// newest active agent at a step boundary, or NIL
+__device__ __forceinline__ u32 pause_victim(const SimDev& D, const Lead& L) {
+  if (L.n_ready == 0) return NIL;
+  u32 best = NIL, best_seq = 0;
+  for (u32 id = ready_next(D, L, 0); id != NIL; id = ready_next(D, L, id + 1)) {
+    const u32 q = D.agents[id].act_seq;
+    if (best == NIL || q > best_seq) {
+      best = id;
+      best_seq = q;
+    }
+  }
+  return best;
+}
+
+// FIFO rings for pending_ and paused_ (controller.hpp:123-124); an agent is
+// in at most one of active/pending/paused, so capacity n suffices.
+__device__ __forceinline__ u32 ring_at(u32 head, u32 k, u32 n) {
+  u32 i = head + k;
+  return i >= n ? i - n : i;
+}
 __device__ __forceinline__ void pend_push(const SimDev& D, Lead& L, u32 id) {
-  D.pend[(L.pend_head + L.pend_size) % L.n] = id;
+  D.pend[ring_at(L.pend_head, L.pend_size, L.n)] = id;
   ++L.pend_size;
 }
 __device__ __forceinline__ u32 pend_pop(const SimDev& D, Lead& L) {
   u32 id = D.pend[L.pend_head];
-  L.pend_head = (L.pend_head + 1) % L.n;
+  L.pend_head = ring_at(L.pend_head, 1, L.n);
   --L.pend_size;
   return id;
 }
 __device__ __forceinline__ void paus_push(const SimDev& D, Lead& L, u32 id) {
-  D.paus[(L.paus_head + L.paus_size) % L.n] = id;
+  D.paus[ring_at(L.paus_head, L.paus_size, L.n)] = id;
   ++L.paus_size;
 }
 __device__ __forceinline__ u32 paus_pop(const SimDev& D, Lead& L) {
   u32 id = D.paus[L.paus_head];
-  L.paus_head = (L.paus_head + 1) % L.n;
+  L.paus_head = ring_at(L.paus_head, 1, L.n);
   --L.paus_size;
   return id;
 }
 
-// Engine::schedule for agent events (engine.cpp:143-145); keeps the cached
-// minimum current so ticks never need a rescan.
+// Implicit pins: agent `id` now pins its path prefix [0, tokens).
+__device__ __forceinline__ void set_pinned(const SimDev& D, Lead& L, u32 id, u64 tokens) {
+  AgentDev& a = D.agents[id];
+  const u64 old_pg = a.pinned_pg, new_pg = tokens / L.ps;
+  a.pinned_pg = static_cast<u32>(new_pg);
+  if (old_pg == new_pg) return;
+  const u64 S = L.S;
+  L.pin_priv += (new_pg > S ? new_pg - S : 0);
+  L.pin_priv -= (old_pg > S ? old_pg - S : 0);
+  if (S == 0) return;
+  const u64 jo = old_pg < S ? old_pg : S, jn = new_pg < S ? new_pg : S;
+  if (jo == jn) return;
+  if (jo > 0 && --D.pin_hist[jo] == 0) D.pin_lvl[jo >> 5] &= ~(1u << (jo & 31));
+  if (jn > 0 && D.pin_hist[jn]++ == 0) D.pin_lvl[jn >> 5] |= 1u << (jn & 31);
+  if (jn > L.pin_max) {
+    L.pin_max = jn;
+  } else if (jo == L.pin_max && D.pin_hist[jo] == 0) {
+    u64 w = jo >> 5;  // highest non-empty level below jo
+    u32 bits = D.pin_lvl[w] & ((1u << (jo & 31)) - 1);
+    while (bits == 0 && w > 0) bits = D.pin_lvl[--w];
+    L.pin_max = bits ? (w << 5) + 31 - __clz(bits) : 0;
+  }
+}
+
+__device__ __forceinline__ bool heap_less(const HeapEnt& x, const HeapEnt& y) {
+  return x.t < y.t || (x.t == y.t && x.k < y.k);
+}
+
+// Engine::schedule for agent events (engine.cpp:143-145)
 __device__ __forceinline__ void sched_agent(const SimDev& D, Lead& L, u32 id, double t,
                                             uint8_t kind) {
   AgentDev& a = D.agents[id];
@@ -162,16 +244,43 @@ __device__ __forceinline__ void sched_agent(const SimDev& D, Lead& L, u32 id, do
     fail(L, E_EVENT_BUSY);
     return;
   }
-  const u64 o = L.ord++;
-  a.ev_time = t;
-  a.ev_ord = o;
   a.ev_kind = kind;
-  if (L.amin_valid && (!L.amin_any || t < L.amin_t || (t == L.amin_t && o < L.amin_o))) {
-    L.amin_any = 1;
-    L.amin_t = t;
-    L.amin_o = o;
-    L.amin_a = id;
+  const HeapEnt e{t, (L.ord++ << kAgentBits) | id};
+  HeapEnt* h = D.heap;
+  u32 i = L.hsize++;
+  while (i > 0) {
+    const u32 p = (i - 1) >> 1;
+    const HeapEnt pe = h[p];
+    if (!heap_less(e, pe)) break;
+    h[i] = pe;
+    i = p;
   }
+  h[i] = e;
+}
+
+__device__ __forceinline__ void heap_pop(const SimDev& D, Lead& L) {
+  HeapEnt* h = D.heap;
+  const u32 n = --L.hsize;
+  if (n == 0) return;
+  const HeapEnt last = h[n];
+  u32 i = 0;
+  for (;;) {
+    const u32 l = 2 * i + 1;
+    if (l >= n) break;
+    u32 c = l;
+    HeapEnt ce = h[l];
+    if (l + 1 < n) {
+      const HeapEnt re = h[l + 1];
+      if (heap_less(re, ce)) {
+        c = l + 1;
+        ce = re;
+      }
+    }
+    if (!heap_less(ce, last)) break;
+    h[i] = ce;
+    i = c;
+  }
+  h[i] = last;
 }
 
 // Engine::schedule_admission (engine.cpp:149-154)
@@ -257,7 +366,7 @@ __device__ __forceinline__ u64 range_chunks(u64 p0, u64 p1) {
 
 // ------------------------------------------------------------ the handlers
 
-// Engine::on_control_tick (engine.cpp:245-266) — kernel-3 signals.
+// Engine::on_control_tick (engine.cpp:245-266) — the kernel-3 signal step.
 __device__ void on_tick(const SimDev& D, Lead& L) {
   const double usage = static_cast<double>(L.used) / L.capacity_d;
   const double m = L.hit_m, r = L.hit_r;
@@ -288,13 +397,14 @@ __device__ void on_tick(const SimDev& D, Lead& L) {
 }
 
 // Controller::admission_pass (controller.cpp:124-160) with the commands
-// applied as Engine::on_admission_check does (engine.cpp:268-291).
+// applied as Engine::on_admission_check does (engine.cpp:268-291). Commands
+// can be applied immediately: pausing only removes agents from active_ and
+// happens before any admit, which never reads agent state.
 __device__ void admission_pass(const SimDev& D, Lead& L) {
   const u64 limit = adm_limit(L);
   if (L.gated) {
     while (L.act_size > limit) {
-      u32 id = L.act_tail;
-      while (id != NIL && D.agents[id].state != S_AWAIT) id = D.agents[id].prev;
+      const u32 id = pause_victim(D, L);
       if (id == NIL) break;
       act_erase(D, L, id);
       paus_push(D, L, id);
@@ -367,15 +477,16 @@ __device__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.rebuilt = 0;
   L.clock = L.gpu_busy = L.makespan = L.device_busy = 0.0;
   L.ord = 0;
-  L.amin_valid = 1;
-  L.amin_any = 0;
+  L.hsize = 0;
   L.finished = 0;
   L.n_ready = 0;
-  L.used = L.cclock = L.pinned_pages = L.discarded = L.lookups = 0;
+  L.used = L.cclock = L.discarded = L.lookups = 0;
   L.agent_steps = L.events = L.evict_calls = L.evicted = 0;
+  L.pin_max = L.pin_priv = 0;
   L.hit_pages = L.created_pages = L.refreshed_pages = L.evict_scanned = L.agent_events = 0;
   L.hit_m = L.hit_r = 0.0;
   L.n = D.n_agents;
+  L.nwords = (D.n_agents + 31) / 32;
   L.steps = D.n_steps;
   L.kind = D.policy.kind;
   L.cap = D.policy.cap;
@@ -390,7 +501,7 @@ __device__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.su = L.sh = 0.0;
   L.have_s = 0;
   L.ticks = 0;
-  L.act_head = L.act_tail = NIL;
+  L.act_seq = 0;
   L.act_size = 0;
   L.pend_head = 0;
   L.pend_size = L.n;  // every agent starts pending (engine.cpp:89-93)
@@ -406,6 +517,7 @@ __device__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.capacity_d = static_cast<double>(D.engine.capacity);
   L.ps = D.engine.page_size;
   L.shared_len = D.shared_len;
+  L.S = D.shared_pages;
   // Engine::run: admission check at t=0 (ordinal 0), first tick (ordinal 1)
   L.adm_on = 1;
   L.adm_t = 0.0;
@@ -429,7 +541,138 @@ __device__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   op.vic_cap = 0;
   op.vic_n = nullptr;
   op.log_victims = D.log != nullptr;
+  op.implicit_pins = 1;
+  op.pin_max = 0;
+  op.agents = D.agents;
   L.phase = PH_EVENT;
+}
+
+// Fast path for the dominant event stream of a controlled run: control ticks
+// and admission checks that change nothing (C2 has
+// 760K of them against 32K agent events). Processes them with the hot state in
+// registers until the next event that needs the general path: an agent event,
+// an admission check that would admit / resume / pause / dispatch, the horizon,
+// or the end of the run. Same arithmetic, same order as on_tick /
+// on_admission_check (engine.cpp:245-291, controller.cpp:67-160).
+__device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
+  if (L.finished == L.n || L.status != KVG_OK) return;
+  const double t_agent = L.hsize > 0 ? D.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
+  const double horizon = L.horizon;
+  // state that no housekeeping event can change
+  const bool nready0 = L.n_ready == 0;
+  const u64 act = L.act_size;
+  const bool admit_src = L.pend_size > 0 || (L.gated && L.paus_size > 0);
+  const u32 kind = L.kind;
+  const double usage = static_cast<double>(L.used) / L.capacity_d;
+  const double decay = L.decay, interval = L.interval;
+  const u64 pending = static_cast<u64>(L.pend_size) + L.paus_size;
+  const u64 dec = L.decoded_cum, rec = L.rec_cum;
+  const u64 trace_cap = D.trace_cap;
+  kvg_trace_row* const trace = D.trace;
+  const kvg_controller_config c = L.cfg;
+  // evolving state
+  double clock = L.clock, tick_t = L.tick_t, adm_t = L.adm_t;
+  double hit_m = L.hit_m, hit_r = L.hit_r, window = L.window, su = L.su, sh = L.sh;
+  int have_s = L.have_s, tick_on = L.tick_on, adm_on = L.adm_on;
+  u64 ord = L.ord, tick_o = L.tick_o, adm_o = L.adm_o, events = L.events, ticks = L.ticks;
+  unsigned long long n_trace = L.n_trace;
+  for (;;) {
+    // next housekeeping event, if it precedes every agent event (rank 0)
+    bool tick;
+    if (tick_on && (!adm_on || tick_t <= adm_t)) {
+      if (!(tick_t < t_agent)) break;
+      tick = true;
+    } else if (adm_on) {
+      if (!(adm_t < t_agent)) break;
+      tick = false;
+    } else {
+      break;
+    }
+    const double bt = tick ? tick_t : adm_t;
+    if (bt > horizon) break;
+    if (tick) {
+      clock = bt;
+      tick_on = 0;
+      const double m = hit_m, r = hit_r;
+      const double hit = r > 0 ? m / r : 1.0;
+      ++ticks;  // Controller::update_window
+      if (kind == KVG_POLICY_AIMD) {
+        double u = usage, h = hit;
+        if (c.signal_smoothing > 0) {
+          if (have_s) {
+            u = c.signal_smoothing * su + (1 - c.signal_smoothing) * usage;
+            h = c.signal_smoothing * sh + (1 - c.signal_smoothing) * hit;
+          }
+          su = u;
+          sh = h;
+          have_s = 1;
+        }
+        double w = window;
+        if (u < c.u_low)
+          w = w + c.alpha;
+        else if (u > c.u_high && h < c.h_thresh)
+          w = w * c.beta;
+        window = w < c.w_min ? c.w_min : (c.w_max < w ? c.w_max : w);
+      }
+      const unsigned long long i = n_trace++;
+      if (i < trace_cap) {
+        kvg_trace_row row;
+        row.time = clock;
+        row.usage = usage;
+        row.hit_rate = hit;
+        row.window = kind == KVG_POLICY_AIMD ? window
+                     : kind == KVG_POLICY_UNCONTROLLED ? static_cast<double>(L.n)
+                                                       : static_cast<double>(L.cap);
+        row.active = act;
+        row.pending = pending;
+        row.decoded_cum = dec;
+        row.recompute_cum = rec;
+        row.transfers = 0;
+        row.hit_matched = m;
+        row.hit_requested = r;
+        trace[i] = row;
+      }
+      hit_m = m * decay;
+      hit_r = r * decay;
+      tick_on = 1;
+      tick_t = clock + interval;
+      tick_o = ord++;
+      if (!(adm_on && adm_t == clock)) {  // schedule_admission
+        if (adm_on) break;                // cannot happen; general path reports it
+        adm_on = 1;
+        adm_t = clock;
+        adm_o = ord++;
+      }
+      ++events;
+    } else {
+      const u64 limit = kind == KVG_POLICY_UNCONTROLLED ? ~0ull
+                        : kind == KVG_POLICY_AIMD ? static_cast<u64>(floor(window))
+                                                  : static_cast<u64>(L.cap);
+      // nothing ready => no pause victim and nothing to dispatch
+      const bool noop = nready0 && !(act < limit && admit_src);
+      if (!noop) break;  // the general path runs the real admission pass
+      clock = bt;
+      adm_on = 0;
+      ++events;
+    }
+  }
+  L.clock = clock;
+  L.tick_t = tick_t;
+  L.adm_t = adm_t;
+  L.hit_m = hit_m;
+  L.hit_r = hit_r;
+  L.window = window;
+  L.su = su;
+  L.sh = sh;
+  L.have_s = have_s;
+  L.tick_on = tick_on;
+  L.adm_on = adm_on;
+  L.ord = ord;
+  L.tick_o = tick_o;
+  L.adm_o = adm_o;
+  L.events = events;
+  L.ticks = ticks;
+  L.n_trace = n_trace;
 }
 
 // Runs the state machine until a cooperative op is posted in `op`.
@@ -441,26 +684,21 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
     switch (L.phase) {
       // ------------------------------------------------ event loop (98-136)
       case PH_EVENT: {
-        if (!L.amin_valid) {
-          op.kind = OP_ARGMIN;
-          L.phase = PH_ARGMIN_DONE;
-          return;
-        }
-        int which = -1;  // 0 agent, 1 tick, 2 admission
+        fast_housekeeping(D, L);
+        int which = -1;  // 0 agent, 1 tick, 2 admission (the event ranks)
         double bt = 0;
-        u64 bo = 0;
-        if (L.amin_any) {
+        if (L.hsize > 0) {
           which = 0;
-          bt = L.amin_t;
-          bo = L.amin_o;
+          bt = D.heap[0].t;
         }
-        if (L.tick_on && (which < 0 || L.tick_t < bt || (L.tick_t == bt && (which > 1 ||
-                                                                           (which == 1 && L.tick_o < bo))))) {
-          which = 1; bt = L.tick_t; bo = L.tick_o;
+        // ranks break time ties: completions, then the tick, then admission
+        if (L.tick_on && (which < 0 || L.tick_t < bt)) {
+          which = 1;
+          bt = L.tick_t;
         }
-        if (L.adm_on && (which < 0 || L.adm_t < bt || (L.adm_t == bt && (which > 2 ||
-                                                                         (which == 2 && L.adm_o < bo))))) {
-          which = 2; bt = L.adm_t; bo = L.adm_o;
+        if (L.adm_on && (which < 0 || L.adm_t < bt)) {
+          which = 2;
+          bt = L.adm_t;
         }
         if (which < 0) {
           if (L.finished != L.n) fail(L, E_DRAINED);
@@ -470,10 +708,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         u32 agent = 0;
         uint8_t kind = EV_NONE;
         if (which == 0) {
-          agent = L.amin_a;
+          agent = static_cast<u32>(D.heap[0].k & ((1u << kAgentBits) - 1));
+          heap_pop(D, L);
           kind = D.agents[agent].ev_kind;
           D.agents[agent].ev_kind = EV_NONE;
-          L.amin_valid = 0;
         } else if (which == 1) {
           L.tick_on = 0;
         } else {
@@ -497,24 +735,56 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
             ++L.events;
             continue;
           }
-          op.kind = OP_READY;
-          op.created = 0;
-          L.phase = PH_ADM_READY;
-          return;
+          L.batch_n = 0;
+          L.m_next = ready_next(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
+          L.phase = PH_MEMBER;
+          continue;
         }
         L.ev_agent = agent;
         ++L.agent_events;
         AgentDev& a = D.agents[agent];
         if (kind == EV_GEN) {  // on_generation_complete (engine.cpp:184-222)
           L.makespan = L.makespan < L.clock ? L.clock : L.makespan;
-          if (a.pinned > 0) {
-            post_range(op, agent, 0, a.pinned / L.ps, RF_PIN | RF_STRICT, -1, 0);
-            L.phase = PH_GEN_UNPINNED;
-            return;
+          set_pinned(D, L, agent, 0);  // unpin(pinned_len) — implicit pins
+          kvg_agent_stats& st = D.stats[agent];
+          L.decoded_cum += a.f_gen;
+          L.rec_cum += a.f_rec;
+          st.generated_tokens += a.f_gen;
+          st.recompute_tokens += a.f_rec;
+          if (a.f_rec > 0) ++st.recompute_events;
+          ++a.step;
+          if (a.step >= L.steps) {
+            set_state(D, L, agent, S_DONE);
+            // discard_suffix(context, shared_len) (cache_tree.cpp:404-437):
+            // page_ceil(shared_len) keeps a straddling page (quirk Q2)
+            const u64 fp = (L.shared_len + L.ps - 1) / L.ps;
+            const u64 np = a.ctx / L.ps;
+            if (fp * L.ps < a.ctx && fp < np) {
+              post_range(op, agent, fp, np, RF_FREE, 0, 0);
+              L.phase = PH_GEN_DISCARDED;
+              return;
+            }
+            op.freed = 0;
+            op.err = E_NONE;
+            L.phase = PH_GEN_DISCARDED;
+            continue;
           }
-          op.pin_down = 0;
-          op.err = E_NONE;
-          L.phase = PH_GEN_UNPINNED;
+          const bool req = L.kind == KVG_POLICY_REQUEST_CAP;
+          if (a.f_has_tool) {
+            set_state(D, L, agent, S_TOOL);
+            L.ledger.tool_wait += a.f_tool;
+            if (req) act_erase(D, L, agent);
+            sched_agent(D, L, agent, L.clock + a.f_tool, EV_TOOL);
+          } else {
+            set_state(D, L, agent, S_AWAIT);
+            a.ready_since = L.clock;
+            if (req) {
+              act_erase(D, L, agent);
+              pend_push(D, L, agent);
+            }
+          }
+          sched_admission(L);
+          ++L.events;
           continue;
         }
         if (kind == EV_TOOL) {  // on_tool_complete (engine.cpp:224-235)
@@ -533,40 +803,27 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         fail(L, E_OFFLOAD);
         continue;
       }
-      case PH_ARGMIN_DONE:
-        L.amin_valid = 1;
-        L.amin_any = op.amin_any;
-        L.amin_t = op.amin_t;
-        L.amin_o = op.amin_o;
-        L.amin_a = op.amin_a;
-        L.phase = PH_EVENT;
-        continue;
-      // --------------------------------------------- dispatch_batch (305-333)
-      case PH_ADM_READY:
-        L.nready = op.created;
-        L.ready_i = 0;
-        L.batch_n = 0;
-        L.phase = PH_MEMBER;
-        continue;
-      case PH_MEMBER: {  // dispatch_member (engine.cpp:337-396)
-        if (L.ready_i >= L.nready) {
+      // --------------------------------------------- dispatch_member (337-396)
+      case PH_MEMBER: {
+        const u32 id = L.m_next;
+        if (id == NIL) {
           L.phase = PH_BATCH_END;
           continue;
         }
-        const u32 id = D.ready[L.ready_i];
         AgentDev& a = D.agents[id];
         L.m_id = id;
-        if (a.pinned > 0) {  // only reachable with offload transfers
+        if (a.pinned_pg > 0) {  // only reachable with offload transfers
           fail(L, E_OFFLOAD);
           continue;
         }
         L.m_ctx0 = a.ctx;
         L.m_nctx = a.ctx / L.ps;
         L.m_now = ++L.cclock;  // match_prefix clock bump (cache_tree.cpp:115)
-        // fused match_prefix + pin(matched): stamp the matched path with the
-        // insert's stamp (now+1). If the insert fails it is restored to `now`;
-        // while pinned its stamp is invisible to eviction.
-        post_range(op, id, 0, L.m_nctx, RF_STAMP | RF_PIN, +1, L.m_now + 1);
+        // match_prefix: one pipelined probe pass over the context's pages
+        // stamps the resident prefix with the insert's stamp (now+1); a failed
+        // insert restores `now`. While this agent pins the prefix, its stamp
+        // is invisible to eviction.
+        post_range(op, id, 0, L.m_nctx, RF_STAMP, 0, L.m_now + 1);
         L.phase = PH_M_MATCHED;
         if (L.m_nctx == 0) {
           op.kind = OP_NONE;
@@ -578,15 +835,14 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         if (op.err) fail(L, op.err);
         const u64 f = op.first_miss < L.m_nctx ? op.first_miss : L.m_nctx;
         if (op.resident != f) fail(L, E_PREFIX_BROKEN);
-        L.pinned_pages += op.pin_up;
         const u64 matched = f * L.ps;
         L.lookups += f + (f < L.m_nctx ? 1 : 0);
         L.hit_pages += f;
         L.hit_m += static_cast<double>(matched);
         L.hit_r += static_cast<double>(L.m_ctx0);
         log_rec(D, L, KVG_LOG_MATCH, L.m_id, matched, 0);
+        set_pinned(D, L, L.m_id, matched);  // pin(matched) (engine.cpp:340-342)
         AgentDev& a = D.agents[L.m_id];
-        a.pinned = matched;
         const kvg_step_plan& plan = D.plans[static_cast<size_t>(L.m_id) * L.steps + a.step];
         a.ctx += plan.gen_tokens;  // append_tokens
         L.m_nafter = a.ctx / L.ps;
@@ -598,7 +854,6 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       case PH_M_INSERT: {  // CacheTree::insert loop (cache_tree.cpp:170-187)
         if (L.m_nafter == 0) {  // nothing to cache: ok, no clock bump
           op.created = 0;
-          op.pin_up = 0;
           L.phase = PH_M_CREATED;
           continue;
         }
@@ -609,7 +864,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           continue;
         }
         const u64 k = need - free_slots;
-        const u64 e = L.used - L.pinned_pages;
+        const u64 e = L.used - (L.pin_max + L.pin_priv);
         ++L.evict_calls;
         log_rec(D, L, KVG_LOG_EVICT, L.m_id, k, k < e ? k : e);
         if (e == 0) {  // O(1) nothing-evictable fast path
@@ -625,6 +880,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         op.clock = L.cclock;
         op.agent = L.m_id;
         op.log_clock = L.cclock;
+        op.pin_max = L.pin_max;
         op.err = E_NONE;
         L.phase = PH_M_EVICTED;
         return;
@@ -652,7 +908,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           return;
         }
         ++L.cclock;  // insert clock bump (cache_tree.cpp:188) == m_now + 1
-        post_range(op, L.m_id, L.m_f, L.m_nafter, RF_CREATE, +1, L.cclock);
+        post_range(op, L.m_id, L.m_f, L.m_nafter, RF_CREATE, 0, L.cclock);
         L.phase = PH_M_CREATED;
         if (L.m_f == L.m_nafter) {
           op.kind = OP_NONE;
@@ -663,14 +919,13 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       case PH_M_CREATED: {
         if (op.err) fail(L, op.err);
         L.used += op.created;
-        L.pinned_pages += op.pin_up;
         L.created_pages += op.created;
         if (L.m_nafter > 0) L.refreshed_pages += L.m_f;
         AgentDev& a = D.agents[L.m_id];
         const u64 stored = a.ctx - a.ctx % L.ps;
         const u64 matched = L.m_f * L.ps;
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 1, stored);
-        a.pinned = stored;
+        set_pinned(D, L, L.m_id, stored);  // pin(stored), unpin(matched)
         const u64 ctx0 = L.m_ctx0;
         const u64 missing = ctx0 - matched;
         const u64 rec = a.high_water > matched ? a.high_water - matched : 0;
@@ -685,22 +940,22 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         m.d = decode_t(D.cost, plan.gen_tokens, ctx0);
         m.t = m.f + m.r + m.d;
         D.batch[L.batch_n++] = m;
-        a.f_gen = plan.gen_tokens;
-        a.f_rec = rec;
+        a.f_gen = static_cast<u32>(plan.gen_tokens);
+        a.f_rec = static_cast<u32>(rec);
         a.f_has_tool = plan.has_tool != 0;
-        a.f_obs = plan.obs_tokens;
+        a.f_obs = static_cast<u32>(plan.obs_tokens);
         a.f_tool = plan.tool_latency;
         D.stats[L.m_id].wait_time += L.clock - a.ready_since;
         set_state(D, L, L.m_id, S_GEN);
         ++L.agent_steps;
-        ++L.ready_i;
+        L.m_next = ready_next(D, L, L.m_id + 1);
         L.phase = PH_MEMBER;
         continue;
       }
       case PH_M_FAIL: {  // insert failed: engine.cpp:366-373
         AgentDev& a = D.agents[L.m_id];
         a.ctx = L.m_ctx0;  // context.resize + token_counter rollback
-        post_range(op, L.m_id, 0, L.m_f, RF_STAMP | RF_PIN | RF_STRICT, -1, L.m_now);
+        post_range(op, L.m_id, 0, L.m_f, RF_STAMP, 0, L.m_now);
         L.phase = PH_M_RESTORED;
         if (L.m_f == 0) {
           op.kind = OP_NONE;
@@ -710,11 +965,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       }
       case PH_M_RESTORED: {
         if (op.err) fail(L, op.err);
-        L.pinned_pages -= op.pin_down;
-        D.agents[L.m_id].pinned = 0;
+        set_pinned(D, L, L.m_id, 0);  // unpin(matched); pinned_len = 0
         ++D.stats[L.m_id].stall_events;
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 0, 0);
-        ++L.ready_i;
+        L.m_next = ready_next(D, L, L.m_id + 1);
         L.phase = PH_MEMBER;
         continue;
       }
@@ -739,57 +993,6 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
             sched_agent(D, L, m.id, start + wall, EV_GEN);
           }
         }
-        ++L.events;
-        L.phase = PH_EVENT;
-        continue;
-      }
-      // ------------------------------------ on_generation_complete (184-222)
-      case PH_GEN_UNPINNED: {
-        if (op.err) fail(L, op.err);
-        const u32 id = L.ev_agent;
-        AgentDev& a = D.agents[id];
-        if (a.pinned > 0) {
-          L.pinned_pages -= op.pin_down;
-          a.pinned = 0;
-        }
-        kvg_agent_stats& st = D.stats[id];
-        L.decoded_cum += a.f_gen;
-        L.rec_cum += a.f_rec;
-        st.generated_tokens += a.f_gen;
-        st.recompute_tokens += a.f_rec;
-        if (a.f_rec > 0) ++st.recompute_events;
-        ++a.step;
-        if (a.step >= L.steps) {
-          set_state(D, L, id, S_DONE);
-          // discard_suffix(context, shared_len) (cache_tree.cpp:404-437):
-          // page_ceil(shared_len) keeps a straddling page (quirk Q2)
-          const u64 fp = (L.shared_len + L.ps - 1) / L.ps;
-          const u64 np = a.ctx / L.ps;
-          if (fp * L.ps < a.ctx && fp < np) {
-            post_range(op, id, fp, np, RF_FREE, 0, 0);
-            L.phase = PH_GEN_DISCARDED;
-            return;
-          }
-          op.freed = 0;
-          op.err = E_NONE;
-          L.phase = PH_GEN_DISCARDED;
-          continue;
-        }
-        const bool req = L.kind == KVG_POLICY_REQUEST_CAP;
-        if (a.f_has_tool) {
-          set_state(D, L, id, S_TOOL);
-          L.ledger.tool_wait += a.f_tool;
-          if (req) act_erase(D, L, id);
-          sched_agent(D, L, id, L.clock + a.f_tool, EV_TOOL);
-        } else {
-          set_state(D, L, id, S_AWAIT);
-          a.ready_since = L.clock;
-          if (req) {
-            act_erase(D, L, id);
-            pend_push(D, L, id);
-          }
-        }
-        sched_admission(L);
         ++L.events;
         L.phase = PH_EVENT;
         continue;
@@ -826,15 +1029,12 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
 // Kernels
 // ==========================================================================
 
-__device__ __forceinline__ void run_op(Op& op, Hist& h, Red& red, const AgentDev* ag, u32 n,
-                                       u32* ready, int tid, int warp, int lane, int nw) {
+__device__ __forceinline__ void run_op(Op& op, Hist& h, int tid, int warp, int lane, int nw) {
   switch (op.kind) {
     case OP_RANGE: coop_range(op, warp, lane, nw); break;
     case OP_EVICT: coop_evict(op, h, tid, warp, lane, nw); break;
-    case OP_ARGMIN: coop_argmin(op, red, ag, n, tid, warp, lane, nw); break;
     case OP_REBUILD: coop_rebuild(op, tid, warp, lane, nw); break;
     case OP_SCANFREE: coop_scanfree(op, warp, lane, nw); break;
-    case OP_READY: coop_ready(op, ag, n, ready, tid, warp, lane, nw); break;
     default: break;
   }
 }
@@ -842,37 +1042,43 @@ __device__ __forceinline__ void run_op(Op& op, Hist& h, Red& red, const AgentDev
 __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   __shared__ Lead L;
   __shared__ Op op;
-  __shared__ Hist h;
-  __shared__ Red red;
   const SimDev& D = sims[blockIdx.x];
+  Hist h{D.hist, D.hist + kBins};
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const u32 n = D.n_agents;
   for (u32 i = tid; i < n; i += blockDim.x) {
     AgentDev a;
-    a.ev_time = 0;
-    a.ev_ord = 0;
     a.ctx = D.prompt_tokens;
-    a.high_water = a.pinned = 0;
+    a.high_water = 0;
+    a.pinned_pg = 0;
     a.ready_since = 0;
     a.f_gen = a.f_rec = a.f_obs = 0;
     a.f_tool = 0;
     a.step = 0;
+    a.pad = 0;
     a.state = S_PENDING;
     a.ev_kind = EV_NONE;
     a.f_has_tool = 0;
     a.in_active = 0;
-    a.next = a.prev = NIL;
+    a.act_seq = 0;
+    a.pad0 = 0;
+    a.ready = 0;
     D.agents[i] = a;
     D.pend[i] = i;
     D.stats[i] = kvg_agent_stats{0, 0, 0, 0, 0, 0.0, -1.0, 0};
   }
+  const u32 nwords = (n + 31) / 32;
+  for (u32 i = tid; i < nwords; i += blockDim.x) D.rbits[i] = 0;
+  for (u32 i = tid; i < (nwords + 31) / 32; i += blockDim.x) D.rl1[i] = 0;
+  for (u64 i = tid; i <= D.shared_pages; i += blockDim.x) D.pin_hist[i] = 0;
+  for (u64 i = tid; i <= D.shared_pages / 32; i += blockDim.x) D.pin_lvl[i] = 0;
   if (tid == 0) lead_init(D, L, op);
   __syncthreads();
   for (;;) {
     if (tid == 0) leader_step(D, L, op);
     __syncthreads();
     if (op.kind == OP_EXIT) break;
-    run_op(op, h, red, D.agents, n, D.ready, tid, warp, lane, nw);
+    run_op(op, h, tid, warp, lane, nw);
     __syncthreads();
   }
 }
@@ -888,235 +1094,6 @@ __global__ void __launch_bounds__(1024, 1) engine_kernel_big(const SimDev* __res
   engine_body(sims);
 }
 
-// --------------------------------------------------------------------------
-// Cache-op executor (CacheTree seam). One CTA executes ops in order.
-
-enum CPhase : int {
-  C_NEXT = 0, C_MATCH_DONE, C_INS_COUNT, C_INS_COUNTED, C_INS_EVICTED, C_INS_COMMIT,
-  C_INS_DONE, C_EVICT_DONE, C_PIN_DONE, C_DISC_PROBED, C_DISC_DONE, C_END
-};
-
-struct CLead {
-  int phase;
-  u32 i;
-  u64 used, clock, pinned, discarded, n0_victims;
-  double hit_m, hit_r;
-  u64 n, k, e, fp, head_owner;
-  int rebuilt;
-};
-
-__device__ void cache_result(const CacheDev& C, CLead& L, Op& op, int status, u64 r0, u64 r1) {
-  kvg_cache_op_result& r = C.results[L.i];
-  r.status = status;
-  r.r0 = r0;
-  r.r1 = r1;
-  r.clock = L.clock;
-  r.used = L.used;
-  r.victims_begin = L.n0_victims;
-  r.victims_end = __ldcg(op.vic_n);
-  ++L.i;
-  L.phase = C_NEXT;
-}
-
-__device__ void cache_leader(const CacheDev& C, CLead& L, Op& op) {
-  op.kind = OP_NONE;
-  for (;;) {
-    const kvg_cache_op* o = &C.ops[L.i < C.n_ops ? L.i : 0];
-    switch (L.phase) {
-      case C_NEXT: {
-        if (L.i >= C.n_ops) {
-          L.phase = C_END;
-          continue;
-        }
-        L.n0_victims = __ldcg(op.vic_n);
-        L.rebuilt = 0;
-        const u64 ps = C.page_size;
-        switch (o->kind) {
-          case KVG_OP_MATCH:  // cache_tree.cpp:114-142
-            L.n = o->len / ps;
-            ++L.clock;
-            post_range(op, o->agent, 0, L.n, RF_STAMP, 0, L.clock);
-            L.phase = C_MATCH_DONE;
-            if (L.n == 0) { op.kind = OP_NONE; continue; }
-            return;
-          case KVG_OP_INSERT:  // cache_tree.cpp:170-228
-            L.n = o->len / ps;
-            if (L.n == 0) { cache_result(C, L, op, KVG_OK, 1, 0); continue; }
-            L.phase = C_INS_COUNT;
-            continue;
-          case KVG_OP_EVICT:
-            L.k = o->arg;
-            L.e = L.used - L.pinned;
-            if (L.k == 0 || L.e == 0) { cache_result(C, L, op, KVG_OK, 0, 0); continue; }
-            op.kind = OP_EVICT; op.k = L.k; op.evictable = L.e; op.clock = L.clock;
-            op.agent = 0; op.err = E_NONE;
-            L.phase = C_EVICT_DONE;
-            return;
-          case KVG_OP_PIN:
-          case KVG_OP_UNPIN:
-            if (o->arg % ps != 0 || o->arg > o->len) {
-              cache_result(C, L, op, KVG_ERR_CONFIG, 0, 0);
-              continue;
-            }
-            post_range(op, o->agent, 0, o->arg / ps, RF_PIN | RF_STRICT, o->kind == KVG_OP_PIN ? 1 : -1, 0);
-            L.phase = C_PIN_DONE;
-            if (o->arg == 0) { op.kind = OP_NONE; continue; }
-            return;
-          case KVG_OP_DISCARD: {  // cache_tree.cpp:404-437
-            L.fp = (o->arg + ps - 1) / ps;
-            if (L.fp * ps >= o->len || L.fp >= o->len / ps) {
-              cache_result(C, L, op, KVG_OK, 0, 0);
-              continue;
-            }
-            post_range(op, o->agent, 0, L.fp + 1, 0, 0, 0);  // path + branch head present?
-            L.phase = C_DISC_PROBED;
-            return;
-          }
-          default:
-            cache_result(C, L, op, KVG_ERR_CONFIG, 0, 0);
-            continue;
-        }
-      }
-      case C_MATCH_DONE: {
-        const u64 f = op.first_miss < L.n ? op.first_miss : L.n;
-        const u64 matched = f * C.page_size;
-        L.hit_m += static_cast<double>(matched);
-        L.hit_r += static_cast<double>(o->len);
-        cache_result(C, L, op, op.resident == f ? KVG_OK : KVG_ERR_STATE, matched, 0);
-        continue;
-      }
-      case C_INS_COUNT:  // count_missing_slots (cache_tree.cpp:144-168)
-        post_range(op, o->agent, 0, L.n, 0, 0, 0);
-        L.phase = C_INS_COUNTED;
-        return;
-      case C_INS_COUNTED: {
-        const u64 f = op.first_miss < L.n ? op.first_miss : L.n;
-        L.fp = f;
-        const u64 need = L.n - f;
-        const u64 free_slots = C.capacity - L.used;
-        if (need <= free_slots) { L.phase = C_INS_COMMIT; continue; }
-        L.k = need - free_slots;
-        L.e = L.used - L.pinned;
-        if (L.e == 0) { cache_result(C, L, op, KVG_OK, 0, 0); continue; }
-        op.kind = OP_EVICT; op.k = L.k; op.evictable = L.e; op.clock = L.clock;
-        op.agent = o->agent; op.err = E_NONE;
-        L.phase = C_INS_EVICTED;
-        return;
-      }
-      case C_INS_EVICTED: {
-        const u64 r = op.freed;
-        L.used -= r;
-        L.discarded += r * C.page_size;
-        L.phase = C_INS_COUNT;  // eviction may strip the unpinned path: recount
-        continue;
-      }
-      case C_INS_COMMIT: {
-        if (static_cast<u64>(op.occ_n) + range_chunks(0, L.n) > (static_cast<u64>(op.mask) + 1) / 2) {
-          if (L.rebuilt) { cache_result(C, L, op, KVG_ERR_STATE, 0, 0); continue; }
-          L.rebuilt = 1;
-          op.kind = OP_REBUILD;
-          return;
-        }
-        ++L.clock;
-        post_range(op, o->agent, 0, L.n, RF_STAMP | RF_CREATE, 0, L.clock);
-        L.phase = C_INS_DONE;
-        return;
-      }
-      case C_INS_DONE:
-        L.used += op.created;
-        cache_result(C, L, op, KVG_OK, 1, op.created);
-        continue;
-      case C_EVICT_DONE: {
-        const u64 r = op.freed;
-        L.used -= r;
-        L.discarded += r * C.page_size;
-        cache_result(C, L, op, KVG_OK, r, 0);
-        continue;
-      }
-      case C_PIN_DONE:
-        L.pinned += op.pin_up;
-        L.pinned -= op.pin_down;
-        cache_result(C, L, op, op.err ? KVG_ERR_STATE : KVG_OK, 0, 0);
-        continue;
-      case C_DISC_PROBED: {
-        if (op.first_miss <= L.fp) { cache_result(C, L, op, KVG_OK, 0, 0); continue; }
-        const u64 head_owner = L.fp < C.shared_pages ? 0 : static_cast<u64>(o->agent) + 1;
-        op.kind = OP_SCANFREE;
-        op.p0 = L.fp;
-        op.owner_filter = head_owner == 0 ? ~0ull : head_owner;
-        op.freed = 0;
-        op.err = E_NONE;
-        L.phase = C_DISC_DONE;
-        return;
-      }
-      case C_DISC_DONE:
-        L.used -= op.freed;
-        L.discarded += static_cast<u64>(op.freed) * C.page_size;
-        cache_result(C, L, op, op.err ? KVG_ERR_STATE : KVG_OK, op.freed, 0);
-        continue;
-      default:
-        op.kind = OP_EXIT;
-        return;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(1024) cache_kernel(const CacheDev* __restrict__ cd) {
-  __shared__ CLead L;
-  __shared__ Op op;
-  __shared__ Hist h;
-  __shared__ Red red;
-  const CacheDev& C = *cd;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  CacheState* st = reinterpret_cast<CacheState*>(C.state);
-  if (tid == 0) {
-    L.phase = C_NEXT;
-    L.i = 0;
-    L.used = st->used;
-    L.clock = st->clock;
-    L.pinned = st->pinned_pages;
-    L.discarded = st->discarded;
-    L.hit_m = st->hit_m;
-    L.hit_r = st->hit_r;
-    const bool sw = st->swapped & 1;
-    op.table = sw ? C.alt : C.table;
-    op.alt = sw ? C.table : C.alt;
-    op.occ = sw ? C.alt_occ : C.occ;
-    op.alt_occ = sw ? C.occ : C.alt_occ;
-    op.mask = C.bucket_mask;
-    op.occ_n = static_cast<unsigned int>(st->occ_n);
-    op.shared_pages = C.shared_pages;
-    op.log = nullptr;
-    op.log_cap = 0;
-    op.log_n = nullptr;
-    op.vic = C.victims;
-    op.vic_cap = C.victim_cap;
-    op.vic_n = reinterpret_cast<unsigned long long*>(&st->n_victims);
-    op.log_victims = 1;
-    op.log_clock = 0;
-  }
-  __syncthreads();
-  for (;;) {
-    if (tid == 0) {
-      Slot* before = op.table;
-      cache_leader(C, L, op);
-      (void)before;
-    }
-    __syncthreads();
-    if (op.kind == OP_EXIT) break;
-    run_op(op, h, red, nullptr, 0, nullptr, tid, warp, lane, nw);
-    __syncthreads();
-    if (tid == 0 && op.kind == OP_REBUILD) st->swapped ^= 1;
-  }
-  if (tid == 0) {
-    st->used = L.used;
-    st->clock = L.clock;
-    st->pinned_pages = L.pinned;
-    st->discarded = L.discarded;
-    st->hit_m = L.hit_m;
-    st->hit_r = L.hit_r;
-    st->occ_n = op.occ_n;
-  }
-}
-
 }  // namespace kvg
+
+#include "cache.cuh"
