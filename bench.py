@@ -311,7 +311,9 @@ def run_b200(args):
             else "kvg::engine_kernel_big",
             "algorithmic_bytes_per_launch": ab,
             "kernel_ms_per_launch": kern_ms / args.steps}
-    # ---- end to end through the C ABI with host buffers
+    # ---- end to end through the C ABI with host buffers: every step creates
+    # the batch from host populations (H2D), runs it, and the kernel streams
+    # results / trace rows / agent stats into pinned host memory (D2H)
     e2e_ms = []
     h2d = sum(p.c.agents * p.c.steps * C.sizeof(abi.StepPlan) for p in pops.values()) + \
         len(specs) * 512
@@ -319,18 +321,14 @@ def run_b200(args):
     for _ in range(args.e2e_steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        b2 = engine.Batch(specs, device=device)           # H2D of populations + descriptors
+        b2 = engine.Batch(specs, device=device, host_outputs=True)
         b2.run()
-        got = 0
-        for i in range(len(specs)):                       # D2H: results, traces, agent stats
-            b2.result(i)
-            got += len(b2.trace_array(i)) * C.sizeof(abi.TraceRow)
-            got += specs[i].population.c.agents * C.sizeof(abi.AgentStats)
-            got += C.sizeof(abi.SimResult)
+        res2 = b2.results_raw()
+        d2h = sum(r.ticks * C.sizeof(abi.TraceRow) for r in res2) + \
+            sum(s.population.c.agents for s in specs) * C.sizeof(abi.AgentStats) + \
+            len(res2) * C.sizeof(abi.SimResult)
         b2.close()
-        torch.cuda.synchronize()
         e2e_ms.append(1e3 * (time.perf_counter() - t0))
-        d2h = got
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)

@@ -198,6 +198,7 @@ typedef struct kvg_sim_result {
   uint64_t refreshed_pages; /* resident pages refreshed by successful inserts */
   uint64_t evict_scanned;   /* resident pages scanned by eviction selects     */
   uint64_t agent_events;    /* agent state-machine advances                   */
+  uint64_t device_cycles;   /* SM clock cycles this simulation ran (device)   */
   kvg_phase_label phases[3];
 } kvg_sim_result;
 
@@ -244,6 +245,11 @@ typedef struct kvg_batch_options {
   uint32_t warps_per_sim; /* 0 = automatic (1 for small sims, up to 32)   */
   uint32_t log_capacity;  /* per-sim event-log records; 0 disables logging */
   uint64_t trace_capacity;/* per-sim trace rows; 0 = automatic (grows)     */
+  uint32_t host_outputs;  /* 1: kvg_batch_run also delivers results, agent
+                             stats and (densely packed) trace rows into
+                             pinned host memory before returning; 0: they
+                             stay in HBM until first accessed */
+  uint32_t _pad;
 } kvg_batch_options;
 
 KVG_API void kvg_batch_options_init(kvg_batch_options* o);
@@ -273,6 +279,13 @@ KVG_API kvg_status kvg_batch_agent_stats(kvg_batch* b, size_t i,
                                          size_t* n_agents);
 KVG_API kvg_status kvg_batch_log(kvg_batch* b, size_t i, kvg_log_record* out,
                                  size_t cap, size_t* n_records);
+/* Every simulation's result of the last run, one call (cap >= n). */
+KVG_API kvg_status kvg_batch_results(kvg_batch* b, kvg_sim_result* out, size_t cap);
+/* Host pointers to the run's output arrays (valid until the next run or
+ * free). Zero-copy when the batch was created with host_outputs. */
+KVG_API kvg_status kvg_batch_outputs(kvg_batch* b, const kvg_sim_result** results,
+                                     const kvg_trace_row** trace_base,
+                                     const kvg_agent_stats** stats_base);
 KVG_API void kvg_batch_free(kvg_batch* b);
 
 /* One-shot convenience: create, run, read scalar results, free. */

@@ -116,7 +116,7 @@ class SimResult(C.Structure):
                 ("cache_clock", u64), ("pool_used", u64),
                 ("hit_matched", f64), ("hit_requested", f64),
                 ("hit_pages", u64), ("created_pages", u64), ("refreshed_pages", u64),
-                ("evict_scanned", u64), ("agent_events", u64),
+                ("evict_scanned", u64), ("agent_events", u64), ("device_cycles", u64),
                 ("phases", PhaseLabel * 3)]
 
 
@@ -126,7 +126,7 @@ class LogRecord(C.Structure):
 
 class BatchOptions(C.Structure):
     _fields_ = [("warps_per_sim", u32), ("log_capacity", u32),
-                ("trace_capacity", u64)]
+                ("trace_capacity", u64), ("host_outputs", u32), ("_pad", u32)]
 
 
 class CacheOp(C.Structure):

@@ -49,7 +49,7 @@ def _stale(target, sources):
 
 def build_native(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
-    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh", ".inc"))]
     headers.append(os.path.join(REPO, "include", "kvgpu.h"))
     srcs = {
         "engine.o": (os.path.join(CSRC, "engine.cu"), "nvcc"),

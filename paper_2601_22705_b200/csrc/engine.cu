@@ -173,7 +173,7 @@ __device__ __forceinline__ bool probe_from(const Op& op, u64 tag, u32 b, int lan
 }
 
 // Claims an empty bucket for `tag`, starting at bucket `b`; returns it.
-__device__ u32 claim(Op& op, Slot* table, u32* occ, unsigned int* occ_n, u32 mask,
+__device__ __noinline__ u32 claim(Op& op, Slot* table, u32* occ, unsigned int* occ_n, u32 mask,
                      u64 tag, u32 b, int lane) {
   for (;;) {
     int won = 0;
@@ -266,7 +266,7 @@ __device__ __forceinline__ void range_chunk(Op& op, u64 tag, u64 lo, u64 hi, u32
 // context of C chunks costs ~C/(nw*kProbeDepth) DRAM round trips, not C.
 constexpr int kProbeDepth = 8;
 
-__device__ void coop_range(Op& op, int warp, int lane, int nw) {
+__device__ __noinline__ void coop_range(Op& op, int warp, int lane, int nw) {
   const u64 p0 = op.p0, p1 = op.p1;
   if (p0 >= p1) return;
   const u64 S = op.shared_pages;
@@ -292,7 +292,7 @@ __device__ void coop_range(Op& op, int warp, int lane, int nw) {
         s[g] = ld_slot(&op.table[(size_t)b[g] * kChunk + lane]);
       }
     }
-#pragma unroll
+#pragma unroll 1
     for (int g = 0; g < kProbeDepth; ++g) {
       const u64 it = base + static_cast<u64>(g) * nw;
       if (it >= total) break;
@@ -363,10 +363,12 @@ __device__ __forceinline__ void scan_buckets(const Op& op, int warp, int lane, i
       thr[g] = 0;
       if (i < n_occ && op.implicit_pins) {
         const u64 owner = __shfl_sync(FULL, s[g].key, 0) >> 32;
-        thr[g] = owner == 0 ? op.pin_max : __ldcg(&op.agents[owner - 1].pinned_pg);
+        // plain load: the records may live in shared memory (leader wrote them
+        // before the barrier that started this op)
+        thr[g] = owner == 0 ? op.pin_max : op.agents[owner - 1].pinned_pg;
       }
     }
-#pragma unroll
+#pragma unroll 1
     for (int g = 0; g < kScanDepth; ++g) {
       const u32 i = base + g * nw;
       if (i < n_occ) f(bk[g], s[g], thr[g]);
@@ -396,7 +398,7 @@ __device__ __forceinline__ void emit_victim(Op& op, u64 key, u64 stamp, u32 agen
 // Warp 0: find the histogram bin holding rank op.need (1-based) among
 // nbins bins. Returns the bin; *rank_in_bin receives the rank inside it.
 // Every lane gets both values through shuffles (no smem read-after-write).
-__device__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int lane, u64* rank_in_bin) {
+__device__ __noinline__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int lane, u64* rank_in_bin) {
   const u32 per = (nbins + 31) / 32;
   const u32 base = lane * per;
   u32 local = 0;
@@ -441,7 +443,7 @@ __device__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int lane, u64* rank
 // Radix select over stamps (9-bit digits, shared-memory histogram with
 // warp-aggregated atomics), exact threshold stamp T and the deepest-j cut
 // inside it (equal stamps lie on one root path), then one scatter pass.
-__device__ void coop_evict(Op& op, Hist& h, int tid, int warp, int lane, int nw) {
+__device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int lane, int nw) {
   const int nt = nw * 32;
   if (tid == 0) {
     op.all = op.k >= op.evictable;
@@ -510,7 +512,7 @@ __device__ void coop_evict(Op& op, Hist& h, int tid, int warp, int lane, int nw)
 
 // SCANFREE: free resident pages with index >= p0 and (owner == owner_filter
 // or owner_filter == ~0). Cache-API discard_suffix below a shared head.
-__device__ void coop_scanfree(Op& op, int warp, int lane, int nw) {
+__device__ __noinline__ void coop_scanfree(Op& op, int warp, int lane, int nw) {
   unsigned int freed = 0;
   int err = 0;
   scan_buckets(op, warp, lane, nw, [&](u32 b, const Slot& s, u64) {
@@ -538,7 +540,7 @@ __device__ void coop_scanfree(Op& op, int warp, int lane, int nw) {
 
 // REBUILD: copy buckets holding at least one resident page into the
 // alternate table (pre-cleared here), then swap tables.
-__device__ void coop_rebuild(Op& op, int tid, int warp, int lane, int nw) {
+__device__ __noinline__ void coop_rebuild(Op& op, int tid, int warp, int lane, int nw) {
   const int nt = nw * 32;
   const size_t nslots = (static_cast<size_t>(op.mask) + 1) * kChunk;
   for (size_t i = tid; i < nslots; i += nt) {
@@ -576,3 +578,22 @@ __device__ void coop_rebuild(Op& op, int tid, int warp, int lane, int nw) {
 // ==========================================================================
 
 #include "leader.cuh"
+
+namespace kvg {
+
+// Compacts each simulation's trace rows (ragged, capacity-strided in HBM)
+// into one dense array so the host receives them in a single DMA.
+// Block b copies sim b's rows as 8-byte words (rows are 88 B, so a 16-byte
+// vector would misalign at odd row offsets).
+__global__ void __launch_bounds__(256) pack_traces(const SimDev* __restrict__ sims,
+                                                   const u64* __restrict__ dst_off,
+                                                   kvg_trace_row* __restrict__ packed) {
+  const SimDev& D = sims[blockIdx.x];
+  const u64 rows = D.counts[0] < D.trace_cap ? D.counts[0] : D.trace_cap;
+  const u64* src = reinterpret_cast<const u64*>(D.trace);
+  u64* dst = reinterpret_cast<u64*>(packed + dst_off[blockIdx.x]);
+  const u64 words = rows * sizeof(kvg_trace_row) / sizeof(u64);
+  for (u64 i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldcs(src + i);
+}
+
+}  // namespace kvg

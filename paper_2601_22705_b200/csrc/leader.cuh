@@ -49,6 +49,7 @@ struct Lead {
   u64 used, cclock, discarded, lookups, agent_steps, events, evict_calls, evicted;
   u64 pin_max, pin_priv;  // implicit pins: shared prefix max, private pinned pages
   u64 hit_pages, created_pages, refreshed_pages, evict_scanned, agent_events;
+  long long t_start;
   double hit_m, hit_r;
   // controller (controller.hpp:117-126)
   double window, su, sh;
@@ -61,7 +62,12 @@ struct Lead {
   unsigned long long n_trace, n_log;
   // dispatch context
   u32 batch_n, m_id, m_next, pad1;
-  u64 m_ctx0, m_f, m_nctx, m_nafter, m_now, m_k, m_e;
+  u64 m_ctx0, m_f, m_nctx, m_nafter, m_now, m_k, m_e, m_stamp;
+  // hot per-agent structures: shared memory for small sims, else HBM
+  AgentDev* ag;
+  HeapEnt* heap;
+  u32* rbits;
+  u32* rl1;
   // config snapshot
   double interval, decay, horizon, capacity_d;
   u64 capacity, ps, shared_len, S;
@@ -101,15 +107,15 @@ __device__ __forceinline__ void ready_sync(const SimDev& D, Lead& L, AgentDev& a
   if (want == a.ready) return;
   a.ready = want;
   const u32 w = id >> 5, bit = 1u << (id & 31);
-  u32 v = D.rbits[w];
+  u32 v = L.rbits[w];
   if (want) {
-    if (v == 0) D.rl1[w >> 5] |= 1u << (w & 31);
-    D.rbits[w] = v | bit;
+    if (v == 0) L.rl1[w >> 5] |= 1u << (w & 31);
+    L.rbits[w] = v | bit;
     ++L.n_ready;
   } else {
     v &= ~bit;
-    D.rbits[w] = v;
-    if (v == 0) D.rl1[w >> 5] &= ~(1u << (w & 31));
+    L.rbits[w] = v;
+    if (v == 0) L.rl1[w >> 5] &= ~(1u << (w & 31));
     --L.n_ready;
   }
 }
@@ -118,13 +124,13 @@ __device__ __forceinline__ void ready_sync(const SimDev& D, Lead& L, AgentDev& a
 __device__ __forceinline__ u32 ready_next(const SimDev& D, const Lead& L, u32 from) {
   if (from >= L.n) return NIL;
   const u32 w = from >> 5;
-  const u32 bits = D.rbits[w] & (~0u << (from & 31));
+  const u32 bits = L.rbits[w] & (~0u << (from & 31));
   if (bits) return (w << 5) + __ffs(bits) - 1;
   for (u32 w1 = w + 1; w1 < L.nwords;) {
-    const u32 m = D.rl1[w1 >> 5] & (~0u << (w1 & 31));
+    const u32 m = L.rl1[w1 >> 5] & (~0u << (w1 & 31));
     if (m) {
       const u32 ww = ((w1 >> 5) << 5) + __ffs(m) - 1;
-      return (ww << 5) + __ffs(D.rbits[ww]) - 1;
+      return (ww << 5) + __ffs(L.rbits[ww]) - 1;
     }
     w1 = ((w1 >> 5) + 1) << 5;
   }
@@ -133,7 +139,7 @@ __device__ __forceinline__ u32 ready_next(const SimDev& D, const Lead& L, u32 fr
 
 // AgentRecord::set_state (workload.cpp:130-137)
 __device__ __forceinline__ void set_state(const SimDev& D, Lead& L, u32 id, uint8_t s) {
-  AgentDev& a = D.agents[id];
+  AgentDev& a = L.ag[id];
   if (!legal_edge(a.state, s)) {
     fail(L, E_ILLEGAL_TRANSITION);
     return;
@@ -148,7 +154,7 @@ __device__ __forceinline__ void set_state(const SimDev& D, Lead& L, u32 id, uint
 // admission sequence number; the victim is the ready agent (active and
 // AwaitingAdmission = at_boundary) with the largest sequence number.
 __device__ __forceinline__ void act_push(const SimDev& D, Lead& L, u32 id) {
-  AgentDev& a = D.agents[id];
+  AgentDev& a = L.ag[id];
   a.in_active = 1;
   a.act_seq = ++L.act_seq;
   ++L.act_size;
@@ -156,7 +162,7 @@ __device__ __forceinline__ void act_push(const SimDev& D, Lead& L, u32 id) {
 }
 
 __device__ __forceinline__ bool act_erase(const SimDev& D, Lead& L, u32 id) {
-  AgentDev& a = D.agents[id];
+  AgentDev& a = L.ag[id];
   if (!a.in_active) {
     fail(L, E_NOT_ACTIVE);
     return false;
@@ -168,11 +174,11 @@ __device__ __forceinline__ bool act_erase(const SimDev& D, Lead& L, u32 id) {
 }
 
 // newest active agent at a step boundary, or NIL
-__device__ __forceinline__ u32 pause_victim(const SimDev& D, const Lead& L) {
+__device__ __noinline__ u32 pause_victim(const SimDev& D, const Lead& L) {
   if (L.n_ready == 0) return NIL;
   u32 best = NIL, best_seq = 0;
   for (u32 id = ready_next(D, L, 0); id != NIL; id = ready_next(D, L, id + 1)) {
-    const u32 q = D.agents[id].act_seq;
+    const u32 q = L.ag[id].act_seq;
     if (best == NIL || q > best_seq) {
       best = id;
       best_seq = q;
@@ -210,7 +216,7 @@ __device__ __forceinline__ u32 paus_pop(const SimDev& D, Lead& L) {
 
 // Implicit pins: agent `id` now pins its path prefix [0, tokens).
 __device__ __forceinline__ void set_pinned(const SimDev& D, Lead& L, u32 id, u64 tokens) {
-  AgentDev& a = D.agents[id];
+  AgentDev& a = L.ag[id];
   const u64 old_pg = a.pinned_pg, new_pg = tokens / L.ps;
   a.pinned_pg = static_cast<u32>(new_pg);
   if (old_pg == new_pg) return;
@@ -239,14 +245,14 @@ __device__ __forceinline__ bool heap_less(const HeapEnt& x, const HeapEnt& y) {
 // Engine::schedule for agent events (engine.cpp:143-145)
 __device__ __forceinline__ void sched_agent(const SimDev& D, Lead& L, u32 id, double t,
                                             uint8_t kind) {
-  AgentDev& a = D.agents[id];
+  AgentDev& a = L.ag[id];
   if (a.ev_kind != EV_NONE) {
     fail(L, E_EVENT_BUSY);
     return;
   }
   a.ev_kind = kind;
   const HeapEnt e{t, (L.ord++ << kAgentBits) | id};
-  HeapEnt* h = D.heap;
+  HeapEnt* h = L.heap;
   u32 i = L.hsize++;
   while (i > 0) {
     const u32 p = (i - 1) >> 1;
@@ -259,7 +265,7 @@ __device__ __forceinline__ void sched_agent(const SimDev& D, Lead& L, u32 id, do
 }
 
 __device__ __forceinline__ void heap_pop(const SimDev& D, Lead& L) {
-  HeapEnt* h = D.heap;
+  HeapEnt* h = L.heap;
   const u32 n = --L.hsize;
   if (n == 0) return;
   const HeapEnt last = h[n];
@@ -367,7 +373,7 @@ __device__ __forceinline__ u64 range_chunks(u64 p0, u64 p1) {
 // ------------------------------------------------------------ the handlers
 
 // Engine::on_control_tick (engine.cpp:245-266) — the kernel-3 signal step.
-__device__ void on_tick(const SimDev& D, Lead& L) {
+__device__ __noinline__ void on_tick(const SimDev& D, Lead& L) {
   const double usage = static_cast<double>(L.used) / L.capacity_d;
   const double m = L.hit_m, r = L.hit_r;
   const double hit = r > 0 ? m / r : 1.0;
@@ -400,7 +406,7 @@ __device__ void on_tick(const SimDev& D, Lead& L) {
 // applied as Engine::on_admission_check does (engine.cpp:268-291). Commands
 // can be applied immediately: pausing only removes agents from active_ and
 // happens before any admit, which never reads agent state.
-__device__ void admission_pass(const SimDev& D, Lead& L) {
+__device__ __noinline__ void admission_pass(const SimDev& D, Lead& L) {
   const u64 limit = adm_limit(L);
   if (L.gated) {
     while (L.act_size > limit) {
@@ -420,14 +426,14 @@ __device__ void admission_pass(const SimDev& D, Lead& L) {
     } else if (L.pend_size > 0) {
       u32 id = pend_pop(D, L);
       act_push(D, L, id);
-      if (D.agents[id].state == S_PENDING) set_state(D, L, id, S_AWAIT);  // admit
+      if (L.ag[id].state == S_PENDING) set_state(D, L, id, S_AWAIT);  // admit
     } else {
       break;
     }
   }
 }
 
-__device__ void finalize(const SimDev& D, Lead& L) {
+__device__ __noinline__ void finalize(const SimDev& D, Lead& L) {
   kvg_sim_result* r = D.result;
   r->status = L.status;
   r->n_phases = 0;
@@ -466,15 +472,17 @@ __device__ void finalize(const SimDev& D, Lead& L) {
   r->refreshed_pages = L.refreshed_pages;
   r->evict_scanned = L.evict_scanned;
   r->agent_events = L.agent_events;
+  r->device_cycles = static_cast<u64>(clock64() - L.t_start);
   D.counts[0] = L.n_trace;
   D.counts[1] = L.n_log;
   D.counts[2] = static_cast<u64>(L.err);
 }
 
-__device__ void lead_init(const SimDev& D, Lead& L, Op& op) {
+__device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.status = KVG_OK;
   L.err = E_NONE;
   L.rebuilt = 0;
+  L.t_start = clock64();
   L.clock = L.gpu_busy = L.makespan = L.device_busy = 0.0;
   L.ord = 0;
   L.hsize = 0;
@@ -543,7 +551,7 @@ __device__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   op.log_victims = D.log != nullptr;
   op.implicit_pins = 1;
   op.pin_max = 0;
-  op.agents = D.agents;
+  op.agents = L.ag;
   L.phase = PH_EVENT;
 }
 
@@ -556,7 +564,7 @@ __device__ void lead_init(const SimDev& D, Lead& L, Op& op) {
 // on_admission_check (engine.cpp:245-291, controller.cpp:67-160).
 __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   if (L.finished == L.n || L.status != KVG_OK) return;
-  const double t_agent = L.hsize > 0 ? D.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
+  const double t_agent = L.hsize > 0 ? L.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
   const double horizon = L.horizon;
   // state that no housekeeping event can change
   const bool nready0 = L.n_ready == 0;
@@ -689,7 +697,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         double bt = 0;
         if (L.hsize > 0) {
           which = 0;
-          bt = D.heap[0].t;
+          bt = L.heap[0].t;
         }
         // ranks break time ties: completions, then the tick, then admission
         if (L.tick_on && (which < 0 || L.tick_t < bt)) {
@@ -708,10 +716,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         u32 agent = 0;
         uint8_t kind = EV_NONE;
         if (which == 0) {
-          agent = static_cast<u32>(D.heap[0].k & ((1u << kAgentBits) - 1));
+          agent = static_cast<u32>(L.heap[0].k & ((1u << kAgentBits) - 1));
           heap_pop(D, L);
-          kind = D.agents[agent].ev_kind;
-          D.agents[agent].ev_kind = EV_NONE;
+          kind = L.ag[agent].ev_kind;
+          L.ag[agent].ev_kind = EV_NONE;
         } else if (which == 1) {
           L.tick_on = 0;
         } else {
@@ -742,7 +750,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         }
         L.ev_agent = agent;
         ++L.agent_events;
-        AgentDev& a = D.agents[agent];
+        AgentDev& a = L.ag[agent];
         if (kind == EV_GEN) {  // on_generation_complete (engine.cpp:184-222)
           L.makespan = L.makespan < L.clock ? L.clock : L.makespan;
           set_pinned(D, L, agent, 0);  // unpin(pinned_len) — implicit pins
@@ -810,7 +818,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.phase = PH_BATCH_END;
           continue;
         }
-        AgentDev& a = D.agents[id];
+        AgentDev& a = L.ag[id];
         L.m_id = id;
         if (a.pinned_pg > 0) {  // only reachable with offload transfers
           fail(L, E_OFFLOAD);
@@ -820,10 +828,14 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         L.m_nctx = a.ctx / L.ps;
         L.m_now = ++L.cclock;  // match_prefix clock bump (cache_tree.cpp:115)
         // match_prefix: one pipelined probe pass over the context's pages
-        // stamps the resident prefix with the insert's stamp (now+1); a failed
-        // insert restores `now`. While this agent pins the prefix, its stamp
-        // is invisible to eviction.
-        post_range(op, id, 0, L.m_nctx, RF_STAMP, 0, L.m_now + 1);
+        // stamps the resident prefix with the stamp it will END UP with: the
+        // insert's (now+1) if the insert is predicted to succeed, the match's
+        // (now) if this is the retry of a stalled agent. A misprediction costs
+        // one extra pass (restore, or refresh inside the create); while this
+        // agent pins the prefix its stamp is invisible to eviction, so the
+        // final state is identical either way.
+        L.m_stamp = a.stalled ? L.m_now : L.m_now + 1;
+        post_range(op, id, 0, L.m_nctx, RF_STAMP, 0, L.m_stamp);
         L.phase = PH_M_MATCHED;
         if (L.m_nctx == 0) {
           op.kind = OP_NONE;
@@ -842,7 +854,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         L.hit_r += static_cast<double>(L.m_ctx0);
         log_rec(D, L, KVG_LOG_MATCH, L.m_id, matched, 0);
         set_pinned(D, L, L.m_id, matched);  // pin(matched) (engine.cpp:340-342)
-        AgentDev& a = D.agents[L.m_id];
+        AgentDev& a = L.ag[L.m_id];
         const kvg_step_plan& plan = D.plans[static_cast<size_t>(L.m_id) * L.steps + a.step];
         a.ctx += plan.gen_tokens;  // append_tokens
         L.m_nafter = a.ctx / L.ps;
@@ -908,12 +920,17 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           return;
         }
         ++L.cclock;  // insert clock bump (cache_tree.cpp:188) == m_now + 1
-        post_range(op, L.m_id, L.m_f, L.m_nafter, RF_CREATE, 0, L.cclock);
-        L.phase = PH_M_CREATED;
-        if (L.m_f == L.m_nafter) {
-          op.kind = OP_NONE;
-          continue;
+        if (L.m_stamp == L.cclock) {  // prefix already carries the insert stamp
+          post_range(op, L.m_id, L.m_f, L.m_nafter, RF_CREATE, 0, L.cclock);
+          if (L.m_f == L.m_nafter) {
+            op.kind = OP_NONE;
+            L.phase = PH_M_CREATED;
+            continue;
+          }
+        } else {  // predicted stall did not happen: refresh the prefix too
+          post_range(op, L.m_id, 0, L.m_nafter, RF_STAMP | RF_CREATE, 0, L.cclock);
         }
+        L.phase = PH_M_CREATED;
         return;
       }
       case PH_M_CREATED: {
@@ -921,7 +938,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         L.used += op.created;
         L.created_pages += op.created;
         if (L.m_nafter > 0) L.refreshed_pages += L.m_f;
-        AgentDev& a = D.agents[L.m_id];
+        AgentDev& a = L.ag[L.m_id];
         const u64 stored = a.ctx - a.ctx % L.ps;
         const u64 matched = L.m_f * L.ps;
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 1, stored);
@@ -947,18 +964,21 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         a.f_tool = plan.tool_latency;
         D.stats[L.m_id].wait_time += L.clock - a.ready_since;
         set_state(D, L, L.m_id, S_GEN);
+        a.stalled = 0;
         ++L.agent_steps;
         L.m_next = ready_next(D, L, L.m_id + 1);
         L.phase = PH_MEMBER;
         continue;
       }
       case PH_M_FAIL: {  // insert failed: engine.cpp:366-373
-        AgentDev& a = D.agents[L.m_id];
+        AgentDev& a = L.ag[L.m_id];
         a.ctx = L.m_ctx0;  // context.resize + token_counter rollback
+        a.stalled = 1;
         post_range(op, L.m_id, 0, L.m_f, RF_STAMP, 0, L.m_now);
         L.phase = PH_M_RESTORED;
-        if (L.m_f == 0) {
+        if (L.m_f == 0 || L.m_stamp == L.m_now) {  // nothing to restore
           op.kind = OP_NONE;
+          op.err = E_NONE;
           continue;
         }
         return;
@@ -1039,13 +1059,41 @@ __device__ __forceinline__ void run_op(Op& op, Hist& h, int tid, int warp, int l
   }
 }
 
+// Agents whose hot records fit in shared memory (per-CTA dynamic smem).
+constexpr u32 kSmemAgents = 128;
+
+__device__ __forceinline__ size_t smem_bytes_for(u32 n) {
+  const u32 nwords = (n + 31) / 32;
+  return static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt)) +
+         (nwords + (nwords + 31) / 32) * sizeof(u32);
+}
+
 __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   __shared__ Lead L;
   __shared__ Op op;
+  extern __shared__ __align__(16) unsigned char dyn[];
   const SimDev& D = sims[blockIdx.x];
   Hist h{D.hist, D.hist + kBins};
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const u32 n = D.n_agents;
+  const u32 nwords = (n + 31) / 32;
+  if (tid == 0) {
+    unsigned int dyn_bytes;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_bytes));
+    if (n <= kSmemAgents && smem_bytes_for(n) <= dyn_bytes) {
+      L.ag = reinterpret_cast<AgentDev*>(dyn);
+      L.heap = reinterpret_cast<HeapEnt*>(dyn + static_cast<size_t>(n) * sizeof(AgentDev));
+      L.rbits = reinterpret_cast<u32*>(dyn + static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt)));
+      L.rl1 = L.rbits + nwords;
+    } else {
+      L.ag = D.agents;
+      L.heap = D.heap;
+      L.rbits = D.rbits;
+      L.rl1 = D.rl1;
+    }
+  }
+  __syncthreads();
+  AgentDev* const ag = L.ag;
   for (u32 i = tid; i < n; i += blockDim.x) {
     AgentDev a;
     a.ctx = D.prompt_tokens;
@@ -1055,7 +1103,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     a.f_gen = a.f_rec = a.f_obs = 0;
     a.f_tool = 0;
     a.step = 0;
-    a.pad = 0;
+    a.stalled = 0;
     a.state = S_PENDING;
     a.ev_kind = EV_NONE;
     a.f_has_tool = 0;
@@ -1063,15 +1111,15 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     a.act_seq = 0;
     a.pad0 = 0;
     a.ready = 0;
-    D.agents[i] = a;
+    ag[i] = a;
     D.pend[i] = i;
     D.stats[i] = kvg_agent_stats{0, 0, 0, 0, 0, 0.0, -1.0, 0};
   }
-  const u32 nwords = (n + 31) / 32;
-  for (u32 i = tid; i < nwords; i += blockDim.x) D.rbits[i] = 0;
-  for (u32 i = tid; i < (nwords + 31) / 32; i += blockDim.x) D.rl1[i] = 0;
+  for (u32 i = tid; i < nwords; i += blockDim.x) L.rbits[i] = 0;
+  for (u32 i = tid; i < (nwords + 31) / 32; i += blockDim.x) L.rl1[i] = 0;
   for (u64 i = tid; i <= D.shared_pages; i += blockDim.x) D.pin_hist[i] = 0;
   for (u64 i = tid; i <= D.shared_pages / 32; i += blockDim.x) D.pin_lvl[i] = 0;
+  __syncthreads();
   if (tid == 0) lead_init(D, L, op);
   __syncthreads();
   for (;;) {

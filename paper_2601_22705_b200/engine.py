@@ -64,6 +64,9 @@ def lib():
                                         P(C.c_size_t)]
     L.kvg_batch_log.argtypes = [C.c_void_p, C.c_size_t, P(abi.LogRecord), C.c_size_t,
                                 P(C.c_size_t)]
+    L.kvg_batch_results.argtypes = [C.c_void_p, P(abi.SimResult), C.c_size_t]
+    L.kvg_batch_outputs.argtypes = [C.c_void_p, P(P(abi.SimResult)), P(P(abi.TraceRow)),
+                                    P(P(abi.AgentStats))]
     L.kvg_batch_free.argtypes = [C.c_void_p]
     L.kvg_batch_free.restype = None
     L.kvg_run_batch.argtypes = [C.c_int, P(abi.SimDesc), C.c_size_t, P(abi.SimResult)]
@@ -143,14 +146,14 @@ class Batch:
     """A set of independent simulations executed on one GPU in one launch."""
 
     def __init__(self, specs: list[SimSpec], device: int = 0, warps_per_sim: int = 0,
-                 log_capacity: int = 0, trace_capacity: int = 0):
+                 log_capacity: int = 0, trace_capacity: int = 0, host_outputs: bool = False):
         self.specs = specs
         self.descs = (abi.SimDesc * max(1, len(specs)))()
         for i, sp in enumerate(specs):
             self.descs[i] = abi.SimDesc(population=C.pointer(sp.population.c), policy=sp.policy,
                                         cost=sp.cost, engine=sp.engine)
         opt = abi.BatchOptions(warps_per_sim=warps_per_sim, log_capacity=log_capacity,
-                               trace_capacity=trace_capacity)
+                               trace_capacity=trace_capacity, host_outputs=int(host_outputs))
         h = C.c_void_p()
         _check(lib().kvg_batch_create(device, self.descs, len(specs), C.byref(opt), C.byref(h)))
         self.h = h
@@ -176,12 +179,9 @@ class Batch:
         return abi.struct_to_dict(r)
 
     def results_raw(self) -> list[abi.SimResult]:
-        out = []
-        for i in range(self.n):
-            r = abi.SimResult()
-            _check(lib().kvg_batch_result(self.h, i, C.byref(r)))
-            out.append(r)
-        return out
+        arr = (abi.SimResult * max(1, self.n))()
+        _check(lib().kvg_batch_results(self.h, arr, self.n))
+        return list(arr)[: self.n]
 
     def trace(self, i: int) -> list[dict]:
         n = C.c_size_t()

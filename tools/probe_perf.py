@@ -20,6 +20,10 @@ def run(name, specs, reps=3, **kw):
     look = sum(r.lookups for r in rs)
     ev = sum(r.events for r in rs)
     best = min(ms)
+    cyc = sorted(r.device_cycles for r in rs)
+    if len(cyc) > 1:
+        print(f"  per-sim device ms @1.965GHz: p50={cyc[len(cyc)//2]/1.965e6:.1f} "
+              f"p90={cyc[int(len(cyc)*0.9)]/1.965e6:.1f} max={cyc[-1]/1.965e6:.1f}")
     print(f"{name}: sims={len(specs)} create={1e3*(t1-t0):.1f}ms run={best:.2f}ms "
           f"agent_steps/s={steps/best*1e3:.3e} lookups/s={look/best*1e3:.3e} "
           f"events={ev} evict_calls={sum(r.evict_calls for r in rs)} "
