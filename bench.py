@@ -56,20 +56,14 @@ def env_rank():
 # --------------------------------------------------------------------------- workloads
 
 def build_scenarios(workload: str, rank: int, sims: int):
-    from paper_2601_22705_b200 import config
+    from paper_2601_22705_b200 import sweep
+    scen = sweep.weak_shard(workload, rank, sims)
     if workload == "c4":
-        scen = config.c4_sweep(sims, seed=42 + rank)
         desc = (f"C4 controller sweep: {sims} sims of C1 (64 agents x 10 steps, private 1024-token "
                 f"prompts, 12,629-page cache, Qwen3-32B KV sizing), workload seed {42 + rank}")
     elif workload == "c2":
-        s = config.c2_qwen("aimd")
-        s.seed = 7 + rank
-        scen = [s]
         desc = "C2: 1024 agents x 16 steps, 4K->55.7K contexts, 2,038,926-page cache, aimd"
     else:
-        s = config.c1_toy("aimd")
-        s.seed = 42 + rank
-        scen = [s]
         desc = "C1 toy: 64 agents x 10 steps, aimd"
     return scen, desc
 
@@ -291,14 +285,8 @@ def run_b200(args):
     all_units, all_lookups = cnt.tolist()
     value = all_units * args.steps / (max_ms / 1e3)
     # ---- NCCL final metric gather: per-sim summary records of every rank
-    rec = torch.tensor([[r.makespan, float(r.agent_steps), float(r.lookups), float(r.status)]
-                        for r in results], dtype=torch.float64, device="cuda")
-    if dist:
-        gathered = [torch.empty_like(rec) for _ in range(world)]
-        dist.all_gather(gathered, rec)
-        summary = torch.cat(gathered)
-    else:
-        summary = rec
+    from paper_2601_22705_b200 import sweep
+    summary = sweep.gather_records(sweep.records(results), dist, device="cuda")
     makespans = summary[:, 0].cpu().tolist()
     # ---- roofline of the engine kernel
     ab = algorithmic_bytes(results)

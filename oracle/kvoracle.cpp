@@ -66,6 +66,8 @@ struct FlatCache {
   std::uint64_t used = 0, clock = 0, discarded = 0, offloaded = 0;
   double hit_m = 0, hit_r = 0;
   std::uint64_t evict_calls = 0, evicted = 0;
+  std::uint64_t pinned = 0;  // resident pages with pins > 0 (evictable = used - pinned)
+  std::uint64_t dsum = 0;    // running sum of kvdigest::page_term over resident pages
   std::vector<std::pair<std::uint64_t, std::uint64_t>>* victims = nullptr;
   std::vector<kvg_log_record>* log = nullptr;  // EVICT + VICTIM records
   std::uint32_t log_agent = 0;
@@ -82,6 +84,27 @@ struct FlatCache {
     std::uint64_t owner = k < shared_pages ? 0 : std::uint64_t(a) + 1;
     return (owner << 32) | k;
   }
+  static std::uint64_t term(std::uint64_t key, const Page& p) {
+    return kvdigest::page_term(key >> 32, key & 0xffffffffULL, p.stamp,
+                               static_cast<std::uint64_t>(p.pins), 0);
+  }
+  void restamp(std::uint64_t key, Page* p, std::uint64_t stamp) {
+    dsum -= term(key, *p);
+    p->stamp = stamp;
+    dsum += term(key, *p);
+  }
+  void add_page(std::uint64_t key, std::uint64_t stamp) {
+    Page pg{stamp, 0};
+    pages.emplace(key, pg);
+    dsum += term(key, pg);
+    ++used;
+  }
+  void drop_page(std::unordered_map<std::uint64_t, Page>::iterator it) {
+    dsum -= term(it->first, it->second);
+    if (it->second.pins > 0) --pinned;
+    pages.erase(it);
+    --used;
+  }
   Page* find(std::uint32_t a, std::uint64_t k) {
     auto it = pages.find(key(a, k));
     return it == pages.end() ? nullptr : &it->second;
@@ -96,7 +119,7 @@ struct FlatCache {
   std::uint64_t match(std::uint32_t a, std::uint64_t len) {
     const std::uint64_t now = ++clock;
     const std::uint64_t f = first_miss(a, len / ps);
-    for (std::uint64_t k = 0; k < f; ++k) find(a, k)->stamp = now;
+    for (std::uint64_t k = 0; k < f; ++k) restamp(key(a, k), find(a, k), now);
     hit_m += static_cast<double>(f * ps);
     hit_r += static_cast<double>(len);
     return f * ps;
@@ -112,10 +135,14 @@ struct FlatCache {
   /* evict, cache_tree.cpp:270-319 in its per-page form. */
   std::uint64_t evict(std::uint64_t needed) {
     if (needed == 0) return 0;
+    ++evict_calls;
+    if (used == pinned) {  // nothing evictable: the common stall-storm case
+      if (log) log->push_back(kvg_log_record{KVG_LOG_EVICT, log_agent, clock, needed, 0});
+      return 0;
+    }
     std::vector<std::pair<std::uint64_t, Page*>> cand;
     for (auto& kv : pages)
       if (kv.second.pins == 0) cand.emplace_back(kv.first, &kv.second);
-    ++evict_calls;
     std::uint64_t take = std::min<std::uint64_t>(needed, cand.size());
     if (log) log->push_back(kvg_log_record{KVG_LOG_EVICT, log_agent, clock, needed, take});
     if (take == 0) return 0;
@@ -125,10 +152,9 @@ struct FlatCache {
       if (log)
         log->push_back(kvg_log_record{KVG_LOG_VICTIM, log_agent, clock, cand[i].first,
                                       cand[i].second->stamp});
-      pages.erase(cand[i].first);
+      drop_page(pages.find(cand[i].first));
     }
     evicted += take;
-    used -= take;
     discarded += take * ps;
     return take;
   }
@@ -151,11 +177,10 @@ struct FlatCache {
     for (std::uint64_t k = 0; k < n; ++k) {
       Page* p = find(a, k);
       if (p == nullptr) {
-        pages.emplace(key(a, k), Page{now, 0});
-        ++used;
+        add_page(key(a, k), now);
         if (inserted) ++*inserted;
       } else {
-        p->stamp = now;
+        restamp(key(a, k), p, now);
       }
     }
     return true;
@@ -168,7 +193,12 @@ struct FlatCache {
       Page* p = find(a, k);
       if (p == nullptr) throw StateError("pin path missing from tree");
       if (delta < 0 && p->pins == 0) throw StateError("unpin on a node with zero pin count");
+      const std::uint64_t kk = key(a, k);
+      dsum -= term(kk, *p);
+      if (p->pins == 0 && delta > 0) ++pinned;
       p->pins += delta;
+      if (p->pins == 0) --pinned;
+      dsum += term(kk, *p);
     }
   }
 
@@ -183,27 +213,29 @@ struct FlatCache {
     // the branch subtree: pages on any path through page fp
     std::vector<std::uint64_t> doomed;
     const std::uint64_t head_owner = key(a, fp) >> 32;
-    for (auto& kv : pages) {
-      std::uint64_t owner = kv.first >> 32, idx = kv.first & 0xffffffffULL;
-      // below a shared head: every page deeper than it (shared or private);
-      // below a private head: that agent's deeper pages only
-      bool below = idx >= fp && (head_owner == 0 || owner == head_owner);
-      if (!below) continue;
-      if (kv.second.pins > 0) throw StateError("discard_suffix would drop pinned nodes");
-      doomed.push_back(kv.first);
+    if (head_owner != 0) {
+      // private head: the subtree is this agent's chain from fp (resident
+      // pages of a chain are a contiguous prefix: walk until the first miss)
+      for (std::uint64_t k = fp;; ++k) {
+        auto it = pages.find((head_owner << 32) | k);
+        if (it == pages.end()) break;
+        if (it->second.pins > 0) throw StateError("discard_suffix would drop pinned nodes");
+        doomed.push_back(it->first);
+      }
+    } else {
+      // shared head: every page deeper than it, shared or private
+      for (auto& kv : pages) {
+        if ((kv.first & 0xffffffffULL) < fp) continue;
+        if (kv.second.pins > 0) throw StateError("discard_suffix would drop pinned nodes");
+        doomed.push_back(kv.first);
+      }
     }
-    for (std::uint64_t k : doomed) pages.erase(k);
-    used -= doomed.size();
+    for (std::uint64_t k : doomed) drop_page(pages.find(k));
     discarded += doomed.size() * ps;
   }
 
-  std::uint64_t digest() const {
-    std::uint64_t sum = 0;
-    for (const auto& kv : pages)
-      sum += kvdigest::page_term(kv.first >> 32, kv.first & 0xffffffffULL,
-                                 kv.second.stamp,
-                                 static_cast<std::uint64_t>(kv.second.pins), 0);
-    std::uint64_t h = kvdigest::fold(0x1234, sum);
+  std::uint64_t digest() const {  // O(1): dsum is maintained incrementally
+    std::uint64_t h = kvdigest::fold(0x1234, dsum);
     h = kvdigest::fold(h, used);
     h = kvdigest::fold(h, clock);
     h = kvdigest::fold(h, kvdigest::dbits(hit_m));
@@ -682,6 +714,41 @@ struct Sim {
     res->pool_used = cache.used;
     res->hit_matched = cache.hit_m;
     res->hit_requested = cache.hit_r;
+    classify(res);
+  }
+
+  /* classify_phases, metrics.cpp:41-81 (called from finish_result, engine.cpp:413) */
+  void classify(kvg_sim_result* res) const {
+    const kvg_phase_params& pp = d->engine.phases;
+    const double mk = res->makespan;
+    res->n_phases = 0;
+    if (mk <= 0) return;
+    auto hot = [&](const kvg_trace_row& r) {
+      return r.usage >= pp.sat_threshold && r.hit_rate < pp.hit_threshold;
+    };
+    auto push = [&](std::uint32_t ph, double a, double b) {
+      res->phases[res->n_phases++] = kvg_phase_label{ph, 0, a, b};
+    };
+    std::size_t enter = trace.size();
+    for (std::size_t i = 0; i < trace.size(); ++i)
+      if (hot(trace[i])) { enter = i; break; }
+    if (enter == trace.size()) {
+      push(KVG_PHASE_WARMUP, 0.0, mk);
+      return;
+    }
+    const double ms = trace[enter].time;
+    double me = mk;
+    int bad = 0;
+    for (std::size_t i = enter + 1; i < trace.size(); ++i) {
+      if (hot(trace[i])) { bad = 0; continue; }
+      if (++bad >= pp.hysteresis) {
+        me = trace[i + 1 - static_cast<std::size_t>(pp.hysteresis)].time;
+        break;
+      }
+    }
+    if (ms > 0) push(KVG_PHASE_WARMUP, 0.0, ms);
+    push(KVG_PHASE_MIDDLE, ms, me);
+    if (me < mk) push(KVG_PHASE_COOLDOWN, me, mk);
   }
 };
 

@@ -169,7 +169,9 @@ __device__ void cache_leader(const CacheDev& C, CLead& L, Op& op) {
       case C_DISC_DONE:
         L.used -= op.freed;
         L.discarded += static_cast<u64>(op.freed) * C.page_size;
-        cache_result(C, L, op, op.err ? KVG_ERR_STATE : KVG_OK, op.freed, 0);
+        // discard_suffix returns nothing (cache_tree.hpp:138); the pool
+        // usage in the op result shows what it dropped
+        cache_result(C, L, op, op.err ? KVG_ERR_STATE : KVG_OK, 0, 0);
         continue;
       default:
         op.kind = OP_EXIT;

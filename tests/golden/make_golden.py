@@ -22,34 +22,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 from paper_2601_22705_b200 import config  # noqa: E402
 from tests.golden_cases import CASES, cache_fuzz_program, case_scenario  # noqa: E402
+from tests.golden_hash import hx, run_record  # noqa: E402
 from tests.helpers import ref_lib, ref_run  # noqa: E402
 from paper_2601_22705_b200 import abi  # noqa: E402
 import ctypes as C  # noqa: E402
 
 PRESETS = "/root/reference/proj/configs"
-
-
-def hx(v):
-    return struct.pack("<d", v).hex() if isinstance(v, float) else v
-
-
-def run_hashes(run):
-    h_tr = hashlib.sha256()
-    for r in run["trace"]:
-        for f in abi.TRACE_FIELDS:
-            h_tr.update(str(hx(r[f])).encode())
-    h_ag = hashlib.sha256()
-    for a in run["agents"]:
-        for f in abi.AGENT_FIELDS:
-            h_ag.update(str(hx(a[f])).encode())
-    h_dg = hashlib.sha256(run["digests"].tobytes()) if run["digests"] is not None else None
-    res = {k: hx(v) for k, v in run["result"].items() if k not in ("phases", "ledger")}
-    res["ledger"] = {k: hx(v) for k, v in run["result"]["ledger"].items()}
-    res["phases"] = [[p["phase"], hx(p["start"]), hx(p["end"])]
-                     for p in run["result"]["phases"][: run["result"]["n_phases"]]]
-    return dict(status=run["status"], result=res, trace_sha=h_tr.hexdigest(),
-                agents_sha=h_ag.hexdigest(), n_events=len(run["digests"]) if run["digests"] is not None else None,
-                digest_sha=h_dg.hexdigest() if h_dg else None)
 
 
 def main():
@@ -63,7 +41,7 @@ def main():
     for case in CASES:
         s, pol = case_scenario(case, scen)
         r = ref_run(s, pol, digests=case.get("digests", True))
-        runs[case["id"]] = run_hashes(r)
+        runs[case["id"]] = run_record(r)
         print(case["id"], r["result"]["makespan"], len(r["trace"]))
     with open(os.path.join(HERE, "reference_runs.json"), "w") as fh:
         json.dump(runs, fh, indent=1, sort_keys=True)

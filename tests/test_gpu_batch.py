@@ -1,0 +1,101 @@
+"""Batch-level behaviour of the device engine at BASELINE scale."""
+import pytest
+
+from paper_2601_22705_b200 import abi, config, engine
+from tests.helpers import oracle_run
+from tests.parity import diff_all
+
+pytestmark = pytest.mark.gpu
+
+
+def _det(r: dict) -> dict:
+    """Result fields that must be deterministic (drops the timing counter)."""
+    return {k: v for k, v in r.items() if k != "device_cycles"}
+AGENT_ALL = abi.AGENT_FIELDS + ("finish_time", "finish_ordinal")
+
+
+@pytest.fixture(scope="module")
+def c4_batch():
+    pop = engine.Population(config.c1_toy().workload, 42)
+    scen = config.c4_sweep(4096)
+    specs = [engine.SimSpec.from_scenario(s, population=pop) for s in scen]
+    b = engine.Batch(specs)
+    b.run()
+    yield scen, pop, b
+    b.close()
+
+
+def test_c4_conservation_properties(c4_batch):
+    scen, pop, b = c4_batch
+    rs = b.results_raw()
+    assert len(rs) == 4096
+    for r in rs:
+        assert r.status == 0
+        assert r.agent_steps == 64 * 10          # work conservation
+        assert r.decoded_tokens == 64 * 10 * 256
+        device = r.ledger.prefill_fresh + r.ledger.prefill_recompute + r.ledger.decode
+        assert abs(device - r.device_busy) <= 1e-9 * max(1.0, r.device_busy)
+        assert r.device_busy <= r.makespan + 1e-9
+        assert r.workload_hash == 0xa0ac2d3c3bc97b20
+
+
+@pytest.mark.parametrize("k", [0, 1, 63, 64, 255, 256, 1023, 1024, 2047, 4095])
+def test_c4_sample_sims_bit_exact_vs_oracle(c4_batch, k):
+    scen, pop, b = c4_batch
+    g = dict(status=b.result(k)["status"], result=b.result(k), trace=b.trace(k),
+             agents=b.agent_stats(k))
+    o = oracle_run(scen[k], pop=pop.c)
+    assert diff_all(g, o, AGENT_ALL) == []
+
+
+def test_host_delivery_equals_device_outputs():
+    s = config.c1_toy("uncontrolled")
+    spec = engine.SimSpec.from_scenario(s)
+    a = engine.Batch([spec, spec])
+    a.run()
+    h = engine.Batch([spec, spec], host_outputs=True)
+    h.run()
+    for i in range(2):
+        assert _det(a.result(i)) == _det(h.result(i))
+        assert a.trace(i) == h.trace(i)
+        assert a.agent_stats(i) == h.agent_stats(i)
+
+
+def test_trace_overflow_regrows_and_reruns():
+    s = config.c1_toy("aimd")
+    spec = engine.SimSpec.from_scenario(s)
+    small = engine.Batch([spec], trace_capacity=8)
+    small.run()
+    big = engine.Batch([spec])
+    big.run()
+    assert small.trace(0) == big.trace(0) and len(big.trace(0)) == 1393
+
+
+def test_rerun_is_deterministic():
+    s = config.c1_toy("uncontrolled")
+    b = engine.Batch([engine.SimSpec.from_scenario(s)])
+    b.run()
+    first = (_det(b.result(0)), b.trace(0))
+    b.run()
+    assert (_det(b.result(0)), b.trace(0)) == first
+
+
+def test_horizon_partial_result():
+    s = config.c1_toy("uncontrolled")
+    s.engine.horizon = 100.0
+    b = engine.Batch([engine.SimSpec.from_scenario(s)])
+    st = b.run()
+    assert st == abi.KVG_ERR_HORIZON
+    r = b.result(0)
+    assert r["status"] == abi.KVG_ERR_HORIZON
+    o = oracle_run(s)
+    assert o["status"] == abi.KVG_ERR_HORIZON
+    assert r["makespan"] == o["result"]["makespan"]
+    assert b.trace(0) == o["trace"]
+
+
+def test_run_simulation_mirror():
+    s = config.c1_toy("aimd")
+    out = engine.run_simulation(engine.Population(s.workload, s.seed), *s.resolved()[:1],
+                                s.cost.to_abi(), s.resolved()[1].to_abi())
+    assert out["result"]["makespan"] == oracle_run(s)["result"]["makespan"]
