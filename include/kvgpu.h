@@ -204,12 +204,14 @@ typedef struct kvg_sim_result {
 
 /* Optional per-simulation event log (parity testing). */
 enum {
-  KVG_LOG_MATCH = 1,   /* agent, clock, a = matched tokens, b = lookups   */
+  KVG_LOG_MATCH = 1,   /* agent, clock, a = matched tokens, b = host_matched */
   KVG_LOG_INSERT = 2,  /* agent, clock, a = ok,            b = stored     */
   KVG_LOG_EVICT = 3,   /* clock,        a = needed,        b = reclaimed  */
   KVG_LOG_VICTIM = 4,  /*               a = page key,      b = stamp      */
   KVG_LOG_FINISH = 5,  /* agent,        a = time bits,     b = ordinal    */
-  KVG_LOG_DISCARD = 6  /* agent, clock, a = from page,     b = pages      */
+  KVG_LOG_DISCARD = 6, /* agent, clock, a = from page,     b = pages      */
+  KVG_LOG_RELOAD = 7   /* agent, clock, a = promoted,      b = offloaded tokens of
+                          the evictions the reload triggered                */
 };
 typedef struct kvg_log_record {
   uint32_t kind;
@@ -313,13 +315,16 @@ enum {
   KVG_OP_EVICT = 3,   /* evict(arg)                 -> r0 = reclaimed                  */
   KVG_OP_PIN = 4,     /* pin(seq, arg tokens)                                          */
   KVG_OP_UNPIN = 5,   /* unpin(seq, arg tokens)     -> status on underflow             */
-  KVG_OP_DISCARD = 6  /* discard_suffix(seq, arg)                                      */
+  KVG_OP_DISCARD = 6, /* discard_suffix(seq, arg)                                     */
+  KVG_OP_RELOAD = 7   /* reload(seq, from=arg, max=arg2) -> r0 = promoted, r1 = offloaded
+                         tokens of the evictions it triggered (offload mode)           */
 };
 typedef struct kvg_cache_op {
   uint32_t kind;
   uint32_t agent;
   uint64_t len; /* sequence length in tokens */
   uint64_t arg;
+  uint64_t arg2;
 } kvg_cache_op;
 typedef struct kvg_cache_op_result {
   int32_t status;

@@ -29,6 +29,8 @@
 #include <cstring>
 #include <deque>
 #include <limits>
+#include <map>
+#include <queue>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -54,30 +56,44 @@ struct StateError : std::logic_error {
 
 /* ======================= flat page cache (cache_tree.cpp) =================== */
 
+/* One page of the radix tree, named by (owner, page index). `host` is the
+ * node tier (cache_tree.hpp:37-61, Tier::kHost in offload mode); `bnd` marks
+ * a page that STARTS a radix node. Node boundaries are invisible to discard
+ * mode, but offload-mode reload promotes host nodes one node-chunk at a time
+ * (cache_tree.cpp:337-366), so the restatement tracks exactly where the
+ * reference splits or creates nodes. */
 struct Page {
   std::uint64_t stamp = 0;
   std::int64_t pins = 0;
+  bool host = false;
+  bool bnd = false;
 };
 
 struct FlatCache {
   std::uint64_t capacity = 0, ps = 1, prompt = 0, shared_pages = 0;
-  bool shared = false;
-  std::unordered_map<std::uint64_t, Page> pages;  // resident (device) pages
+  bool shared = false, offload = false;
+  std::unordered_map<std::uint64_t, Page> pages;  // every page in the tree (device or host)
+  std::set<std::uint64_t> order;  // offload mode: page keys in (owner, index) order
   std::uint64_t used = 0, clock = 0, discarded = 0, offloaded = 0;
   double hit_m = 0, hit_r = 0;
   std::uint64_t evict_calls = 0, evicted = 0;
-  std::uint64_t pinned = 0;  // resident pages with pins > 0 (evictable = used - pinned)
-  std::uint64_t dsum = 0;    // running sum of kvdigest::page_term over resident pages
+  std::uint64_t pinned = 0;  // DEVICE pages with pins > 0 (evictable = used - pinned)
+  std::uint64_t dsum = 0;    // running sum of kvdigest::page_term over all pages
+  /* owner (agent+1) whose page at index shared_pages still belongs to the node
+   * holding the last shared page (the first agent to insert past the shared
+   * prompt creates one leaf spanning both), 0 if none. */
+  std::uint64_t glued = 0;
   std::vector<std::pair<std::uint64_t, std::uint64_t>>* victims = nullptr;
   std::vector<kvg_log_record>* log = nullptr;  // EVICT + VICTIM records
   std::uint32_t log_agent = 0;
 
-  void init(std::uint64_t cap, std::uint64_t page, std::uint64_t p, bool sh) {
+  void init(std::uint64_t cap, std::uint64_t page, std::uint64_t p, bool sh, bool off) {
     if (cap == 0 || page == 0) throw std::invalid_argument("capacity and page size must be > 0");
     capacity = cap;
     ps = page;
     prompt = p;
     shared = sh;
+    offload = off;
     shared_pages = sh ? p / page : 0;  // pages wholly inside the shared prompt
   }
   std::uint64_t key(std::uint32_t a, std::uint64_t k) const {
@@ -86,119 +102,309 @@ struct FlatCache {
   }
   static std::uint64_t term(std::uint64_t key, const Page& p) {
     return kvdigest::page_term(key >> 32, key & 0xffffffffULL, p.stamp,
-                               static_cast<std::uint64_t>(p.pins), 0);
-  }
-  void restamp(std::uint64_t key, Page* p, std::uint64_t stamp) {
-    dsum -= term(key, *p);
-    p->stamp = stamp;
-    dsum += term(key, *p);
-  }
-  void add_page(std::uint64_t key, std::uint64_t stamp) {
-    Page pg{stamp, 0};
-    pages.emplace(key, pg);
-    dsum += term(key, pg);
-    ++used;
-  }
-  void drop_page(std::unordered_map<std::uint64_t, Page>::iterator it) {
-    dsum -= term(it->first, it->second);
-    if (it->second.pins > 0) --pinned;
-    pages.erase(it);
-    --used;
+                               static_cast<std::uint64_t>(p.pins), p.host ? 1 : 0);
   }
   Page* find(std::uint32_t a, std::uint64_t k) {
     auto it = pages.find(key(a, k));
     return it == pages.end() ? nullptr : &it->second;
   }
-  std::uint64_t first_miss(std::uint32_t a, std::uint64_t n) {
+  Page* find_key(std::uint64_t kk) {
+    auto it = pages.find(kk);
+    return it == pages.end() ? nullptr : &it->second;
+  }
+  /* Applies f to a page while keeping the digest sum and counters exact. */
+  template <typename F>
+  void modify(std::uint64_t kk, Page* p, F&& f) {
+    dsum -= term(kk, *p);
+    const bool was_dev = !p->host, was_pin = p->pins > 0;
+    f(*p);
+    if (was_dev && was_pin) --pinned;
+    if (!p->host && p->pins > 0) ++pinned;
+    if (was_dev && p->host) --used;
+    if (!was_dev && !p->host) ++used;
+    dsum += term(kk, *p);
+  }
+  void add_page(std::uint64_t kk, std::uint64_t stamp, bool bnd) {
+    Page pg;
+    pg.stamp = stamp;
+    pg.bnd = bnd;
+    pages.emplace(kk, pg);
+    if (offload) order.insert(kk);
+    dsum += term(kk, pg);
+    ++used;
+    if (!bnd && shared_pages > 0 && (kk & 0xffffffffULL) == shared_pages && (kk >> 32) != 0)
+      glued = kk >> 32;
+  }
+  void drop_page(std::unordered_map<std::uint64_t, Page>::iterator it) {
+    dsum -= term(it->first, it->second);
+    if (!it->second.host) {
+      if (it->second.pins > 0) --pinned;
+      --used;
+    }
+    if (glued != 0 && it->first == ((glued << 32) | shared_pages)) glued = 0;
+    if (offload) order.erase(it->first);
+    pages.erase(it);
+  }
+  void set_bnd(std::uint64_t kk, Page* p) {
+    if (p->bnd) return;
+    p->bnd = true;
+    if (glued != 0 && kk == ((glued << 32) | shared_pages)) glued = 0;
+  }
+  /* First page index in [0, n) absent from agent a's path (the tree is
+   * prefix-closed along every path). */
+  std::uint64_t walk(std::uint32_t a, std::uint64_t n) {
     std::uint64_t k = 0;
     while (k < n && find(a, k) != nullptr) ++k;
     return k;
   }
+  /* split_node at the end of a walk over [0, f) that stopped at f (n = the
+   * walk's limit): the node holding page f-1 is split where it leaves the
+   * path (cache_tree.cpp:128, 212, 350, 415). Two ways a node continues past
+   * the walked pages: the shared prompt's node glued to another agent's
+   * private pages (whenever a walk covers the whole shared prompt), or the
+   * agent's own next page when the walk stopped at its length limit. */
+  void split_walk_end(std::uint32_t a, std::uint64_t f, std::uint64_t n) {
+    if (shared_pages > 0 && glued != 0 && glued != std::uint64_t(a) + 1 && f >= shared_pages) {
+      const std::uint64_t kk = (glued << 32) | shared_pages;
+      set_bnd(kk, find_key(kk));
+    }
+    if (f == n && f > 0) {
+      const std::uint64_t kk = key(a, f);
+      if (Page* p = find_key(kk)) set_bnd(kk, p);
+    }
+  }
+  /* split_node so a node boundary falls before page q of a's path (whatever
+   * page continues the node holding page q-1 starts a new node). */
+  void split_before(std::uint32_t a, std::uint64_t q) {
+    if (q == 0) return;
+    const std::uint64_t kk = key(a, q);
+    if (Page* p = find_key(kk)) {
+      if (!p->bnd) {
+        set_bnd(kk, p);
+        return;
+      }
+    }
+    if (shared_pages > 0 && q == shared_pages && glued != 0) {
+      const std::uint64_t gk = (glued << 32) | shared_pages;
+      set_bnd(gk, find_key(gk));
+    }
+  }
+  /* Does the node holding page q-1 of a's path continue past it? */
+  bool continues(std::uint32_t a, std::uint64_t q) {
+    if (q == 0) return false;
+    if (Page* p = find(a, q))
+      if (!p->bnd) return true;
+    return shared_pages > 0 && q == shared_pages && glued != 0 && glued != std::uint64_t(a) + 1;
+  }
 
-  /* match_prefix, cache_tree.cpp:114-142 (discard mode: no host phase). */
-  std::uint64_t match(std::uint32_t a, std::uint64_t len) {
+  /* match_prefix, cache_tree.cpp:114-142: device pages until the first host
+   * page are matched (and refreshed); every later page on the path counts as
+   * host_matched (Q4: device pages below a host node are not refreshed). */
+  std::uint64_t match(std::uint32_t a, std::uint64_t len, std::uint64_t* host_matched) {
     const std::uint64_t now = ++clock;
-    const std::uint64_t f = first_miss(a, len / ps);
-    for (std::uint64_t k = 0; k < f; ++k) restamp(key(a, k), find(a, k), now);
-    hit_m += static_cast<double>(f * ps);
+    const std::uint64_t n = len / ps;
+    const std::uint64_t f = walk(a, n);
+    split_walk_end(a, f, n);
+    std::uint64_t d = 0;
+    for (; d < f; ++d) {
+      const std::uint64_t kk = key(a, d);
+      Page* p = find_key(kk);
+      if (p->host) break;
+      modify(kk, p, [&](Page& q) { q.stamp = now; });
+    }
+    if (host_matched) *host_matched = (f - d) * ps;
+    hit_m += static_cast<double>(d * ps);
     hit_r += static_cast<double>(len);
-    return f * ps;
+    return d * ps;
   }
 
-  /* descendants-first order: (stamp asc, page index desc). */
-  static bool lru_before(const std::pair<std::uint64_t, Page*>& x,
-                         const std::pair<std::uint64_t, Page*>& y) {
-    if (x.second->stamp != y.second->stamp) return x.second->stamp < y.second->stamp;
-    return (x.first & 0xffffffffULL) > (y.first & 0xffffffffULL);
+  /* Eviction key: (M asc, page index desc) with M the newest device stamp in
+   * the page's subtree. In discard mode stamps never increase
+   * from root to leaf, so M is the page's own stamp; offload-mode reloads
+   * stamp promoted chunks newer than their parents, and a node can only be
+   * taken once its device subtree is gone, which M expresses per page. */
+  struct Cand {
+    std::uint64_t m, idx, kk;
+    Page* p;
+  };
+  static bool lru_before(const Cand& x, const Cand& y) {
+    if (x.m != y.m) return x.m < y.m;
+    if (x.idx != y.idx) return x.idx > y.idx;
+    return x.kk < y.kk;
+  }
+  /* Candidates with their keys. Offload: one descending pass over the
+   * ordered page keys computes M as a suffix max along every private chain;
+   * the shared chain's pages also cover every private chain below it. */
+  void candidates(std::vector<Cand>& cand) {
+    if (!offload) {
+      for (auto& kv : pages)
+        if (kv.second.pins == 0)
+          cand.push_back(Cand{kv.second.stamp, kv.first & 0xffffffffULL, kv.first, &kv.second});
+      return;
+    }
+    std::uint64_t run = 0, cur = ~0ULL, below_shared = 0;
+    for (auto it = order.rbegin(); it != order.rend(); ++it) {
+      const std::uint64_t kk = *it, owner = kk >> 32;
+      if (owner != cur) {
+        if (cur != ~0ULL && cur != 0) below_shared = std::max(below_shared, run);
+        cur = owner;
+        run = owner == 0 ? below_shared : 0;
+      }
+      Page& p = pages.find(kk)->second;
+      if (!p.host) run = std::max(run, p.stamp);
+      if (!p.host && p.pins == 0) cand.push_back(Cand{run, kk & 0xffffffffULL, kk, &p});
+    }
   }
 
-  /* evict, cache_tree.cpp:270-319 in its per-page form. */
-  std::uint64_t evict(std::uint64_t needed) {
+  /* evict, cache_tree.cpp:270-319 in its per-page form. Offload victims move
+   * to the host tier (their pages stay in the tree); discard victims leave. */
+  std::uint64_t evict(std::uint64_t needed, std::uint64_t* offl_tokens = nullptr) {
     if (needed == 0) return 0;
     ++evict_calls;
     if (used == pinned) {  // nothing evictable: the common stall-storm case
       if (log) log->push_back(kvg_log_record{KVG_LOG_EVICT, log_agent, clock, needed, 0});
       return 0;
     }
-    std::vector<std::pair<std::uint64_t, Page*>> cand;
-    for (auto& kv : pages)
-      if (kv.second.pins == 0) cand.emplace_back(kv.first, &kv.second);
+    std::vector<Cand> cand;
+    candidates(cand);
     std::uint64_t take = std::min<std::uint64_t>(needed, cand.size());
     if (log) log->push_back(kvg_log_record{KVG_LOG_EVICT, log_agent, clock, needed, take});
     if (take == 0) return 0;
     std::partial_sort(cand.begin(), cand.begin() + take, cand.end(), lru_before);
     for (std::uint64_t i = 0; i < take; ++i) {
-      if (victims) victims->emplace_back(cand[i].first, cand[i].second->stamp);
+      const Cand& c = cand[i];
+      if (victims) victims->emplace_back(c.kk, c.p->stamp);
       if (log)
-        log->push_back(kvg_log_record{KVG_LOG_VICTIM, log_agent, clock, cand[i].first,
-                                      cand[i].second->stamp});
-      drop_page(pages.find(cand[i].first));
+        log->push_back(kvg_log_record{KVG_LOG_VICTIM, log_agent, clock, c.kk, c.p->stamp});
+    }
+    // the last node popped is split when only its tail was taken
+    // (cache_tree.cpp:287-290): its first victim page starts a new node
+    set_bnd(cand[take - 1].kk, cand[take - 1].p);
+    for (std::uint64_t i = 0; i < take; ++i) {
+      const Cand& c = cand[i];
+      if (offload) modify(c.kk, c.p, [](Page& q) { q.host = true; });
+      else drop_page(pages.find(c.kk));
     }
     evicted += take;
-    discarded += take * ps;
+    if (offload) {
+      offloaded += take * ps;
+      if (offl_tokens) *offl_tokens += take * ps;
+    } else {
+      discarded += take * ps;
+    }
     return take;
   }
 
-  /* insert, cache_tree.cpp:170-228. Returns ok; *inserted = new slots. */
+  /* count_missing_slots, cache_tree.cpp:144-168: absent pages plus host
+   * pages on the path. */
+  std::uint64_t missing(std::uint32_t a, std::uint64_t n) {
+    const std::uint64_t f = walk(a, n);
+    std::uint64_t m = n - f;
+    if (offload)
+      for (std::uint64_t k = 0; k < f; ++k)
+        if (find(a, k)->host) ++m;
+    return m;
+  }
+
+  /* insert, cache_tree.cpp:170-228. Returns ok; *inserted = new device slots
+   * (created + promoted from host). */
   bool insert(std::uint32_t a, std::uint64_t len, std::uint64_t* inserted,
-              std::uint64_t* evicted) {
+              std::uint64_t* evicted_pages, std::uint64_t* offl_tokens = nullptr) {
     const std::uint64_t n = len / ps;
     if (inserted) *inserted = 0;
     if (n == 0) return true;
     for (;;) {
-      std::uint64_t need = n - first_miss(a, n);  // count_missing_slots:144-168
+      std::uint64_t need = missing(a, n);
       std::uint64_t free_slots = capacity - used;
       if (need <= free_slots) break;
-      std::uint64_t ev = evict(need - free_slots);
-      if (evicted) *evicted += ev;
+      std::uint64_t ev = evict(need - free_slots, offl_tokens);
+      if (evicted_pages) *evicted_pages += ev;
       if (ev == 0) return false;  // evictions so far persist (Q3)
     }
     const std::uint64_t now = ++clock;
-    for (std::uint64_t k = 0; k < n; ++k) {
-      Page* p = find(a, k);
-      if (p == nullptr) {
-        add_page(key(a, k), now);
-        if (inserted) ++*inserted;
-      } else {
-        restamp(key(a, k), p, now);
-      }
+    const std::uint64_t f = walk(a, n);
+    split_walk_end(a, f, n);
+    for (std::uint64_t k = 0; k < f; ++k) {
+      const std::uint64_t kk = key(a, k);
+      Page* p = find_key(kk);
+      if (p->host && inserted) ++*inserted;
+      modify(kk, p, [&](Page& q) {
+        q.host = false;
+        q.stamp = now;
+      });
+    }
+    for (std::uint64_t k = f; k < n; ++k) {
+      add_page(key(a, k), now, k == f);
+      if (inserted) ++*inserted;
     }
     return true;
   }
 
-  /* pin / unpin, cache_tree.cpp:370-402 (page-aligned lengths). */
+  /* reload, cache_tree.cpp:321-368: promote host nodes from `from`, one
+   * node-chunk at a time, evicting per chunk; a chunk that still does not fit
+   * stops the reload. Promoted chunks can be evicted again by later chunks'
+   * evictions (quirk Q1). Returns promoted tokens. */
+  std::uint64_t reload(std::uint32_t a, std::uint64_t len, std::uint64_t from,
+                       std::uint64_t max_tokens, std::uint64_t* offl_tokens) {
+    if (from >= len || max_tokens == 0) return 0;
+    // walk to `from` (cache_tree.cpp:326-334): it must lie on the cached
+    // path, on a node boundary
+    if (from % ps != 0) throw StateError("reload offset is not a node boundary");
+    for (std::uint64_t k = 0; k < from / ps; ++k)
+      if (find(a, k) == nullptr) throw StateError("reload offset is not on a cached path");
+    if (continues(a, from / ps)) throw StateError("reload offset is not a node boundary");
+    const std::uint64_t now = ++clock;
+    const std::uint64_t n = len / ps;
+    std::uint64_t p = from / ps, promoted = 0;
+    while (p < n && promoted < max_tokens) {
+      Page* head = find(a, p);
+      if (head == nullptr || !head->host) break;
+      std::uint64_t j = p + 1;
+      while (j < n) {
+        Page* q = find(a, j);
+        if (q == nullptr || q->bnd) break;
+        ++j;
+      }
+      bool full = !continues(a, j);
+      std::uint64_t ka = j - p;
+      const std::uint64_t want = (max_tokens - promoted) / ps;
+      if (ka > want) {
+        ka = want;
+        full = false;
+      }
+      if (ka == 0) break;
+      if (!full) split_before(a, p + ka);
+      if (capacity - used < ka) {
+        evict(ka - (capacity - used), offl_tokens);
+        if (capacity - used < ka) break;
+      }
+      for (std::uint64_t k = p; k < p + ka; ++k) {
+        const std::uint64_t kk = key(a, k);
+        modify(kk, find_key(kk), [&](Page& q) {
+          q.host = false;
+          q.stamp = now;
+        });
+      }
+      promoted += ka * ps;
+      p += ka;
+      if (!full) break;
+    }
+    return promoted;
+  }
+
+  /* pin / unpin, cache_tree.cpp:370-402: every node covering [0, len). */
   void pin(std::uint32_t a, std::uint64_t len, int delta) {
     if (len % ps != 0) throw std::invalid_argument("pin length not on a node boundary");
-    for (std::uint64_t k = 0; k < len / ps; ++k) {
+    const std::uint64_t n = len / ps;
+    for (std::uint64_t k = 0; k < n; ++k) {
       Page* p = find(a, k);
       if (p == nullptr) throw StateError("pin path missing from tree");
       if (delta < 0 && p->pins == 0) throw StateError("unpin on a node with zero pin count");
+    }
+    if (continues(a, n)) throw std::invalid_argument("pin length not on a node boundary");
+    for (std::uint64_t k = 0; k < n; ++k) {
       const std::uint64_t kk = key(a, k);
-      dsum -= term(kk, *p);
-      if (p->pins == 0 && delta > 0) ++pinned;
-      p->pins += delta;
-      if (p->pins == 0) --pinned;
-      dsum += term(kk, *p);
+      modify(kk, find_key(kk), [&](Page& q) { q.pins += delta; });
     }
   }
 
@@ -207,15 +413,17 @@ struct FlatCache {
     from = (from + ps - 1) / ps * ps;  // page_ceil (Q2: straddling page survives)
     if (from >= len) return;
     const std::uint64_t fp = from / ps;
-    if (fp >= len / ps) return;            // no full page at `from`
-    for (std::uint64_t k = 0; k <= fp; ++k)  // path to `from` and the branch head
+    for (std::uint64_t k = 0; k < fp; ++k)  // path to `from`
       if (find(a, k) == nullptr) return;
+    split_before(a, fp);  // the node straddling `from` is split there (:415)
+    if (fp >= len / ps) return;  // no full page at `from`: no branch
+    if (find(a, fp) == nullptr) return;
     // the branch subtree: pages on any path through page fp
     std::vector<std::uint64_t> doomed;
     const std::uint64_t head_owner = key(a, fp) >> 32;
     if (head_owner != 0) {
-      // private head: the subtree is this agent's chain from fp (resident
-      // pages of a chain are a contiguous prefix: walk until the first miss)
+      // private head: this agent's chain from fp (present pages of a chain
+      // are a contiguous prefix: walk until the first miss)
       for (std::uint64_t k = fp;; ++k) {
         auto it = pages.find((head_owner << 32) | k);
         if (it == pages.end()) break;
@@ -235,6 +443,451 @@ struct FlatCache {
   }
 
   std::uint64_t digest() const {  // O(1): dsum is maintained incrementally
+    std::uint64_t h = kvdigest::fold(0x1234, dsum);
+    h = kvdigest::fold(h, used);
+    h = kvdigest::fold(h, clock);
+    h = kvdigest::fold(h, kvdigest::dbits(hit_m));
+    h = kvdigest::fold(h, kvdigest::dbits(hit_r));
+    h = kvdigest::fold(h, discarded);
+    h = kvdigest::fold(h, offloaded);
+    return h;
+  }
+};
+
+/* ================== node-level tree cache (offload mode) ==================== */
+
+/* Offload-mode restatement at NODE granularity. Every reference algorithm
+ * (cache_tree.cpp) is followed step for step, including the node
+ * bookkeeping that decides eviction order: splits, ordinals, pin counts and
+ * children_with_device. That last counter is not self-consistent in offload
+ * mode: a reload (or insert) that promotes a host node whose subtree already
+ * holds a device node (quirk Q1) calls propagate_gain again and double-counts
+ * it in the parent (cache_tree.cpp:94-102, 357-361), after which the parent
+ * can never become an eviction frontier. A per-page model cannot see that,
+ * so offload mode keeps nodes. Segments are (first page, page count) along
+ * the population's token scheme: pages below the shared prompt belong to
+ * owner 0, the rest to the node's `tail` owner. */
+struct TNode {
+  std::uint32_t parent = 0;
+  std::uint64_t start = 0, npages = 0;
+  std::uint64_t tail = 0;  // owner (agent+1) of the pages at or past the shared prompt
+  std::map<std::uint64_t, std::uint32_t> children;  // child head page key -> node
+  std::uint64_t last_access = 0, ordinal = 0, device_slots = 0;
+  int pin_count = 0, cwd = 0;  // cwd = children_with_device
+  bool host = false, alive = true;
+  bool subtree_has_device() const { return device_slots > 0 || cwd > 0; }
+};
+
+struct TreeCache {
+  std::uint64_t capacity = 0, ps = 1, shared_pages = 0;
+  bool offload = true;
+  std::vector<TNode> nodes;  // nodes[0] = root
+  std::vector<std::uint32_t> free_ids;
+  std::uint64_t used = 0, clock = 0, discarded = 0, offloaded = 0, next_ordinal = 0;
+  double hit_m = 0, hit_r = 0;
+  std::uint64_t evict_calls = 0, evicted = 0;
+  std::uint64_t dsum = 0;
+  std::vector<std::pair<std::uint64_t, std::uint64_t>>* victims = nullptr;
+  std::vector<kvg_log_record>* log = nullptr;
+  std::uint32_t log_agent = 0;
+
+  void init(std::uint64_t cap, std::uint64_t page, std::uint64_t p, bool sh, bool off) {
+    if (cap == 0 || page == 0) throw std::invalid_argument("capacity and page size must be > 0");
+    capacity = cap;
+    ps = page;
+    shared_pages = sh ? p / page : 0;
+    offload = off;
+    nodes.assign(1, TNode{});
+  }
+  std::uint64_t key(std::uint32_t a, std::uint64_t k) const {
+    std::uint64_t owner = k < shared_pages ? 0 : std::uint64_t(a) + 1;
+    return (owner << 32) | k;
+  }
+  std::uint64_t nkey(const TNode& n, std::uint64_t k) const {
+    return ((k < shared_pages ? 0 : n.tail) << 32) | k;
+  }
+  std::uint64_t terms(const TNode& n) const {
+    std::uint64_t s = 0;
+    for (std::uint64_t k = n.start; k < n.start + n.npages; ++k) {
+      const std::uint64_t kk = nkey(n, k);
+      s += kvdigest::page_term(kk >> 32, k, n.last_access, static_cast<std::uint64_t>(n.pin_count),
+                               n.host ? 1 : 0);
+    }
+    return s;
+  }
+  template <typename F>
+  void modify(std::uint32_t id, F&& f) {
+    dsum -= terms(nodes[id]);
+    f(nodes[id]);
+    dsum += terms(nodes[id]);
+  }
+  std::uint32_t new_node() {
+    if (!free_ids.empty()) {
+      std::uint32_t id = free_ids.back();
+      free_ids.pop_back();
+      nodes[id] = TNode{};
+      return id;
+    }
+    nodes.emplace_back();
+    return static_cast<std::uint32_t>(nodes.size() - 1);
+  }
+  /* find_child (cache_tree.cpp:56-66): needs a full page of the sequence. */
+  std::uint32_t find_child(std::uint32_t node, std::uint32_t a, std::uint64_t p,
+                           std::uint64_t n_full) const {
+    if (p >= n_full) return 0;
+    auto it = nodes[node].children.find(key(a, p));
+    return it == nodes[node].children.end() ? 0 : it->second;
+  }
+  /* common_len in whole pages (a partial trailing page never counts). */
+  std::uint64_t common(std::uint32_t c, std::uint32_t a, std::uint64_t p, std::uint64_t n_full) const {
+    const TNode& n = nodes[c];
+    std::uint64_t k = std::min(n.npages, n_full - p);
+    if (n.tail != std::uint64_t(a) + 1) {
+      const std::uint64_t sh = shared_pages > p ? shared_pages - p : 0;
+      k = std::min(k, sh);
+    }
+    return k;
+  }
+  /* split_node, cache_tree.cpp:68-92 (offset in pages). */
+  std::uint32_t split(std::uint32_t id, std::uint64_t off) {
+    const std::uint32_t sid = new_node();
+    TNode& node = nodes[id];
+    TNode& s = nodes[sid];
+    s.start = node.start + off;
+    s.npages = node.npages - off;
+    s.tail = node.tail;
+    s.children = std::move(node.children);
+    for (auto& kv : s.children) nodes[kv.second].parent = sid;
+    s.parent = id;
+    s.last_access = node.last_access;
+    s.ordinal = next_ordinal++;
+    s.host = node.host;
+    s.pin_count = node.pin_count;
+    s.cwd = node.cwd;
+    if (!node.host) {
+      s.device_slots = node.device_slots - off;
+      node.device_slots = off;
+    }
+    node.npages = off;
+    node.children.clear();
+    node.cwd = s.subtree_has_device() ? 1 : 0;
+    node.children.emplace(nkey(s, s.start), sid);
+    return sid;  // page attributes unchanged: the digest sum is unchanged
+  }
+  void propagate_gain(std::uint32_t id) {  // cache_tree.cpp:94-102
+    std::uint32_t p = nodes[id].parent;
+    for (;;) {
+      TNode& pn = nodes[p];
+      const bool had = pn.subtree_has_device();
+      pn.cwd += 1;
+      if (had || p == 0) break;  // the root has no parent
+      p = pn.parent;
+    }
+  }
+  void propagate_loss(std::uint32_t id) {  // cache_tree.cpp:104-112
+    std::uint32_t p = nodes[id].parent;
+    for (;;) {
+      TNode& pn = nodes[p];
+      pn.cwd -= 1;
+      if (pn.subtree_has_device() || p == 0) break;
+      p = pn.parent;
+    }
+  }
+
+  /* match_prefix, cache_tree.cpp:114-142 */
+  std::uint64_t match(std::uint32_t a, std::uint64_t len, std::uint64_t* host_matched) {
+    const std::uint64_t now = ++clock;
+    const std::uint64_t n = len / ps;
+    std::uint32_t node = 0;
+    std::uint64_t pos = 0, matched = 0, hm = 0;
+    bool host_phase = false;
+    while (pos < n) {
+      const std::uint32_t c = find_child(node, a, pos, n);
+      if (c == 0) break;
+      if (nodes[c].host) host_phase = true;
+      const std::uint64_t ka = common(c, a, pos, n);
+      const bool full = ka == nodes[c].npages;
+      if (ka == 0) break;
+      if (!full) split(c, ka);
+      if (host_phase) {
+        hm += ka;
+      } else {
+        modify(c, [&](TNode& x) { x.last_access = now; });
+        matched += ka;
+      }
+      pos += ka;
+      node = c;
+      if (!full) break;
+    }
+    hit_m += static_cast<double>(matched * ps);
+    hit_r += static_cast<double>(len);
+    if (host_matched) *host_matched = hm * ps;
+    return matched * ps;
+  }
+
+  std::uint64_t missing(std::uint32_t a, std::uint64_t n) const {  // cache_tree.cpp:144-168
+    std::uint32_t node = 0;
+    std::uint64_t pos = 0, m = 0;
+    while (pos < n) {
+      const std::uint32_t c = find_child(node, a, pos, n);
+      if (c == 0) return m + (n - pos);
+      const std::uint64_t ka = common(c, a, pos, n);
+      const bool full = ka == nodes[c].npages;
+      if (ka == 0) return m;
+      if (nodes[c].host) m += ka;
+      pos += ka;
+      node = c;
+      if (!full) return m + (n - pos);
+    }
+    return m;
+  }
+
+  bool is_frontier(std::uint32_t id) const {  // cache_tree.cpp:230-234
+    const TNode& n = nodes[id];
+    return id != 0 && !n.host && n.device_slots > 0 && n.pin_count == 0 && n.cwd == 0;
+  }
+  using Ent = std::pair<std::pair<std::uint64_t, std::uint64_t>, std::uint32_t>;
+  void collect_frontier(std::uint32_t id, std::vector<Ent>& out) const {  // :236-249
+    for (const auto& kv : nodes[id].children) {
+      const std::uint32_t c = kv.second;
+      if (!nodes[c].subtree_has_device()) continue;
+      if (is_frontier(c)) {
+        out.push_back({{nodes[c].last_access, nodes[c].ordinal}, c});
+        continue;
+      }
+      collect_frontier(c, out);
+    }
+  }
+  void free_subtree(std::uint32_t id, std::uint64_t* toks) {
+    for (auto& kv : nodes[id].children) free_subtree(kv.second, toks);
+    if (toks) *toks += nodes[id].npages * ps;
+    dsum -= terms(nodes[id]);
+    nodes[id].alive = false;
+    nodes[id].children.clear();
+    free_ids.push_back(id);
+  }
+
+  /* evict, cache_tree.cpp:270-319 */
+  std::uint64_t evict(std::uint64_t needed, std::uint64_t* offl_tokens = nullptr) {
+    if (needed == 0) return 0;
+    ++evict_calls;
+    std::vector<Ent> init;
+    collect_frontier(0, init);
+    std::priority_queue<Ent, std::vector<Ent>, std::greater<Ent>> heap(std::greater<Ent>(),
+                                                                       std::move(init));
+    std::uint64_t reclaimed = 0;
+    const std::size_t log0 = log ? log->size() : 0;
+    if (log) log->push_back(kvg_log_record{KVG_LOG_EVICT, log_agent, clock, needed, 0});
+    while (reclaimed < needed && !heap.empty()) {
+      auto [stamp, id] = heap.top();
+      heap.pop();
+      if (!is_frontier(id) || nodes[id].last_access != stamp.first ||
+          nodes[id].ordinal != stamp.second)
+        continue;
+      const std::uint64_t take = std::min(nodes[id].device_slots, needed - reclaimed);
+      std::uint32_t v = id;
+      if (take < nodes[id].device_slots) v = split(id, nodes[id].npages - take);
+      const TNode& vn = nodes[v];
+      for (std::uint64_t k = vn.start + vn.npages; k-- > vn.start;) {  // record_victims
+        const std::uint64_t kk = nkey(vn, k);
+        if (victims) victims->emplace_back(kk, vn.last_access);
+        if (log) log->push_back(kvg_log_record{KVG_LOG_VICTIM, log_agent, clock, kk, vn.last_access});
+      }
+      used -= vn.device_slots;
+      reclaimed += vn.device_slots;
+      const std::uint32_t parent = vn.parent;
+      if (offload) {
+        const std::uint64_t toks = vn.npages * ps;
+        offloaded += toks;
+        if (offl_tokens) *offl_tokens += toks;
+        modify(v, [](TNode& x) {
+          x.device_slots = 0;
+          x.host = true;
+        });
+        propagate_loss(v);
+      } else {
+        std::uint64_t dropped = 0;
+        propagate_loss(v);
+        const std::uint64_t head = nkey(nodes[v], nodes[v].start);
+        free_subtree(v, &dropped);
+        discarded += dropped;
+        nodes[parent].children.erase(head);
+      }
+      if (is_frontier(parent))
+        heap.push({{nodes[parent].last_access, nodes[parent].ordinal}, parent});
+    }
+    if (log) (*log)[log0].b = reclaimed;
+    evicted += reclaimed;
+    return reclaimed;
+  }
+
+  /* insert, cache_tree.cpp:170-228 */
+  bool insert(std::uint32_t a, std::uint64_t len, std::uint64_t* inserted,
+              std::uint64_t* evicted_pages, std::uint64_t* offl_tokens = nullptr) {
+    const std::uint64_t n = len / ps;
+    if (inserted) *inserted = 0;
+    if (n == 0) return true;
+    for (;;) {
+      const std::uint64_t need = missing(a, n);
+      const std::uint64_t free_slots = capacity - used;
+      if (need <= free_slots) break;
+      const std::uint64_t ev = evict(need - free_slots, offl_tokens);
+      if (evicted_pages) *evicted_pages += ev;
+      if (ev == 0) return false;
+    }
+    const std::uint64_t now = ++clock;
+    std::uint32_t node = 0;
+    std::uint64_t pos = 0;
+    while (pos < n) {
+      const std::uint32_t c = find_child(node, a, pos, n);
+      if (c == 0) {
+        const std::uint32_t l = new_node();
+        TNode& ln = nodes[l];
+        ln.start = pos;
+        ln.npages = n - pos;
+        ln.tail = std::uint64_t(a) + 1;
+        ln.parent = node;
+        ln.last_access = now;
+        ln.ordinal = next_ordinal++;
+        ln.device_slots = n - pos;
+        dsum += terms(ln);
+        used += ln.device_slots;
+        if (inserted) *inserted += ln.device_slots;
+        nodes[node].children.emplace(key(a, pos), l);
+        propagate_gain(l);
+        pos = n;
+        break;
+      }
+      const std::uint64_t ka = common(c, a, pos, n);
+      const bool full = ka == nodes[c].npages;
+      if (ka == 0) break;
+      if (!full) split(c, ka);
+      if (nodes[c].host) {
+        const std::uint64_t pages = nodes[c].npages;
+        modify(c, [&](TNode& x) {
+          x.host = false;
+          x.device_slots = pages;
+        });
+        used += pages;
+        if (inserted) *inserted += pages;
+        propagate_gain(c);
+      }
+      modify(c, [&](TNode& x) { x.last_access = now; });
+      pos += ka;
+      node = c;
+    }
+    return true;
+  }
+
+  /* reload, cache_tree.cpp:321-368 */
+  std::uint64_t reload(std::uint32_t a, std::uint64_t len, std::uint64_t from,
+                       std::uint64_t max_tokens, std::uint64_t* offl_tokens) {
+    if (from >= len || max_tokens == 0) return 0;
+    const std::uint64_t n = len / ps;
+    std::uint32_t node = 0;
+    std::uint64_t pos = 0;  // tokens
+    while (pos < from) {
+      const std::uint32_t c = (pos % ps == 0) ? find_child(node, a, pos / ps, n) : 0;
+      if (c == 0) throw StateError("reload offset is not on a cached path");
+      if (nodes[c].npages * ps > from - pos) throw StateError("reload offset is not a node boundary");
+      pos += nodes[c].npages * ps;
+      node = c;
+    }
+    const std::uint64_t now = ++clock;
+    std::uint64_t promoted = 0;
+    while (pos < len && promoted < max_tokens) {
+      const std::uint32_t c = find_child(node, a, pos / ps, n);
+      if (c == 0) break;
+      if (!nodes[c].host) break;
+      std::uint64_t ka = common(c, a, pos / ps, n);
+      bool full = ka == nodes[c].npages;
+      const std::uint64_t want = (max_tokens - promoted) / ps;
+      if (ka > want) {
+        ka = want;
+        full = false;
+      }
+      if (ka == 0) break;
+      if (ka < nodes[c].npages) split(c, ka);
+      const std::uint64_t pages = ka;
+      if (capacity - used < pages) {
+        evict(pages - (capacity - used), offl_tokens);
+        if (capacity - used < pages) break;
+      }
+      modify(c, [&](TNode& x) {
+        x.host = false;
+        x.device_slots = pages;
+        x.last_access = now;
+      });
+      used += pages;
+      propagate_gain(c);
+      promoted += ka * ps;
+      pos += ka * ps;
+      node = c;
+      if (!full) break;
+    }
+    return promoted;
+  }
+
+  /* pin / unpin, cache_tree.cpp:370-402 */
+  void pin(std::uint32_t a, std::uint64_t len, int delta) {
+    const std::uint64_t n = len / ps;
+    std::uint32_t node = 0;
+    std::uint64_t pos = 0;  // tokens
+    std::vector<std::uint32_t> path;
+    while (pos < len) {
+      const std::uint32_t c = (pos % ps == 0) ? find_child(node, a, pos / ps, (len + ps - 1) / ps) : 0;
+      if (c == 0) throw StateError(delta > 0 ? "pin path missing from tree" : "unpin path missing from tree");
+      if (pos + nodes[c].npages * ps > len)
+        throw std::invalid_argument("pin length not on a node boundary");
+      if (delta < 0 && nodes[c].pin_count == 0)
+        throw StateError("unpin on a node with zero pin count");
+      path.push_back(c);
+      pos += nodes[c].npages * ps;
+      node = c;
+    }
+    (void)n;
+    for (std::uint32_t c : path) modify(c, [&](TNode& x) { x.pin_count += delta; });
+  }
+
+  /* discard_suffix, cache_tree.cpp:404-437 */
+  void discard_suffix(std::uint32_t a, std::uint64_t len, std::uint64_t from) {
+    from = (from + ps - 1) / ps * ps;
+    if (from >= len) return;
+    const std::uint64_t n = len / ps;
+    std::uint32_t node = 0;
+    std::uint64_t pos = 0;  // tokens
+    while (pos < from) {
+      const std::uint32_t c = find_child(node, a, pos / ps, n);
+      if (c == 0) return;
+      const std::uint64_t kp = common(c, a, pos / ps, n);
+      if (kp < nodes[c].npages && pos + kp * ps < from) return;
+      if (nodes[c].npages * ps > from - pos) split(c, (from - pos) / ps);
+      pos += nodes[c].npages * ps;
+      node = c;
+    }
+    const std::uint32_t b = find_child(node, a, from / ps, n);
+    if (b == 0) return;
+    std::uint64_t slots = 0, toks = 0;
+    int pins = 0;
+    std::vector<std::uint32_t> st{b};
+    while (!st.empty()) {
+      const std::uint32_t x = st.back();
+      st.pop_back();
+      slots += nodes[x].device_slots;
+      toks += nodes[x].npages * ps;
+      pins += nodes[x].pin_count;
+      for (auto& kv : nodes[x].children) st.push_back(kv.second);
+    }
+    if (pins > 0) throw StateError("discard_suffix would drop pinned nodes");
+    if (nodes[b].subtree_has_device()) propagate_loss(b);
+    used -= slots;
+    discarded += toks;
+    const std::uint64_t head = nkey(nodes[b], nodes[b].start);
+    free_subtree(b, nullptr);
+    nodes[node].children.erase(head);
+  }
+
+  std::uint64_t digest() const {
     std::uint64_t h = kvdigest::fold(0x1234, dsum);
     h = kvdigest::fold(h, used);
     h = kvdigest::fold(h, clock);
@@ -350,11 +1003,12 @@ struct AgentRec {
   kvg_agent_stats st{};
 };
 
+template <typename CacheT>
 struct Sim {
   const kvg_sim_desc* d;
   const kvg_step_plan* plans;
   std::uint32_t n = 0, steps = 0;
-  FlatCache cache;
+  CacheT cache;
   Ctl ctl;
   std::vector<AgentRec> ag;
   std::set<std::tuple<double, std::uint64_t, std::uint32_t>> agent_q;  // rank 0
@@ -369,6 +1023,10 @@ struct Sim {
   std::uint64_t events = 0;
   kvg_ledger ledger{};
   double device_busy = 0;
+  // link queue (engine.cpp:156-182)
+  std::multiset<double> xfer_ends;
+  double pcie_busy = 0, link_busy = 0;
+  std::uint64_t reloaded = 0;
   std::vector<kvg_trace_row> trace;
   std::vector<std::uint64_t>* digests = nullptr;
   std::vector<kvg_log_record>* log = nullptr;
@@ -394,6 +1052,29 @@ struct Sim {
     agent_q.emplace(t, ord++, id);
     ev_kind[id] = kind;
   }
+  /* transfers_in_flight, engine.cpp:156-160 */
+  std::size_t in_flight() {
+    while (!xfer_ends.empty() && *xfer_ends.begin() <= clock) xfer_ends.erase(xfer_ends.begin());
+    return xfer_ends.size();
+  }
+  /* enqueue_transfer, engine.cpp:164-174; transfer_time, cost_model.cpp:43-47 */
+  double enqueue_transfer(double bytes) {
+    const std::size_t depth = in_flight() + 1;
+    const double dur = d->cost.transfer_sync_overhead +
+                       bytes * static_cast<double>(depth) / d->cost.pcie_bandwidth;
+    const double start = clock < pcie_busy ? pcie_busy : clock;
+    const double end = start + dur;
+    pcie_busy = end;
+    ledger.transfer += dur;
+    link_busy += dur;
+    xfer_ends.insert(end);
+    return end;
+  }
+  /* account_evictions, engine.cpp:178-182 */
+  void account(std::uint64_t offl_tokens) {
+    if (offl_tokens > 0)
+      enqueue_transfer(static_cast<double>(offl_tokens) * d->cost.bytes_per_token);
+  }
   void schedule_admission() {  // engine.cpp:149-154
     if (adm_on && adm_t == clock) return;
     if (adm_on) throw StateError("two admission checks outstanding");
@@ -409,7 +1090,7 @@ struct Sim {
     steps = pop->steps;
     plans = pop->plans;
     cache.init(d->engine.capacity, d->engine.page_size, pop->prompt_tokens,
-               pop->shared_prompt != 0);
+               pop->shared_prompt != 0, d->engine.eviction == KVG_EVICT_OFFLOAD);
     ctl.init(d->policy, n);
     ag.assign(n, AgentRec{});
     ev_kind.assign(n, 0);
@@ -424,22 +1105,44 @@ struct Sim {
   bool dispatch_member(std::uint32_t id, double* t_out, double* ft, double* rt, double* dt) {
     AgentRec& a = ag[id];
     const std::uint64_t ctx = a.ctx;
-    const std::uint64_t matched = cache.match(id, ctx);
+    std::uint64_t host_matched = 0;
+    const std::uint64_t matched = cache.match(id, ctx, &host_matched);
     {
-      std::uint64_t r = matched / cache.ps;
+      std::uint64_t r = (matched + host_matched) / cache.ps;
       lookups += r + (r < ctx / cache.ps ? 1 : 0);
     }
-    logrec(KVG_LOG_MATCH, id, matched, 0);
+    logrec(KVG_LOG_MATCH, id, matched, host_matched);
     cache.pin(id, matched, +1);
     if (a.pinned > 0) cache.pin(id, a.pinned, -1);
     a.pinned = matched;
+    if (cache.offload && host_matched > 0) {  // engine.cpp:343-360
+      std::uint64_t offl = 0;
+      cache.log = log;
+      cache.log_agent = id;
+      const std::uint64_t promoted = cache.reload(id, ctx, matched, host_matched, &offl);
+      cache.log = nullptr;
+      account(offl);
+      logrec(KVG_LOG_RELOAD, id, promoted, offl);
+      if (promoted > 0) {
+        cache.pin(id, matched + promoted, +1);
+        cache.pin(id, matched, -1);
+        a.pinned = matched + promoted;
+        reloaded += promoted;
+        const double end = enqueue_transfer(static_cast<double>(promoted) * d->cost.bytes_per_token);
+        a.st.wait_time += clock - a.ready_since;
+        set_state(id, S_GEN);
+        schedule_agent(end, EV_XFER, id);
+        return false;
+      }
+    }
     const kvg_step_plan& plan = plans[std::size_t(id) * steps + a.step];
     a.ctx += plan.gen_tokens;  // append_tokens
-    std::uint64_t inserted = 0;
+    std::uint64_t inserted = 0, offl = 0;
     cache.log = log;
     cache.log_agent = id;
-    bool ok = cache.insert(id, a.ctx, &inserted, nullptr);
+    bool ok = cache.insert(id, a.ctx, &inserted, nullptr, &offl);
     cache.log = nullptr;
+    account(offl);
     logrec(KVG_LOG_INSERT, id, ok ? 1 : 0, ok ? a.ctx / cache.ps * cache.ps : 0);
     if (!ok) {
       a.ctx = ctx;
@@ -610,6 +1313,15 @@ struct Sim {
     schedule_admission();
   }
 
+  /* engine.cpp:237-243 */
+  void on_transfer_complete(std::uint32_t id) {
+    AgentRec& a = ag[id];
+    makespan = makespan < clock ? clock : makespan;
+    set_state(id, S_AWAIT);
+    a.ready_since = clock;
+    schedule_admission();
+  }
+
   /* engine.cpp:245-266 */
   void on_tick() {
     const double usage = static_cast<double>(cache.used) / static_cast<double>(cache.capacity);
@@ -618,7 +1330,7 @@ struct Sim {
     ctl.update(usage, hit);
     kvg_trace_row row{clock, usage, hit, ctl.display(),
                       ctl.active.size(), ctl.pending.size() + ctl.paused.size(),
-                      decoded_cum, rec_cum, 0, m, r};
+                      decoded_cum, rec_cum, in_flight(), m, r};
     trace.push_back(row);
     cache.hit_m *= d->engine.hit_window_decay;
     cache.hit_r *= d->engine.hit_window_decay;
@@ -671,7 +1383,7 @@ struct Sim {
         switch (ev_kind[agent]) {
           case EV_GEN: on_generation_complete(agent); break;
           case EV_TOOL: on_tool_complete(agent); break;
-          default: throw StateError("transfer event in discard mode");
+          default: on_transfer_complete(agent); break;
         }
       } else if (which == 1) {
         on_tick();
@@ -689,9 +1401,10 @@ struct Sim {
     std::memset(res, 0, sizeof *res);
     res->status = status;
     res->ledger = ledger;
-    res->makespan = makespan;  // no link in discard mode: max(makespan, 0)
+    res->makespan = makespan < pcie_busy ? pcie_busy : makespan;  // engine.cpp:400
     res->device_busy = device_busy;
-    res->link_busy = 0;
+    res->link_busy = link_busy;
+    res->reloaded_tokens = reloaded;
     res->decoded_tokens = decoded_cum;
     res->recompute_tokens = rec_cum;
     double wait = 0;
@@ -756,18 +1469,14 @@ struct Sim {
 
 KVO_API const char* kvo_last_error(void) { return t_err.c_str(); }
 
-/* Runs one simulation on the CPU. Buffers may be NULL; counts are always
- * reported so a caller can size and retry. */
-KVO_API int kvo_run(const kvg_sim_desc* d, kvg_sim_result* res, kvg_trace_row* trace,
+namespace {
+template <typename CacheT>
+int run_one(const kvg_sim_desc* d, kvg_sim_result* res, kvg_trace_row* trace,
                     size_t trace_cap, size_t* n_trace, kvg_agent_stats* agents,
                     size_t agents_cap, uint64_t* digests, size_t digest_cap,
                     size_t* n_digests, kvg_log_record* log, size_t log_cap,
                     size_t* n_log) {
-  if (d->engine.eviction == KVG_EVICT_OFFLOAD) {
-    t_err = "oracle restatement covers discard-mode eviction only";
-    return KVG_ERR_CONFIG;
-  }
-  Sim sim;
+  Sim<CacheT> sim;
   std::vector<std::uint64_t> dig;
   std::vector<kvg_log_record> lg;
   if (digests) sim.digests = &dig;
@@ -795,15 +1504,49 @@ KVO_API int kvo_run(const kvg_sim_desc* d, kvg_sim_result* res, kvg_trace_row* t
     std::memcpy(log, lg.data(), std::min(log_cap, lg.size()) * sizeof(kvg_log_record));
   return status;
 }
+}  // namespace
+
+/* Runs one simulation on the CPU. Buffers may be NULL; counts are always
+ * reported so a caller can size and retry. Discard mode uses the flat page
+ * table, offload mode the node-level tree (see TreeCache). */
+KVO_API int kvo_run(const kvg_sim_desc* d, kvg_sim_result* res, kvg_trace_row* trace,
+                    size_t trace_cap, size_t* n_trace, kvg_agent_stats* agents,
+                    size_t agents_cap, uint64_t* digests, size_t digest_cap,
+                    size_t* n_digests, kvg_log_record* log, size_t log_cap,
+                    size_t* n_log) {
+  if (d->engine.eviction == KVG_EVICT_OFFLOAD)
+    return run_one<TreeCache>(d, res, trace, trace_cap, n_trace, agents, agents_cap, digests,
+                              digest_cap, n_digests, log, log_cap, n_log);
+  return run_one<FlatCache>(d, res, trace, trace_cap, n_trace, agents, agents_cap, digests,
+                            digest_cap, n_digests, log, log_cap, n_log);
+}
 
 /* ----------------------- cache-level differential surface ------------------- */
 
+/* Cache handle: the flat page table (discard) or the node-level tree
+ * (offload; or discard when `eviction` has bit 8 set, to cross-check the two
+ * restatements against each other). */
+struct AnyCache {
+  FlatCache* f = nullptr;
+  TreeCache* t = nullptr;
+  ~AnyCache() {
+    delete f;
+    delete t;
+  }
+};
+
 KVO_API void* kvo_cache_new(uint64_t capacity, uint64_t page_size, uint32_t eviction,
                             uint64_t prompt_tokens, uint32_t shared) {
-  if (eviction != KVG_EVICT_DISCARD) return nullptr;
   try {
-    auto* c = new FlatCache();
-    c->init(capacity, page_size, prompt_tokens, shared != 0);
+    auto* c = new AnyCache();
+    const bool off = (eviction & 0xff) == KVG_EVICT_OFFLOAD;
+    if (off || (eviction & 0x100)) {
+      c->t = new TreeCache();
+      c->t->init(capacity, page_size, prompt_tokens, shared != 0, off);
+    } else {
+      c->f = new FlatCache();
+      c->f->init(capacity, page_size, prompt_tokens, shared != 0, false);
+    }
     return c;
   } catch (const std::exception& e) {
     t_err = e.what();
@@ -811,22 +1554,29 @@ KVO_API void* kvo_cache_new(uint64_t capacity, uint64_t page_size, uint32_t evic
   }
 }
 
-KVO_API void kvo_cache_free(void* h) { delete static_cast<FlatCache*>(h); }
+KVO_API void kvo_cache_free(void* h) { delete static_cast<AnyCache*>(h); }
 
-KVO_API int kvo_cache_op(void* h, const kvg_cache_op* op, kvg_cache_op_result* r,
-                         kvg_victim* victims, size_t cap, size_t* n_victims) {
-  FlatCache* c = static_cast<FlatCache*>(h);
+namespace {
+template <typename CacheT>
+int cache_op(CacheT* c, const kvg_cache_op* op, kvg_cache_op_result* r, kvg_victim* victims,
+             size_t cap, size_t* n_victims) {
   std::vector<std::pair<std::uint64_t, std::uint64_t>> v;
   c->victims = &v;
   std::memset(r, 0, sizeof *r);
   int rc = KVG_OK;
   try {
     switch (op->kind) {
-      case KVG_OP_MATCH: r->r0 = c->match(op->agent, op->len); break;
+      case KVG_OP_MATCH: r->r0 = c->match(op->agent, op->len, &r->r1); break;
       case KVG_OP_INSERT: {
         std::uint64_t ins = 0;
         r->r0 = c->insert(op->agent, op->len, &ins, nullptr) ? 1 : 0;
         r->r1 = ins;
+        break;
+      }
+      case KVG_OP_RELOAD: {
+        std::uint64_t offl = 0;
+        r->r0 = c->reload(op->agent, op->len, op->arg, op->arg2, &offl);
+        r->r1 = offl;
         break;
       }
       case KVG_OP_EVICT: r->r0 = c->evict(op->arg); break;
@@ -848,12 +1598,23 @@ KVO_API int kvo_cache_op(void* h, const kvg_cache_op* op, kvg_cache_op_result* r
     victims[i] = kvg_victim{v[i].first, v[i].second};
   return rc;
 }
+}  // namespace
 
-KVO_API void kvo_cache_stats(void* h, double* m, double* r, uint64_t* discarded) {
-  FlatCache* c = static_cast<FlatCache*>(h);
-  if (m) *m = c->hit_m;
-  if (r) *r = c->hit_r;
-  if (discarded) *discarded = c->discarded;
+KVO_API int kvo_cache_op(void* h, const kvg_cache_op* op, kvg_cache_op_result* r,
+                         kvg_victim* victims, size_t cap, size_t* n_victims) {
+  AnyCache* c = static_cast<AnyCache*>(h);
+  return c->t ? cache_op(c->t, op, r, victims, cap, n_victims)
+              : cache_op(c->f, op, r, victims, cap, n_victims);
 }
 
-KVO_API uint64_t kvo_cache_digest(void* h) { return static_cast<FlatCache*>(h)->digest(); }
+KVO_API void kvo_cache_stats(void* h, double* m, double* r, uint64_t* discarded) {
+  AnyCache* c = static_cast<AnyCache*>(h);
+  if (m) *m = c->t ? c->t->hit_m : c->f->hit_m;
+  if (r) *r = c->t ? c->t->hit_r : c->f->hit_r;
+  if (discarded) *discarded = c->t ? c->t->discarded : c->f->discarded;
+}
+
+KVO_API uint64_t kvo_cache_digest(void* h) {
+  AnyCache* c = static_cast<AnyCache*>(h);
+  return c->t ? c->t->digest() : c->f->digest();
+}

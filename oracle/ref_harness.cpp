@@ -133,6 +133,8 @@ struct DigestSink {
   std::vector<std::uint64_t>* out = nullptr;
   std::uint64_t pending_cache = 0;
   std::uint64_t page_size = 1;
+  std::uint64_t q1_states = 0;   // events that ended in a Q1 state
+  std::uint64_t cwd_states = 0;  // events that ended with a corrupted counter
 };
 thread_local DigestSink t_sink;
 
@@ -194,7 +196,21 @@ void __real__ZNK7kvadmit10Controller16check_invariantsEv(const kvadmit::Controll
 
 __attribute__((visibility("hidden"))) void
 __wrap__ZNK7kvadmit9CacheTree16check_invariantsEv(const kvadmit::CacheTree* t) {
-  __real__ZNK7kvadmit9CacheTree16check_invariantsEv(t);
+  // Quirk Q1: an offload-mode reload can leave a device node
+  // below a host node, which check_invariants rejects. A production
+  // (non-paranoid) run carries on with that state, so the digest harness
+  // does too: that one violation is counted, never thrown.
+  try {
+    __real__ZNK7kvadmit9CacheTree16check_invariantsEv(t);
+  } catch (const kvadmit::InvariantViolation& e) {
+    // ... and the children_with_device over-count Q1 leads to: re-promoting a
+    // host node whose subtree already holds device slots calls
+    // propagate_gain a second time (cache_tree.cpp:94-102, 357-361)
+    const std::string w = e.what();
+    if (w.find("device node below a host node") != std::string::npos) ++t_sink.q1_states;
+    else if (w.find("children_with_device mismatch") != std::string::npos) ++t_sink.cwd_states;
+    else throw;
+  }
   if (t_sink.out != nullptr) t_sink.pending_cache = cache_digest(*t);
 }
 
@@ -209,6 +225,11 @@ __wrap__ZNK7kvadmit10Controller16check_invariantsEv(const kvadmit::Controller* c
 /* ------------------------------------------------------------------------ */
 
 KVR_API const char* kvr_last_error(void) { return t_err.c_str(); }
+
+/* Events of this thread's last kvr_run (with digests) that ended in a Q1
+ * state: device node below a host node. */
+KVR_API uint64_t kvr_last_q1_states(void) { return t_sink.q1_states; }
+KVR_API uint64_t kvr_last_cwd_states(void) { return t_sink.cwd_states; }
 
 KVR_API int kvr_build_population(const kvg_workload_config* cfg, uint64_t seed,
                                  kvg_step_plan* plans, size_t cap,
@@ -301,6 +322,8 @@ KVR_API int kvr_run(const kvg_workload_config* wl, uint64_t seed,
   kvadmit::SimulationResult result;
   int rc = guarded([&] {
     kvadmit::EngineParams ep = to_engine(*engine);
+    t_sink.q1_states = 0;
+    t_sink.cwd_states = 0;
     if (digests != nullptr) {
       ep.paranoid = true;
       t_sink.out = &dig;
@@ -453,6 +476,12 @@ KVR_API int kvr_cache_op(void* h, const kvg_cache_op* op, kvg_cache_op_result* r
       case KVG_OP_PIN: c->tree.pin(s, op->arg); break;
       case KVG_OP_UNPIN: c->tree.unpin(s, op->arg); break;
       case KVG_OP_DISCARD: c->tree.discard_suffix(s, op->arg); break;
+      case KVG_OP_RELOAD: {
+        kvadmit::EvictStats ev;
+        r->r0 = c->tree.reload(s, op->arg, op->arg2, &ev);
+        r->r1 = ev.offloaded_tokens;
+        break;
+      }
       default: throw kvadmit::ConfigError("unknown op");
     }
   });

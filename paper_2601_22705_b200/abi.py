@@ -20,7 +20,7 @@ STATUS_NAMES = {0: "ok", 1: "config", 2: "io", 3: "horizon", 4: "state",
 DIST_CONSTANT, DIST_UNIFORM, DIST_LOGNORMAL = 0, 1, 2
 POLICY_UNCONTROLLED, POLICY_REQUEST_CAP, POLICY_AGENT_CAP, POLICY_AIMD = 0, 1, 2, 3
 EVICT_DISCARD, EVICT_OFFLOAD = 0, 1
-OP_MATCH, OP_INSERT, OP_EVICT, OP_PIN, OP_UNPIN, OP_DISCARD = 1, 2, 3, 4, 5, 6
+OP_MATCH, OP_INSERT, OP_EVICT, OP_PIN, OP_UNPIN, OP_DISCARD, OP_RELOAD = 1, 2, 3, 4, 5, 6, 7
 LOG_MATCH, LOG_INSERT, LOG_EVICT, LOG_VICTIM, LOG_FINISH, LOG_DISCARD = 1, 2, 3, 4, 5, 6
 
 
@@ -130,7 +130,7 @@ class BatchOptions(C.Structure):
 
 
 class CacheOp(C.Structure):
-    _fields_ = [("kind", u32), ("agent", u32), ("len", u64), ("arg", u64)]
+    _fields_ = [("kind", u32), ("agent", u32), ("len", u64), ("arg", u64), ("arg2", u64)]
 
 
 class CacheOpResult(C.Structure):
@@ -157,7 +157,7 @@ AGENT_FIELDS = ("generated_tokens", "recompute_tokens", "recompute_events",
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
-LIB_PATH = os.path.join(PKG_DIR, "libkvgpu.so")
+LIB_PATH = os.environ.get("KVG_LIB") or os.path.join(PKG_DIR, "libkvgpu.so")
 
 
 def struct_to_dict(s) -> dict:

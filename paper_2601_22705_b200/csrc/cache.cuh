@@ -201,6 +201,8 @@ __global__ void __launch_bounds__(1024) cache_kernel(const CacheDev* __restrict_
     op.alt = sw ? C.table : C.alt;
     op.occ = sw ? C.alt_occ : C.occ;
     op.alt_occ = sw ? C.occ : C.alt_occ;
+    op.summ = sw ? C.alt_summ : C.summ;
+    op.alt_summ = sw ? C.summ : C.alt_summ;
     op.mask = C.bucket_mask;
     op.occ_n = static_cast<unsigned int>(st->occ_n);
     op.shared_pages = C.shared_pages;
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(1024) cache_kernel(const CacheDev* __restrict_
     if (tid == 0) cache_leader(C, L, op);
     __syncthreads();
     if (op.kind == OP_EXIT) break;
-    run_op(op, h, tid, warp, lane, nw);
+    run_op<8>(op, h, tid, warp, lane, nw);
     __syncthreads();
     if (tid == 0 && op.kind == OP_REBUILD) st->swapped ^= 1;
   }

@@ -113,8 +113,9 @@ KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity, uint64_t page
   const u64 tb = c->buckets * kvg::kChunk * sizeof(kvg::Slot);
   const u64 ob = align_up(c->buckets * sizeof(u32));
   c->victim_cap = 1 << 20;
+  const u64 sb = align_up(c->buckets * sizeof(kvg::Summ));
   const u64 bytes = 2 * tb + 2 * ob + align_up(sizeof(kvg::CacheState)) +
-                    align_up(sizeof(kvg::CacheDev)) + 2 * 512 * sizeof(u32) + 256;
+                    align_up(sizeof(kvg::CacheDev)) + align_up(2 * 512 * sizeof(u32)) + 2 * sb + 256;
   CUDA_TRY(cudaMalloc(&c->mem, bytes));
   CUDA_TRY(cudaMalloc(&c->d_victims, c->victim_cap * sizeof(kvg_victim)));
   CUDA_TRY(cudaMemset(c->mem, 0xff, 2 * tb));
@@ -135,6 +136,10 @@ KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity, uint64_t page
   c->h.state = reinterpret_cast<u64*>(c->d_state);
   c->h.hist = reinterpret_cast<u32*>(p + 2 * tb + 2 * ob + align_up(sizeof(kvg::CacheState)) +
                                      align_up(sizeof(kvg::CacheDev)));
+  char* sp = p + 2 * tb + 2 * ob + align_up(sizeof(kvg::CacheState)) +
+             align_up(sizeof(kvg::CacheDev)) + align_up(2 * 512 * sizeof(u32));
+  c->h.summ = reinterpret_cast<kvg::Summ*>(sp);
+  c->h.alt_summ = reinterpret_cast<kvg::Summ*>(sp + sb);
   CUDA_TRY(cudaMemset(c->d_state, 0, sizeof(kvg::CacheState)));
   *out = c;
   return KVG_OK;

@@ -31,6 +31,7 @@
 namespace kvg {
 
 constexpr unsigned FULL = 0xffffffffu;
+constexpr u32 NIL32 = 0xffffffffu;
 
 // ------------------------------------------------------------------------
 // small device helpers
@@ -127,6 +128,8 @@ struct Op {
   Slot* alt;
   u32* occ;
   u32* alt_occ;
+  Summ* summ;
+  Summ* alt_summ;
   u32 mask;
   unsigned int occ_n;
   unsigned int alt_n;
@@ -152,6 +155,35 @@ struct Hist {
   unsigned int* dmax;  // [kBins]
 };
 
+__device__ __forceinline__ Summ ld_summ(const Summ* p) {
+  const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p);
+  const ulonglong2 a = __ldcg(q), b = __ldcg(q + 1);
+  Summ s;
+  s.tag = a.x;
+  s.sf = a.y;
+  s.dev = static_cast<u32>(b.x);
+  s.host = static_cast<u32>(b.x >> 32);
+  s.bnd = static_cast<u32>(b.y);
+  s.pad = 0;
+  return s;
+}
+
+// Rewrites bucket b's summary from the per-lane metas the calling warp holds
+// (every lane of the warp must call; lane l owns slot l).
+__device__ __forceinline__ void summ_write(Summ* summ, u32 b, u64 m, int lane) {
+  const bool res = (m & kResident) != 0;
+  const u32 dev = __ballot_sync(FULL, res);
+  const u64 st = m_stamp(m);
+  const int l0 = dev ? __ffs(dev) - 1 : 0;
+  const u64 s0 = __shfl_sync(FULL, st, l0);
+  const bool mixed = __any_sync(FULL, res && (st != s0 || m_pins(m) != 0));
+  if (lane == 0) {
+    Summ* e = &summ[b];
+    __stcg(&e->sf, (dev ? s0 : 0ull) | (mixed ? kMixed : 0ull));
+    __stcg(&e->dev, dev);
+  }
+}
+
 // Continues a linear probe for chunk `tag` from bucket `b`. Returns true and
 // this lane's slot when present; otherwise *bucket is the first empty bucket.
 __device__ __forceinline__ bool probe_from(const Op& op, u64 tag, u32 b, int lane, u32* bucket,
@@ -172,9 +204,10 @@ __device__ __forceinline__ bool probe_from(const Op& op, u64 tag, u32 b, int lan
   }
 }
 
-// Claims an empty bucket for `tag`, starting at bucket `b`; returns it.
-__device__ __noinline__ u32 claim(Op& op, Slot* table, u32* occ, unsigned int* occ_n, u32 mask,
-                     u64 tag, u32 b, int lane) {
+// Claims an empty bucket for `tag`, starting at bucket `b`; returns it. The
+// bucket's summary starts empty.
+__device__ __noinline__ u32 claim(Slot* table, Summ* summ, u32* occ, unsigned int* occ_n,
+                                  u32 mask, u64 tag, u32 b, int lane) {
   for (;;) {
     int won = 0;
     if (lane == 0) {
@@ -189,6 +222,9 @@ __device__ __noinline__ u32 claim(Op& op, Slot* table, u32* occ, unsigned int* o
       if (lane != 0) __stcg(&s->key, tag + lane);
       __stcg(&s->meta, 0ull);
       if (lane == 0) {
+        ulonglong2* q = reinterpret_cast<ulonglong2*>(&summ[b]);
+        __stcg(q, make_ulonglong2(tag, 0ull));
+        __stcg(q + 1, make_ulonglong2(0ull, 0ull));
         unsigned int idx = atomicAdd(occ_n, 1u);
         __stcg(&occ[idx], b);
       }
@@ -206,6 +242,8 @@ struct RangeAcc {
 };
 
 // Per-lane work on one 32-page chunk whose bucket probe already completed.
+// `found` is warp-uniform. Every lane reports its slot's final meta so the
+// warp can rewrite the bucket summary when anything changed.
 __device__ __forceinline__ void range_chunk(Op& op, u64 tag, u64 lo, u64 hi, u32 b, Slot s,
                                             bool found, int lane, RangeAcc& acc) {
   const u32 flags = op.flags;
@@ -213,59 +251,70 @@ __device__ __forceinline__ void range_chunk(Op& op, u64 tag, u64 lo, u64 hi, u32
   const u64 page = (tag & 0xffffffffull) + lane;
   const bool in = page >= lo && page < hi;
   if (!found && (flags & RF_CREATE) && __any_sync(FULL, in)) {
-    b = claim(op, op.table, op.occ, &op.occ_n, op.mask, tag, b, lane);
+    b = claim(op.table, op.summ, op.occ, &op.occ_n, op.mask, tag, b, lane);
     found = true;
     s = Slot{tag + lane, 0};
   }
-  if (!in) return;
-  const bool res = found && (s.meta & kResident);
-  Slot* slot = found ? &op.table[(size_t)b * kChunk + lane] : nullptr;
-  if (!res) {
-    if (flags & RF_CREATE) {
-      const u64 pins = delta > 0 ? static_cast<u64>(delta) : 0;
-      st_meta(slot, m_make(op.stamp, pins));
-      ++acc.created;
-      if (pins) ++acc.up;
-    } else {
+  if (!found) {
+    if (in) {
       acc.miss = page < acc.miss ? page : acc.miss;
       if (flags & RF_STRICT) acc.err = E_PIN_MISSING;
     }
     return;
   }
-  ++acc.resident;
   const u64 m = s.meta;
-  if (flags & RF_FREE) {
-    if (!op.implicit_pins && m_pins(m) != 0) {
-      acc.err = E_DISCARD_PINNED;
-      return;
+  u64 nm = m;
+  if (in) {
+    if (!(m & kResident)) {
+      if (flags & RF_CREATE) {
+        const u64 pins = delta > 0 ? static_cast<u64>(delta) : 0;
+        nm = m_make(op.stamp, pins);
+        ++acc.created;
+        if (pins) ++acc.up;
+      } else {
+        acc.miss = page < acc.miss ? page : acc.miss;
+        if (flags & RF_STRICT) acc.err = E_PIN_MISSING;
+      }
+    } else {
+      ++acc.resident;
+      if (flags & RF_FREE) {
+        if (!op.implicit_pins && m_pins(m) != 0) {
+          acc.err = E_DISCARD_PINNED;
+        } else {
+          nm = 0ull;
+          ++acc.freed;
+        }
+      } else {
+        const u64 stamp = (flags & RF_STAMP) ? op.stamp : m_stamp(m);
+        long long pins = static_cast<long long>(m_pins(m));
+        if (flags & RF_PIN) {
+          long long np = pins + delta;
+          if (np < 0) {
+            acc.err = E_UNPIN_UNDERFLOW;
+            np = 0;
+          }
+          if (pins == 0 && np > 0) ++acc.up;
+          if (pins > 0 && np == 0) ++acc.down;
+          pins = np;
+        }
+        nm = m_make(stamp, static_cast<u64>(pins));
+      }
     }
-    st_meta(slot, 0ull);
-    ++acc.freed;
-    return;
   }
-  const u64 stamp = (flags & RF_STAMP) ? op.stamp : m_stamp(m);
-  long long pins = static_cast<long long>(m_pins(m));
-  if (flags & RF_PIN) {
-    long long np = pins + delta;
-    if (np < 0) {
-      acc.err = E_UNPIN_UNDERFLOW;
-      np = 0;
-    }
-    if (pins == 0 && np > 0) ++acc.up;
-    if (pins > 0 && np == 0) ++acc.down;
-    pins = np;
-  }
-  const u64 nm = m_make(stamp, static_cast<u64>(pins));
-  if (nm != m) st_meta(slot, nm);
+  const bool wrote = nm != m;
+  if (wrote) st_meta(&op.table[(size_t)b * kChunk + lane], nm);
+  if (__any_sync(FULL, wrote)) summ_write(op.summ, b, nm, lane);
 }
 
 // RANGE: agent `op.agent`, pages [p0, p1). Pages below shared_pages belong to
 // the shared prompt (owner 0), the rest to owner agent+1 (workload.cpp:167-171).
 // Each warp owns every nw-th 32-page chunk and keeps kProbeDepth bucket probes
 // in flight (one 512 B coalesced load each) before consuming any of them, so a
-// context of C chunks costs ~C/(nw*kProbeDepth) DRAM round trips, not C.
-constexpr int kProbeDepth = 8;
-
+// context of C chunks costs ~C/(nw*kProbeDepth) DRAM round trips, not C
+// (depth 8 for the big-sim kernel, 4 for the register-lean 1-warp kernel). The
+// in-flight probes rotate through registers (no dynamically indexed arrays,
+// so nothing spills to local memory).
+template <int kProbeDepth>
 __device__ __noinline__ void coop_range(Op& op, int warp, int lane, int nw) {
   const u64 p0 = op.p0, p1 = op.p1;
   if (p0 >= p1) return;
@@ -281,34 +330,44 @@ __device__ __noinline__ void coop_range(Op& op, int warp, int lane, int nw) {
     return it < n_sh ? ((s_lo >> 5) + it) << 5
                      : (owner_priv << 32) | (((q_lo >> 5) + (it - n_sh)) << 5);
   };
-  for (u64 base = warp; base < total; base += static_cast<u64>(nw) * kProbeDepth) {
+  const u64 step = static_cast<u64>(nw);
+  for (u64 base = warp; base < total; base += step * kProbeDepth) {
     Slot s[kProbeDepth];
     u32 b[kProbeDepth];
 #pragma unroll
     for (int g = 0; g < kProbeDepth; ++g) {
-      const u64 it = base + static_cast<u64>(g) * nw;
+      const u64 it = base + static_cast<u64>(g) * step;
+      b[g] = 0;
+      s[g] = Slot{kEmptyKey, 0};
       if (it < total) {
         b[g] = static_cast<u32>(hash64(tag_of(it))) & op.mask;
         s[g] = ld_slot(&op.table[(size_t)b[g] * kChunk + lane]);
       }
     }
+    const u64 left = (total - base + step - 1) / step;
+    const int cnt = left < kProbeDepth ? static_cast<int>(left) : kProbeDepth;
 #pragma unroll 1
-    for (int g = 0; g < kProbeDepth; ++g) {
-      const u64 it = base + static_cast<u64>(g) * nw;
-      if (it >= total) break;
+    for (int g = 0; g < cnt; ++g) {
+      const u64 it = base + static_cast<u64>(g) * step;
+      Slot cur = s[0];
+      u32 cb = b[0];
+#pragma unroll
+      for (int j = 0; j + 1 < kProbeDepth; ++j) {
+        s[j] = s[j + 1];
+        b[j] = b[j + 1];
+      }
       const u64 tag = tag_of(it);
-      const u64 k0 = __shfl_sync(FULL, s[g].key, 0);
+      const u64 k0 = __shfl_sync(FULL, cur.key, 0);
       bool found;
       if (k0 == tag) {
         found = true;
       } else if (k0 == kEmptyKey) {
         found = false;
       } else {
-        found = probe_from(op, tag, (b[g] + 1) & op.mask, lane, &b[g], &s[g]);
+        found = probe_from(op, tag, (cb + 1) & op.mask, lane, &cb, &cur);
       }
       const bool shared = it < n_sh;
-      range_chunk(op, tag, shared ? s_lo : q_lo, shared ? s_hi : q_hi, b[g], s[g], found, lane,
-                  acc);
+      range_chunk(op, tag, shared ? s_lo : q_lo, shared ? s_hi : q_hi, cb, cur, found, lane, acc);
     }
   }
   // warp reductions, then one shared atomic per warp
@@ -334,10 +393,9 @@ __device__ __noinline__ void coop_range(Op& op, int warp, int lane, int nw) {
   }
 }
 
-// Visits every claimed bucket (the dense occupancy list), kScanDepth buckets in
-// flight per warp; f(bucket, slot, pin_threshold) runs per lane. With implicit
-// pins (engine mode) the bucket owner's pinned prefix length is fetched in the
-// same wave: page (owner, idx) is pinned iff idx < threshold.
+// Visits every claimed bucket, one WARP per bucket (lane l holds slot l):
+// the whole-bucket passes (suffix discard, rehash). kScanDepth buckets in
+// flight per warp, rotated through registers.
 constexpr int kScanDepth = 4;
 
 template <typename F>
@@ -346,7 +404,6 @@ __device__ __forceinline__ void scan_buckets(const Op& op, int warp, int lane, i
   for (u32 base = warp; base < n_occ; base += static_cast<u32>(nw) * kScanDepth) {
     u32 bk[kScanDepth];
     Slot s[kScanDepth];
-    u64 thr[kScanDepth];
 #pragma unroll
     for (int g = 0; g < kScanDepth; ++g) {
       const u32 i = base + g * nw;
@@ -355,32 +412,78 @@ __device__ __forceinline__ void scan_buckets(const Op& op, int warp, int lane, i
 #pragma unroll
     for (int g = 0; g < kScanDepth; ++g) {
       const u32 i = base + g * nw;
+      s[g] = Slot{kEmptyKey, 0};
       if (i < n_occ) s[g] = ld_slot(&op.table[(size_t)bk[g] * kChunk + lane]);
     }
-#pragma unroll
-    for (int g = 0; g < kScanDepth; ++g) {
-      const u32 i = base + g * nw;
-      thr[g] = 0;
-      if (i < n_occ && op.implicit_pins) {
-        const u64 owner = __shfl_sync(FULL, s[g].key, 0) >> 32;
-        // plain load: the records may live in shared memory (leader wrote them
-        // before the barrier that started this op)
-        thr[g] = owner == 0 ? op.pin_max : op.agents[owner - 1].pinned_pg;
-      }
-    }
+    const u32 left = (n_occ - base + nw - 1) / nw;
+    const int cnt = left < kScanDepth ? static_cast<int>(left) : kScanDepth;
 #pragma unroll 1
-    for (int g = 0; g < kScanDepth; ++g) {
-      const u32 i = base + g * nw;
-      if (i < n_occ) f(bk[g], s[g], thr[g]);
+    for (int g = 0; g < cnt; ++g) {
+      const u32 cb = bk[0];
+      const Slot cur = s[0];
+#pragma unroll
+      for (int j = 0; j + 1 < kScanDepth; ++j) {
+        bk[j] = bk[j + 1];
+        s[j] = s[j + 1];
+      }
+      f(cb, cur);
     }
   }
 }
 
-// Eviction candidate: resident and unpinned (cache_tree.cpp:230-234 per page).
-__device__ __forceinline__ bool is_candidate(const Op& op, const Slot& s, u64 thr) {
-  if (!(s.meta & kResident)) return false;
-  if (op.implicit_pins) return (s.key & 0xffffffffull) >= thr;
-  return m_pins(s.meta) == 0;
+// Visits every claimed bucket's SUMMARY, one LANE per bucket: the eviction
+// select's input. kSumDepth summaries in flight per lane; f(valid, bucket,
+// summary) is called by every lane of the warp together (warp-convergent, so
+// f may use warp collectives).
+constexpr int kSumDepth = 4;
+
+template <typename F>
+__device__ __forceinline__ void scan_summ(const Op& op, int warp, int lane, int nw, F&& f) {
+  const u32 n_occ = op.occ_n;
+  const u32 stride = static_cast<u32>(nw) * 32u * kSumDepth;
+  for (u32 base = static_cast<u32>(warp) * 32u * kSumDepth; base < n_occ; base += stride) {
+    u32 bk[kSumDepth];
+    Summ e[kSumDepth];
+#pragma unroll
+    for (int g = 0; g < kSumDepth; ++g) {
+      const u32 i = base + g * 32u + lane;
+      bk[g] = i < n_occ ? __ldcg(&op.occ[i]) : NIL32;
+    }
+#pragma unroll
+    for (int g = 0; g < kSumDepth; ++g) {
+      e[g] = Summ{0, 0, 0, 0, 0, 0};
+      if (bk[g] != NIL32) e[g] = ld_summ(&op.summ[bk[g]]);
+    }
+#pragma unroll
+    for (int g = 0; g < kSumDepth; ++g) f(bk[g] != NIL32, bk[g], e[g]);
+  }
+}
+
+__device__ __forceinline__ u32 ge_mask(u64 base, u64 thr) {  // slots with page index >= thr
+  if (thr <= base) return FULL;
+  const u64 d = thr - base;
+  return d >= 32 ? 0u : (FULL << d);
+}
+
+__device__ __forceinline__ u64 pin_thr(const Op& op, u64 owner) {
+  // plain load: the records may live in shared memory (the leader wrote them
+  // before the barrier that started this op)
+  return owner == 0 ? op.pin_max : static_cast<u64>(op.agents[owner - 1].pinned_pg);
+}
+
+// Eviction candidates of a summarised (non-mixed) bucket: resident and
+// unpinned (cache_tree.cpp:230-234 per page). Engine mode: page (owner, idx)
+// is pinned iff idx < its owner's pinned prefix.
+__device__ __forceinline__ u32 cand_of(const Op& op, const Summ& e) {
+  if (!op.implicit_pins) return e.dev;  // explicit pins make a bucket mixed
+  return e.dev & ge_mask(e.tag & 0xffffffffull, pin_thr(op, e.tag >> 32));
+}
+
+// Per-page candidate test (mixed buckets).
+__device__ __forceinline__ bool page_cand(const Op& op, u64 key, u64 meta) {
+  if (!(meta & kResident)) return false;
+  if (op.implicit_pins) return (key & 0xffffffffull) >= pin_thr(op, key >> 32);
+  return m_pins(meta) == 0;
 }
 
 __device__ __forceinline__ void emit_victim(Op& op, u64 key, u64 stamp, u32 agent) {
@@ -438,11 +541,52 @@ __device__ __noinline__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int la
   return bin;
 }
 
+// Histogram contribution of a mixed bucket, page by page (one lane).
+__device__ __noinline__ void hist_mixed(const Op& op, Hist& h, u32 b, u64 prefix, int lo_bits,
+                                        int shift, u32 nbins, bool last) {
+  const Slot* bk = &op.table[(size_t)b * kChunk];
+  for (int l = 0; l < kChunk; ++l) {
+    const Slot s = ld_slot(&bk[l]);
+    if (!page_cand(op, s.key, s.meta)) continue;
+    const u64 st = m_stamp(s.meta);
+    if ((st >> lo_bits) != prefix) continue;
+    const u32 bin = static_cast<u32>((st >> shift) & (nbins - 1));
+    atomicAdd(&h.cnt[bin], 1u);
+    if (last) atomicMax(&h.dmax[bin], static_cast<u32>(s.key & 0xffffffffu));
+  }
+}
+
+// Scatter-free of a mixed bucket, page by page (one lane). Returns pages freed.
+__device__ __noinline__ u32 scatter_mixed(Op& op, u32 b, bool all, u64 T, u64 cut) {
+  Slot* bk = &op.table[(size_t)b * kChunk];
+  u32 freed = 0, dev = 0;
+  for (int l = 0; l < kChunk; ++l) {
+    const Slot s = ld_slot(&bk[l]);
+    const bool res = (s.meta & kResident) != 0;
+    if (res && page_cand(op, s.key, s.meta)) {
+      const u64 st = m_stamp(s.meta);
+      const u64 depth = s.key & 0xffffffffu;
+      if (all || st < T || (st == T && depth >= cut)) {
+        st_meta(&bk[l], 0ull);
+        ++freed;
+        if (op.log_victims) emit_victim(op, s.key, st, op.agent);
+        continue;
+      }
+    }
+    if (res) dev |= 1u << l;
+  }
+  __stcg(&op.summ[b].dev, dev);
+  return freed;
+}
+
 // EVICT (cache_tree.cpp:270-319, per-page form SURVEY.md A.2): free the
 // op.k smallest (stamp asc, page index desc) resident unpinned pages.
-// Radix select over stamps (9-bit digits, shared-memory histogram with
-// warp-aggregated atomics), exact threshold stamp T and the deepest-j cut
-// inside it (equal stamps lie on one root path), then one scatter pass.
+// Radix select over stamps (9-bit digits) on the bucket SUMMARIES, one lane
+// per bucket with weight popc(candidates): the histogram holds page counts,
+// warp-aggregated through __match_any_sync / __reduce_add_sync. It finds the
+// exact threshold stamp T and the cut depth inside it (equal stamps lie on
+// one root path, so "deepest j" is a depth cut); one scatter pass then frees
+// the chosen pages and rewrites the summaries.
 __device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int lane, int nw) {
   const int nt = nw * 32;
   if (tid == 0) {
@@ -467,20 +611,28 @@ __device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int 
       }
       __syncthreads();
       const u64 prefix = op.prefix;
-      scan_buckets(op, warp, lane, nw, [&](u32, const Slot& s, u64 thr) {
-        const u64 st = m_stamp(s.meta);
-        const bool act = is_candidate(op, s, thr) && (st >> lo_bits) == prefix;
+      scan_summ(op, warp, lane, nw, [&](bool valid, u32 b, const Summ& e) {
+        const bool mixed = valid && (e.sf & kMixed);
+        u32 c = 0;
+        u64 st = 0;
+        if (valid && !mixed) {
+          c = cand_of(op, e);
+          st = e.sf & kStampMask;
+        }
+        const bool act = c != 0 && (st >> lo_bits) == prefix;
         const u32 bin = act ? static_cast<u32>((st >> shift) & (nbins - 1)) : 0xffffffffu;
         const unsigned peers = __match_any_sync(FULL, bin);
         if (act) {
           const int leader = __ffs(peers) - 1;
-          if (lane == leader) atomicAdd(&h.cnt[bin], static_cast<u32>(__popc(peers)));
+          const u32 w = __reduce_add_sync(peers, static_cast<u32>(__popc(c)));
+          if (lane == leader) atomicAdd(&h.cnt[bin], w);
           if (last) {
-            const u32 depth = static_cast<u32>(s.key & 0xffffffffu);
-            const u32 mx = __reduce_max_sync(peers, depth);
+            const u32 dm = static_cast<u32>(e.tag & 0xffffffffu) + 31u - __clz(c);
+            const u32 mx = __reduce_max_sync(peers, dm);
             if (lane == leader) atomicMax(&h.dmax[bin], mx);
           }
         }
+        if (mixed) hist_mixed(op, h, b, prefix, lo_bits, shift, nbins, last);
       });
       __syncthreads();
       if (warp == 0) {
@@ -496,15 +648,25 @@ __device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int 
   }
   // scatter-free pass
   unsigned int freed = 0;
-  scan_buckets(op, warp, lane, nw, [&](u32 b, const Slot& s, u64 thr) {
-    if (!is_candidate(op, s, thr)) return;
-    const u64 st = m_stamp(s.meta);
-    const u64 depth = s.key & 0xffffffffu;
-    if (all || st < T || (st == T && depth >= cut)) {
-      st_meta(&op.table[(size_t)b * kChunk + lane], 0ull);
-      ++freed;
-      if (op.log_victims) emit_victim(op, s.key, st, op.agent);
+  scan_summ(op, warp, lane, nw, [&](bool valid, u32 b, const Summ& e) {
+    if (!valid) return;
+    if (e.sf & kMixed) {
+      freed += scatter_mixed(op, b, all, T, cut);
+      return;
     }
+    const u32 c = cand_of(op, e);
+    if (c == 0) return;
+    const u64 st = e.sf & kStampMask;
+    const u32 v = (all || st < T) ? c : (st == T ? c & ge_mask(e.tag & 0xffffffffull, cut) : 0u);
+    if (v == 0) return;
+    freed += __popc(v);
+    Slot* bk = &op.table[(size_t)b * kChunk];
+    for (u32 m = v; m != 0; m &= m - 1) {
+      const int l = __ffs(m) - 1;
+      st_meta(&bk[l], 0ull);
+      if (op.log_victims) emit_victim(op, e.tag + l, st, op.agent);
+    }
+    __stcg(&op.summ[b].dev, e.dev & ~v);
   });
   for (int o = 16; o > 0; o >>= 1) freed += __shfl_down_sync(FULL, freed, o);
   if (lane == 0 && freed) atomicAdd(&op.freed, freed);
@@ -515,17 +677,21 @@ __device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int 
 __device__ __noinline__ void coop_scanfree(Op& op, int warp, int lane, int nw) {
   unsigned int freed = 0;
   int err = 0;
-  scan_buckets(op, warp, lane, nw, [&](u32 b, const Slot& s, u64) {
-    if (!(s.meta & kResident)) return;
-    const u64 owner = s.key >> 32, idx = s.key & 0xffffffffu;
-    if (idx < op.p0) return;
-    if (op.owner_filter != ~0ull && owner != op.owner_filter) return;
-    if (m_pins(s.meta)) {
-      err = E_DISCARD_PINNED;
-      return;
+  scan_buckets(op, warp, lane, nw, [&](u32 b, const Slot& s) {
+    u64 nm = s.meta;
+    if (s.meta & kResident) {
+      const u64 owner = s.key >> 32, idx = s.key & 0xffffffffu;
+      if (idx >= op.p0 && (op.owner_filter == ~0ull || owner == op.owner_filter)) {
+        if (m_pins(s.meta)) {
+          err = E_DISCARD_PINNED;
+        } else {
+          nm = 0ull;
+          st_meta(&op.table[(size_t)b * kChunk + lane], 0ull);
+          ++freed;
+        }
+      }
     }
-    st_meta(&op.table[(size_t)b * kChunk + lane], 0ull);
-    ++freed;
+    if (__any_sync(FULL, nm != s.meta)) summ_write(op.summ, b, nm, lane);
   });
   for (int o = 16; o > 0; o >>= 1) {
     freed += __shfl_down_sync(FULL, freed, o);
@@ -538,8 +704,8 @@ __device__ __noinline__ void coop_scanfree(Op& op, int warp, int lane, int nw) {
   }
 }
 
-// REBUILD: copy buckets holding at least one resident page into the
-// alternate table (pre-cleared here), then swap tables.
+// REBUILD: copy buckets holding at least one resident page (with their
+// summaries) into the alternate table (pre-cleared here), then swap tables.
 __device__ __noinline__ void coop_rebuild(Op& op, int tid, int warp, int lane, int nw) {
   const int nt = nw * 32;
   const size_t nslots = (static_cast<size_t>(op.mask) + 1) * kChunk;
@@ -556,8 +722,14 @@ __device__ __noinline__ void coop_rebuild(Op& op, int tid, int warp, int lane, i
     if (!__any_sync(FULL, (s.meta & kResident) != 0)) continue;
     const u64 tag = __shfl_sync(FULL, s.key, 0);
     u32 nb = static_cast<u32>(hash64(tag)) & op.mask;
-    nb = claim(op, op.alt, op.alt_occ, &op.alt_n, op.mask, tag, nb, lane);
+    nb = claim(op.alt, op.alt_summ, op.alt_occ, &op.alt_n, op.mask, tag, nb, lane);
     __stcg(&op.alt[(size_t)nb * kChunk + lane].meta, s.meta);
+    if (lane == 0) {
+      const ulonglong2* src = reinterpret_cast<const ulonglong2*>(&op.summ[b]);
+      ulonglong2* dst = reinterpret_cast<ulonglong2*>(&op.alt_summ[nb]);
+      __stcg(dst, __ldcg(src));
+      __stcg(dst + 1, __ldcg(src + 1));
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -567,6 +739,9 @@ __device__ __noinline__ void coop_rebuild(Op& op, int tid, int warp, int lane, i
     u32* o = op.occ;
     op.occ = op.alt_occ;
     op.alt_occ = o;
+    Summ* sm = op.summ;
+    op.summ = op.alt_summ;
+    op.alt_summ = sm;
     op.occ_n = op.alt_n;
   }
 }

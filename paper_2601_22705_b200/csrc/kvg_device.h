@@ -35,6 +35,24 @@ struct Slot {
   u64 meta;
 };
 
+// Dense 32 B summary of one claimed bucket, kept parallel to the table and
+// rewritten by whichever warp last modified the bucket. The eviction select
+// reads summaries (one lane per bucket) instead of whole 512 B buckets: in
+// the engine every resident page of a chunk carries the same stamp (an
+// agent's path is always refreshed as a whole prefix), so a bucket's
+// candidates are (dev mask, one stamp). Buckets that break that shape
+// (explicit pins, mixed stamps) are flagged kMixed and handled per page.
+struct Summ {
+  u64 tag;   // owner << 32 | first page of the chunk
+  u64 sf;    // bits 0..39: stamp of every resident page; kMixed
+  u32 dev;   // device-resident slots (bit l = slot l)
+  u32 host;  // host-tier slots (offload)
+  u32 bnd;   // node-start slots (offload: reload chunk boundaries)
+  u32 pad;
+};
+constexpr u64 kMixed = 1ull << 63;
+static_assert(sizeof(Summ) == 32, "Summ must stay 32 B");
+
 enum AgentState : uint8_t { S_PENDING, S_AWAIT, S_GEN, S_TOOL, S_PAUSED, S_DONE };
 enum EventKind : uint8_t { EV_NONE = 0, EV_GEN = 1, EV_TOOL = 2, EV_XFER = 3 };
 
@@ -85,6 +103,8 @@ struct SimDev {
   Slot* alt;
   u32* occ;
   u32* alt_occ;
+  Summ* summ;
+  Summ* alt_summ;
   u32 bucket_mask;    // buckets - 1 (power of two)
   u32 pad0;
   AgentDev* agents;
@@ -115,6 +135,8 @@ struct CacheDev {
   Slot* alt;
   u32* occ;
   u32* alt_occ;
+  Summ* summ;
+  Summ* alt_summ;
   u32 bucket_mask;
   u32 n_ops;
   const kvg_cache_op* ops;

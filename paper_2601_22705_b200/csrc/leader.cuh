@@ -538,6 +538,8 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   op.alt = D.alt;
   op.occ = D.occ;
   op.alt_occ = D.alt_occ;
+  op.summ = D.summ;
+  op.alt_summ = D.alt_summ;
   op.mask = D.bucket_mask;
   op.occ_n = 0;
   op.alt_n = 0;
@@ -1049,9 +1051,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
 // Kernels
 // ==========================================================================
 
+template <int kDepth>
 __device__ __forceinline__ void run_op(Op& op, Hist& h, int tid, int warp, int lane, int nw) {
   switch (op.kind) {
-    case OP_RANGE: coop_range(op, warp, lane, nw); break;
+    case OP_RANGE: coop_range<kDepth>(op, warp, lane, nw); break;
     case OP_EVICT: coop_evict(op, h, tid, warp, lane, nw); break;
     case OP_REBUILD: coop_rebuild(op, tid, warp, lane, nw); break;
     case OP_SCANFREE: coop_scanfree(op, warp, lane, nw); break;
@@ -1068,6 +1071,7 @@ __device__ __forceinline__ size_t smem_bytes_for(u32 n) {
          (nwords + (nwords + 31) / 32) * sizeof(u32);
 }
 
+template <int kDepth>
 __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   __shared__ Lead L;
   __shared__ Op op;
@@ -1126,20 +1130,28 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     if (tid == 0) leader_step(D, L, op);
     __syncthreads();
     if (op.kind == OP_EXIT) break;
-    run_op(op, h, tid, warp, lane, nw);
+    run_op<kDepth>(op, h, tid, warp, lane, nw);
     __syncthreads();
   }
 }
 
-// Throughput variant: one warp per simulation, register budget sized so ~24
-// simulations stay resident per SM (C4: 4096 sweep sims all in flight).
-__global__ void __launch_bounds__(32, 24) engine_kernel_small(const SimDev* __restrict__ sims) {
-  engine_body(sims);
+// Throughput variant: one warp per simulation, register budget (72) sized so 28
+// simulations stay resident per SM: 148 x 28 = 4144 >= the 4096 C4 sweep sims,
+// all in flight in one wave (measured: 24/SM leaves a 544-sim second wave).
+
+#ifndef KVG_SMALL_DEPTH
+#define KVG_SMALL_DEPTH 4
+#endif
+#ifndef KVG_SMALL_MINB
+#define KVG_SMALL_MINB 28
+#endif
+__global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small(const SimDev* __restrict__ sims) {
+  engine_body<KVG_SMALL_DEPTH>(sims);
 }
 
 // Latency variant: up to 32 warps cooperate on one big simulation.
 __global__ void __launch_bounds__(1024, 1) engine_kernel_big(const SimDev* __restrict__ sims) {
-  engine_body(sims);
+  engine_body<8>(sims);
 }
 
 }  // namespace kvg
