@@ -673,6 +673,19 @@ struct TreeCache {
     ++evict_calls;
     std::vector<Ent> init;
     collect_frontier(0, init);
+#ifdef KVO_CHECK_FLAT_FRONTIER
+    {  // the DFS frontier equals the flat set of frontier nodes (no counter
+       // under-count hides a frontier node below a device-less ancestor)
+      std::vector<Ent> flat;
+      for (std::uint32_t i = 1; i < nodes.size(); ++i)
+        if (nodes[i].alive && is_frontier(i))
+          flat.push_back({{nodes[i].last_access, nodes[i].ordinal}, i});
+      std::vector<Ent> a = init;
+      std::sort(a.begin(), a.end());
+      std::sort(flat.begin(), flat.end());
+      if (a != flat) throw StateError("flat frontier differs from the DFS frontier");
+    }
+#endif
     std::priority_queue<Ent, std::vector<Ent>, std::greater<Ent>> heap(std::greater<Ent>(),
                                                                        std::move(init));
     std::uint64_t reclaimed = 0;

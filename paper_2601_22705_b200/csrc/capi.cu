@@ -63,6 +63,27 @@ u64 max_context_pages(const kvg_population* p, u64 ps) {
   return best / ps;
 }
 
+// Offload-mode tree sizes (0 in discard mode): nodes partition the pages the
+// tree holds (device or host), at most every agent's whole context.
+u64 tree_nodes(const kvg_sim_desc& d) {
+  if (d.engine.eviction != KVG_EVICT_OFFLOAD) return 0;
+  const kvg_population* p = d.population;
+  u64 pages = 0;
+  for (u32 a = 0; a < p->agents; ++a) {
+    u64 c = p->prompt_tokens;
+    for (u32 s = 0; s < p->steps; ++s) {
+      const kvg_step_plan& sp = p->plans[static_cast<size_t>(a) * p->steps + s];
+      c += sp.gen_tokens + sp.obs_tokens;
+    }
+    pages += c / d.engine.page_size + 1;
+  }
+  return pages + 2;
+}
+u64 tree_hash_slots(u64 nodes) { return nodes ? next_pow2(4 * nodes) : 1; }
+u64 xfer_ring(const kvg_sim_desc& d) {
+  return d.engine.eviction == KVG_EVICT_OFFLOAD ? 4096 + 4ull * d.population->agents : 1;
+}
+
 // Dynamic shared memory holding a small simulation's hot agent records,
 // event heap and ready bitmaps (leader.cuh engine_body); 0 = keep in HBM.
 size_t hot_smem(u64 n) {

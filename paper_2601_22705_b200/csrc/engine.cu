@@ -69,6 +69,7 @@ enum OpKind : int {
   OP_EVICT,      // radix select + scatter free
   OP_REBUILD,    // rehash live buckets into the alternate table
   OP_SCANFREE,   // free pages by (owner, min index) over the whole table
+  OP_FRONTIER,   // offload tree: compact eviction-frontier nodes (tree.cuh)
 };
 
 enum RangeFlags : u32 {
@@ -143,6 +144,11 @@ struct Op {
   kvg_victim* vic;
   u64 vic_cap;
   unsigned long long* vic_n;
+  // offload tree frontier scan
+  const TNodeDev* tnodes;
+  FrEnt* fr;
+  u32 t_n;
+  unsigned int fr_n;
 };
 
 constexpr int kBins = 512;

@@ -102,8 +102,7 @@ bool validate_sim(const kvg_sim_desc& d, std::string* why) {
   if (!(e.phases.sat_threshold > 0 && e.phases.sat_threshold <= 1)) { *why = "phases.sat_threshold must be in (0,1]"; return false; }
   if (!(e.phases.hit_threshold >= 0 && e.phases.hit_threshold <= 1)) { *why = "phases.hit_threshold must be in [0,1]"; return false; }
   if (e.phases.hysteresis < 1) { *why = "phases.hysteresis must be >= 1"; return false; }
-  if (e.eviction == KVG_EVICT_OFFLOAD) { *why = "offload eviction is not implemented on the device engine yet"; return false; }
-  if (e.eviction != KVG_EVICT_DISCARD) { *why = "unknown eviction mode"; return false; }
+  if (e.eviction != KVG_EVICT_DISCARD && e.eviction != KVG_EVICT_OFFLOAD) { *why = "unknown eviction mode"; return false; }
   const kvg_policy& p = d.policy;
   if (p.kind > KVG_POLICY_AIMD) { *why = "unknown policy"; return false; }
   if ((p.kind == KVG_POLICY_REQUEST_CAP || p.kind == KVG_POLICY_AGENT_CAP) && p.cap < 1) { *why = "fixed cap policies need cap >= 1"; return false; }

@@ -74,6 +74,30 @@ struct AgentDev {     // 64 B: two agents per 128 B line
 };
 static_assert(sizeof(AgentDev) == 64, "AgentDev must stay 64 B");
 
+// Offload mode (EvictionMode::kOffload) keeps the reference's radix tree at
+// NODE granularity: reload promotes host nodes one node-chunk at a time and
+// the reference's children_with_device bookkeeping (including its quirk-Q1
+// over-count) decides which nodes can ever become eviction frontiers, so a
+// per-page model cannot reproduce it. One 64 B record per
+// node in a per-simulation pool; a node is found by the key of its first
+// page through an open-addressing head-key hash.
+struct TNodeDev {
+  u64 last_access, ordinal;
+  u32 parent, first_child, next_sib, prev_sib;  // 0 = none (node 0 is the root)
+  u32 start, npages;   // first page index, segment length in pages
+  u32 tail;            // owner (agent+1) of pages at or past the shared prompt
+  u32 device_slots;
+  int pin_count, cwd;  // cwd = children_with_device
+  u32 host, alive;
+};
+static_assert(sizeof(TNodeDev) == 64, "TNodeDev must stay 64 B");
+
+struct FrEnt {  // eviction frontier heap entry: (last_access, ordinal) order
+  u64 la, ord;
+  u32 id, pad;
+};
+constexpr u64 kTombKey = ~0ull - 1;  // head-hash tombstone
+
 // Event heap entry: (time, ordinal) lexicographic; key = ordinal << 20 | agent.
 struct HeapEnt {
   double t;
@@ -118,6 +142,15 @@ struct SimDev {
   u32* pin_hist;      // [shared_pages+1]: agents per shared-pin depth
   u32* pin_lvl;       // bitmap of non-empty pin_hist levels
   u32* hist;          // [2 * 512]: eviction radix-select histogram scratch
+  // ---- offload-mode tree (unused, 1-element regions, in discard mode)
+  TNodeDev* tnodes;   // [tcap] node pool, node 0 = root
+  u32* tfree;         // [tcap] free-node stack
+  u32* tstack;        // [tcap] DFS stack (subtree walks)
+  FrEnt* fr;          // [tcap] frontier heap
+  u64* hkeys;         // [hmask+1] head-key hash: page key of a node's first page
+  u32* hvals;         //           -> node id
+  double* xring;      // [xcap] link transfer end times (FIFO: ends never decrease)
+  u32 tcap, hmask, xcap, pad1;
   // ---- outputs
   kvg_agent_stats* stats;
   kvg_trace_row* trace;

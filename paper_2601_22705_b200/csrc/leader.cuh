@@ -34,6 +34,16 @@ enum Phase : int {
   PH_M_RESTORED,
   PH_BATCH_END,
   PH_GEN_DISCARDED,
+  // offload mode (node-level tree, tree.cuh)
+  PH_O_MEMBER,
+  PH_O_RELOAD_CHUNK,
+  PH_O_RELOAD_EVICTED,
+  PH_O_RELOAD_END,
+  PH_O_INSERT_START,
+  PH_O_INSERT_COUNT,
+  PH_O_INSERT_EVICTED,
+  PH_O_INSERT_FAIL,
+  PH_O_EVICT_POP,
   PH_DONE,
   PH_EXITED,
 };
@@ -73,6 +83,12 @@ struct Lead {
   u64 capacity, ps, shared_len, S;
   u32 n, steps, kind, cap;
   kvg_controller_config cfg;
+  // offload mode: tree pool, link queue, dispatch continuation (tree.cuh)
+  int offload, o_full, o_then, pad3;
+  u32 t_alloc, t_free_n, x_head, x_size, o_node, o_c;
+  u64 t_next_ord, offloaded, reloaded;
+  double pcie_busy, link_busy;
+  u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
 };
 
 // ------------------------------------------------------------------ helpers
@@ -301,6 +317,12 @@ __device__ __forceinline__ void sched_admission(Lead& L) {
   L.adm_o = L.ord++;
 }
 
+}  // namespace kvg
+
+#include "tree.cuh"
+
+namespace kvg {
+
 // cost_model.cpp:28-41 (compiled with -fmad=false: no contraction)
 __device__ __forceinline__ double prefill_t(const kvg_cost_params& c, u64 n, u64 ctx) {
   double x = static_cast<double>(n), y = static_cast<double>(ctx);
@@ -389,7 +411,7 @@ __device__ __noinline__ void on_tick(const SimDev& D, Lead& L) {
     row.pending = static_cast<u64>(L.pend_size) + L.paus_size;
     row.decoded_cum = L.decoded_cum;
     row.recompute_cum = L.rec_cum;
-    row.transfers = 0;
+    row.transfers = L.offload ? x_in_flight(D, L, L.clock) : 0;
     row.hit_matched = m;
     row.hit_requested = r;
     D.trace[i] = row;
@@ -438,9 +460,9 @@ __device__ __noinline__ void finalize(const SimDev& D, Lead& L) {
   r->status = L.status;
   r->n_phases = 0;
   r->ledger = L.ledger;
-  r->makespan = L.makespan;  // max(makespan, pcie_busy_until=0) (engine.cpp:401)
+  r->makespan = L.makespan < L.pcie_busy ? L.pcie_busy : L.makespan;  // engine.cpp:400
   r->device_busy = L.device_busy;
-  r->link_busy = 0.0;
+  r->link_busy = L.link_busy;
   r->decoded_tokens = L.decoded_cum;
   r->recompute_tokens = L.rec_cum;
   u64 rec_ev = 0, stalls = 0;
@@ -452,8 +474,8 @@ __device__ __noinline__ void finalize(const SimDev& D, Lead& L) {
   }
   r->recompute_events = rec_ev;
   r->stall_events = stalls;
-  r->offloaded_tokens = 0;
-  r->reloaded_tokens = 0;
+  r->offloaded_tokens = L.offloaded;
+  r->reloaded_tokens = L.reloaded;
   r->discarded_tokens = L.discarded;
   r->total_wait_time = wait;
   r->ticks = L.n_trace;
@@ -554,6 +576,12 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   op.implicit_pins = 1;
   op.pin_max = 0;
   op.agents = L.ag;
+  op.tnodes = D.tnodes;
+  op.fr = D.fr;
+  L.offload = D.engine.eviction == KVG_EVICT_OFFLOAD;
+  L.pcie_busy = L.link_busy = 0.0;
+  L.offloaded = L.reloaded = 0;
+  if (L.offload) tree_init(D, L);
   L.phase = PH_EVENT;
 }
 
@@ -637,7 +665,7 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
         row.pending = pending;
         row.decoded_cum = dec;
         row.recompute_cum = rec;
-        row.transfers = 0;
+        row.transfers = L.offload ? x_in_flight(D, L, clock) : 0;
         row.hit_matched = m;
         row.hit_requested = r;
         trace[i] = row;
@@ -683,6 +711,229 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   L.events = events;
   L.ticks = ticks;
   L.n_trace = n_trace;
+}
+
+// The successful tail of dispatch_member (engine.cpp:378-395): recompute
+// attribution, the member's cost-model times, InFlight, wait time, state.
+__device__ __noinline__ void member_success(const SimDev& D, Lead& L, u32 id, u64 ctx0,
+                                            u64 matched) {
+  AgentDev& a = L.ag[id];
+  const u64 stored = a.ctx - a.ctx % L.ps;
+  const u64 missing = ctx0 - matched;
+  const u64 rec = a.high_water > matched ? a.high_water - matched : 0;
+  const u64 fresh = missing - rec;
+  a.high_water = stored;
+  const kvg_step_plan& plan = D.plans[static_cast<size_t>(id) * L.steps + a.step];
+  Member m;
+  m.id = id;
+  m.pad = 0;
+  m.f = prefill_t(D.cost, fresh, ctx0);
+  m.r = prefill_t(D.cost, rec, ctx0);
+  m.d = decode_t(D.cost, plan.gen_tokens, ctx0);
+  m.t = m.f + m.r + m.d;
+  D.batch[L.batch_n++] = m;
+  a.f_gen = static_cast<u32>(plan.gen_tokens);
+  a.f_rec = static_cast<u32>(rec);
+  a.f_has_tool = plan.has_tool != 0;
+  a.f_obs = static_cast<u32>(plan.obs_tokens);
+  a.f_tool = plan.tool_latency;
+  D.stats[id].wait_time += L.clock - a.ready_since;
+  set_state(D, L, id, S_GEN);
+  a.stalled = 0;
+  ++L.agent_steps;
+}
+
+// Offload-mode dispatch_member (engine.cpp:337-396) on the node-level tree.
+// Returns true when it posted the cooperative frontier scan (the CTA runs
+// it, then PH_O_EVICT_POP resumes); false when the phase just advanced.
+__device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
+  TNodeDev* N = D.tnodes;
+  const u32 id = L.m_id;
+  AgentDev& a = L.ag[id];
+  auto post_frontier = [&](u64 need, int then) {
+    L.o_ev_need = need;
+    L.o_then = then;
+    op.kind = OP_FRONTIER;
+    op.fr_n = 0;
+    op.t_n = L.t_alloc;
+    L.phase = PH_O_EVICT_POP;
+  };
+  auto next_member = [&]() {
+    L.m_next = ready_next(D, L, id + 1);
+    L.phase = PH_O_MEMBER;
+  };
+  switch (L.phase) {
+    case PH_O_RELOAD_CHUNK:
+    case PH_O_RELOAD_EVICTED: {  // reload's chunk loop, cache_tree.cpp:337-366
+      const u64 len = L.m_ctx0, n = len / L.ps;
+      if (L.phase == PH_O_RELOAD_CHUNK) {
+        if (!(L.o_pos < len && L.o_promoted < L.o_hm)) {
+          L.phase = PH_O_RELOAD_END;
+          return false;
+        }
+        const u32 c = t_find_child(D, L, L.o_node, id, L.o_pos / L.ps, n);
+        if (c == 0 || !N[c].host) {
+          L.phase = PH_O_RELOAD_END;
+          return false;
+        }
+        u64 ka = t_common(D, L, c, id, L.o_pos / L.ps, n);
+        bool full = ka == N[c].npages;
+        const u64 want = (L.o_hm - L.o_promoted) / L.ps;
+        if (ka > want) {
+          ka = want;
+          full = false;
+        }
+        if (ka == 0) {
+          L.phase = PH_O_RELOAD_END;
+          return false;
+        }
+        if (ka < N[c].npages) t_split(D, L, c, ka);
+        L.o_c = c;
+        L.o_ka = ka;
+        L.o_full = full;
+        if (L.capacity - L.used < ka) {
+          post_frontier(ka - (L.capacity - L.used), PH_O_RELOAD_EVICTED);
+          return true;
+        }
+      } else if (L.capacity - L.used < L.o_ka) {  // evicted, still no room
+        L.phase = PH_O_RELOAD_END;
+        return false;
+      }
+      const u32 c = L.o_c;
+      N[c].host = 0;
+      N[c].device_slots = static_cast<u32>(L.o_ka);
+      N[c].last_access = L.o_now;
+      L.used += L.o_ka;
+      t_gain(D, c);
+      L.o_promoted += L.o_ka * L.ps;
+      L.o_pos += L.o_ka * L.ps;
+      L.o_node = c;
+      L.phase = L.o_full ? PH_O_RELOAD_CHUNK : PH_O_RELOAD_END;
+      return false;
+    }
+    case PH_O_RELOAD_END: {  // engine.cpp:347-360
+      x_account(D, L, L.o_offl);
+      log_rec(D, L, KVG_LOG_RELOAD, id, L.o_promoted, L.o_offl);
+      if (L.o_promoted > 0) {
+        const u64 m = L.o_matched;
+        t_pin(D, L, id, m + L.o_promoted, +1);
+        t_pin(D, L, id, m, -1);
+        a.pinned_pg = static_cast<u32>((m + L.o_promoted) / L.ps);
+        L.reloaded += L.o_promoted;
+        const double end =
+            x_enqueue(D, L, static_cast<double>(L.o_promoted) * D.cost.bytes_per_token);
+        D.stats[id].wait_time += L.clock - a.ready_since;
+        set_state(D, L, id, S_GEN);
+        sched_agent(D, L, id, end, EV_XFER);
+        next_member();
+        return false;
+      }
+      L.phase = PH_O_INSERT_START;
+      return false;
+    }
+    case PH_O_INSERT_START: {
+      const kvg_step_plan& plan = D.plans[static_cast<size_t>(id) * L.steps + a.step];
+      a.ctx += plan.gen_tokens;  // append_tokens
+      L.m_nafter = a.ctx / L.ps;
+      L.o_offl = 0;
+      L.phase = PH_O_INSERT_COUNT;
+      return false;
+    }
+    case PH_O_INSERT_COUNT:
+    case PH_O_INSERT_EVICTED: {  // insert, cache_tree.cpp:170-228
+      if (L.phase == PH_O_INSERT_EVICTED && L.o_ev_rec == 0) {
+        L.phase = PH_O_INSERT_FAIL;
+        return false;
+      }
+      u64 created = 0;
+      if (L.m_nafter > 0) {
+        const u64 need = t_missing(D, L, id, L.m_nafter);
+        const u64 free_slots = L.capacity - L.used;
+        if (need > free_slots) {
+          post_frontier(need - free_slots, PH_O_INSERT_EVICTED);
+          return true;
+        }
+        created = t_insert_commit(D, L, id, L.m_nafter);
+      }
+      x_account(D, L, L.o_offl);
+      const u64 stored = a.ctx - a.ctx % L.ps;
+      log_rec(D, L, KVG_LOG_INSERT, id, 1, stored);
+      t_pin(D, L, id, stored, +1);
+      t_pin(D, L, id, L.o_matched, -1);
+      a.pinned_pg = static_cast<u32>(stored / L.ps);
+      L.created_pages += created;
+      if (L.m_nafter > 0) L.refreshed_pages += L.o_matched / L.ps;
+      member_success(D, L, id, L.m_ctx0, L.o_matched);
+      next_member();
+      return false;
+    }
+    case PH_O_INSERT_FAIL: {  // engine.cpp:366-373
+      x_account(D, L, L.o_offl);
+      log_rec(D, L, KVG_LOG_INSERT, id, 0, 0);
+      a.ctx = L.m_ctx0;
+      t_pin(D, L, id, L.o_matched, -1);
+      a.pinned_pg = 0;
+      ++D.stats[id].stall_events;
+      next_member();
+      return false;
+    }
+    case PH_O_EVICT_POP: {
+      L.evict_scanned += L.t_alloc;
+      L.o_ev_rec = t_evict_pop(D, L, op.fr_n, L.o_ev_need, &L.o_offl);
+      op.kind = OP_NONE;
+      L.phase = L.o_then;
+      return false;
+    }
+    default: {  // PH_O_MEMBER: match, pins, reload start (engine.cpp:337-346)
+      const u32 nid = L.m_next;
+      if (nid == NIL) {
+        L.phase = PH_BATCH_END;
+        return false;
+      }
+      AgentDev& b = L.ag[nid];
+      L.m_id = nid;
+      L.m_ctx0 = b.ctx;
+      L.m_nctx = b.ctx / L.ps;
+      u64 hm = 0;
+      const u64 matched = t_match(D, L, nid, b.ctx, &hm);
+      const u64 r = (matched + hm) / L.ps;
+      L.lookups += r + (r < L.m_nctx ? 1 : 0);
+      L.hit_pages += matched / L.ps;
+      log_rec(D, L, KVG_LOG_MATCH, nid, matched, hm);
+      t_pin(D, L, nid, matched, +1);
+      if (b.pinned_pg > 0) t_pin(D, L, nid, static_cast<u64>(b.pinned_pg) * L.ps, -1);
+      b.pinned_pg = static_cast<u32>(matched / L.ps);
+      L.o_matched = matched;
+      L.o_hm = hm;
+      L.o_offl = 0;
+      L.o_promoted = 0;
+      if (hm == 0) {
+        L.phase = PH_O_INSERT_START;
+        return false;
+      }
+      // reload: walk to `from` = matched (cache_tree.cpp:323-335)
+      if (matched >= b.ctx) {
+        L.phase = PH_O_RELOAD_END;
+        return false;
+      }
+      u32 node = 0;
+      u64 pos = 0;
+      while (pos < matched) {
+        const u32 c = t_find_child(D, L, node, nid, pos / L.ps, L.m_nctx);
+        if (c == 0 || pos + static_cast<u64>(N[c].npages) * L.ps > matched) {
+          fail(L, E_OFFLOAD);
+          return false;
+        }
+        pos += static_cast<u64>(N[c].npages) * L.ps;
+        node = c;
+      }
+      L.o_now = ++L.cclock;
+      L.o_pos = matched;
+      L.o_node = node;
+      L.phase = PH_O_RELOAD_CHUNK;
+      return false;
+    }
+  }
 }
 
 // Runs the state machine until a cooperative op is posted in `op`.
@@ -755,7 +1006,12 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         AgentDev& a = L.ag[agent];
         if (kind == EV_GEN) {  // on_generation_complete (engine.cpp:184-222)
           L.makespan = L.makespan < L.clock ? L.clock : L.makespan;
-          set_pinned(D, L, agent, 0);  // unpin(pinned_len) — implicit pins
+          if (!L.offload) {
+            set_pinned(D, L, agent, 0);  // unpin(pinned_len) — implicit pins
+          } else if (a.pinned_pg > 0) {  // engine.cpp:188-191 on the tree
+            t_pin(D, L, agent, static_cast<u64>(a.pinned_pg) * L.ps, -1);
+            a.pinned_pg = 0;
+          }
           kvg_agent_stats& st = D.stats[agent];
           L.decoded_cum += a.f_gen;
           L.rec_cum += a.f_rec;
@@ -765,6 +1021,12 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           ++a.step;
           if (a.step >= L.steps) {
             set_state(D, L, agent, S_DONE);
+            if (L.offload) {  // discard_suffix on the tree (device and host pages)
+              op.freed = static_cast<unsigned int>(t_discard(D, L, agent, a.ctx, L.shared_len));
+              op.err = E_NONE;
+              L.phase = PH_GEN_DISCARDED;
+              continue;
+            }
             // discard_suffix(context, shared_len) (cache_tree.cpp:404-437):
             // page_ceil(shared_len) keeps a straddling page (quirk Q2)
             const u64 fp = (L.shared_len + L.ps - 1) / L.ps;
@@ -797,6 +1059,14 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           ++L.events;
           continue;
         }
+        if (kind == EV_XFER) {  // on_transfer_complete (engine.cpp:237-243)
+          L.makespan = L.makespan < L.clock ? L.clock : L.makespan;
+          set_state(D, L, agent, S_AWAIT);
+          a.ready_since = L.clock;
+          sched_admission(L);
+          ++L.events;
+          continue;
+        }
         if (kind == EV_TOOL) {  // on_tool_complete (engine.cpp:224-235)
           L.makespan = L.makespan < L.clock ? L.clock : L.makespan;
           a.ctx += a.f_obs;
@@ -815,6 +1085,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       }
       // --------------------------------------------- dispatch_member (337-396)
       case PH_MEMBER: {
+        if (L.offload) {
+          L.phase = PH_O_MEMBER;
+          continue;
+        }
         const u32 id = L.m_next;
         if (id == NIL) {
           L.phase = PH_BATCH_END;
@@ -945,29 +1219,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         const u64 matched = L.m_f * L.ps;
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 1, stored);
         set_pinned(D, L, L.m_id, stored);  // pin(stored), unpin(matched)
-        const u64 ctx0 = L.m_ctx0;
-        const u64 missing = ctx0 - matched;
-        const u64 rec = a.high_water > matched ? a.high_water - matched : 0;
-        const u64 fresh = missing - rec;
-        a.high_water = stored;
-        const kvg_step_plan& plan = D.plans[static_cast<size_t>(L.m_id) * L.steps + a.step];
-        Member m;
-        m.id = L.m_id;
-        m.pad = 0;
-        m.f = prefill_t(D.cost, fresh, ctx0);
-        m.r = prefill_t(D.cost, rec, ctx0);
-        m.d = decode_t(D.cost, plan.gen_tokens, ctx0);
-        m.t = m.f + m.r + m.d;
-        D.batch[L.batch_n++] = m;
-        a.f_gen = static_cast<u32>(plan.gen_tokens);
-        a.f_rec = static_cast<u32>(rec);
-        a.f_has_tool = plan.has_tool != 0;
-        a.f_obs = static_cast<u32>(plan.obs_tokens);
-        a.f_tool = plan.tool_latency;
-        D.stats[L.m_id].wait_time += L.clock - a.ready_since;
-        set_state(D, L, L.m_id, S_GEN);
-        a.stalled = 0;
-        ++L.agent_steps;
+        member_success(D, L, L.m_id, L.m_ctx0, matched);
         L.m_next = ready_next(D, L, L.m_id + 1);
         L.phase = PH_MEMBER;
         continue;
@@ -1022,8 +1274,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       case PH_GEN_DISCARDED: {
         if (op.err) fail(L, op.err);
         const u32 id = L.ev_agent;
-        L.used -= op.freed;
-        L.discarded += static_cast<u64>(op.freed) * L.ps;
+        if (!L.offload) {  // (the tree discard accounted for itself)
+          L.used -= op.freed;
+          L.discarded += static_cast<u64>(op.freed) * L.ps;
+        }
         log_rec(D, L, KVG_LOG_DISCARD, id, 0, op.freed);
         act_erase(D, L, id);  // on_request_complete / on_agent_finished
         ++L.finished;
@@ -1035,6 +1289,17 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         L.phase = PH_EVENT;
         continue;
       }
+      case PH_O_MEMBER:
+      case PH_O_RELOAD_CHUNK:
+      case PH_O_RELOAD_EVICTED:
+      case PH_O_RELOAD_END:
+      case PH_O_INSERT_START:
+      case PH_O_INSERT_COUNT:
+      case PH_O_INSERT_EVICTED:
+      case PH_O_INSERT_FAIL:
+      case PH_O_EVICT_POP:
+        if (offload_step(D, L, op)) return;
+        continue;
       case PH_DONE:
         finalize(D, L);
         L.phase = PH_EXITED;
@@ -1058,6 +1323,7 @@ __device__ __forceinline__ void run_op(Op& op, Hist& h, int tid, int warp, int l
     case OP_EVICT: coop_evict(op, h, tid, warp, lane, nw); break;
     case OP_REBUILD: coop_rebuild(op, tid, warp, lane, nw); break;
     case OP_SCANFREE: coop_scanfree(op, warp, lane, nw); break;
+    case OP_FRONTIER: coop_frontier(op, warp, lane, nw); break;
     default: break;
   }
 }

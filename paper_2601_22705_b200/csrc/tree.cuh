@@ -1,0 +1,496 @@
+// Offload-mode radix tree (EvictionMode::kOffload) for the engine leader
+// (included by leader.cuh after the Lead struct).
+//
+// Node-granular restatement of cache_tree.cpp, step for step with the CPU
+// oracle's TreeCache (oracle/kvoracle.cpp), which is pinned per event to the
+// unmodified reference. Everything here runs on the leader thread except the
+// eviction frontier scan, which is a cooperative op (OP_FRONTIER, engine.cu):
+// all warps of the CTA sweep the node pool and compact the frontier nodes
+// (device, slots > 0, unpinned, children_with_device == 0) into a heap array.
+// The flat sweep equals the reference's collect_frontier DFS (cache_tree.cpp:
+// 236-249): checked on every offload fixture (KVO_CHECK_FLAT_FRONTIER).
+#pragma once
+
+namespace kvg {
+
+// ------------------------------------------------------------ node pool
+
+__device__ __forceinline__ u64 t_key(const Lead& L, u32 a, u64 k) {
+  return ((k < L.S ? 0ull : static_cast<u64>(a) + 1) << 32) | k;
+}
+__device__ __forceinline__ u64 t_nkey(const Lead& L, const TNodeDev& n, u64 k) {
+  return ((k < L.S ? 0ull : static_cast<u64>(n.tail)) << 32) | k;
+}
+__device__ __forceinline__ bool t_subdev(const TNodeDev& n) {
+  return n.device_slots > 0 || n.cwd > 0;
+}
+
+__device__ u32 h_find(const SimDev& D, u64 key) {
+  u32 i = static_cast<u32>(hash64(key)) & D.hmask;
+  for (;;) {
+    const u64 k = D.hkeys[i];
+    if (k == key) return D.hvals[i];
+    if (k == kEmptyKey) return 0;
+    i = (i + 1) & D.hmask;
+  }
+}
+__device__ void h_insert(const SimDev& D, u64 key, u32 v) {
+  u32 i = static_cast<u32>(hash64(key)) & D.hmask;
+  for (;;) {
+    const u64 k = D.hkeys[i];
+    if (k == kEmptyKey || k == kTombKey) {
+      D.hkeys[i] = key;
+      D.hvals[i] = v;
+      return;
+    }
+    i = (i + 1) & D.hmask;
+  }
+}
+__device__ void h_erase(const SimDev& D, u64 key) {
+  u32 i = static_cast<u32>(hash64(key)) & D.hmask;
+  for (;;) {
+    const u64 k = D.hkeys[i];
+    if (k == key) {
+      D.hkeys[i] = kTombKey;
+      return;
+    }
+    if (k == kEmptyKey) return;
+    i = (i + 1) & D.hmask;
+  }
+}
+
+__device__ u32 t_alloc(const SimDev& D, Lead& L) {
+  if (L.t_free_n > 0) return D.tfree[--L.t_free_n];
+  if (L.t_alloc >= D.tcap) {
+    fail(L, E_TABLE_FULL);
+    return 0;
+  }
+  return L.t_alloc++;
+}
+
+__device__ void t_add_child(const SimDev& D, u32 p, u32 c) {
+  TNodeDev* N = D.tnodes;
+  N[c].parent = p;
+  N[c].prev_sib = 0;
+  N[c].next_sib = N[p].first_child;
+  if (N[p].first_child) N[N[p].first_child].prev_sib = c;
+  N[p].first_child = c;
+}
+__device__ void t_remove_child(const SimDev& D, u32 p, u32 c) {
+  TNodeDev* N = D.tnodes;
+  if (N[c].prev_sib) N[N[c].prev_sib].next_sib = N[c].next_sib;
+  else N[p].first_child = N[c].next_sib;
+  if (N[c].next_sib) N[N[c].next_sib].prev_sib = N[c].prev_sib;
+}
+
+// find_child (cache_tree.cpp:56-66): a full page of the sequence is needed.
+__device__ u32 t_find_child(const SimDev& D, const Lead& L, u32 node, u32 a, u64 p, u64 n_full) {
+  if (p >= n_full) return 0;
+  const u32 c = h_find(D, t_key(L, a, p));
+  return (c != 0 && D.tnodes[c].parent == node) ? c : 0;
+}
+
+// common_len in whole pages (a partial trailing page never counts).
+__device__ __forceinline__ u64 t_common(const SimDev& D, const Lead& L, u32 c, u32 a, u64 p,
+                                        u64 n_full) {
+  const TNodeDev& n = D.tnodes[c];
+  u64 k = n.npages < n_full - p ? n.npages : n_full - p;
+  if (n.tail != a + 1) {
+    const u64 sh = L.S > p ? L.S - p : 0;
+    k = k < sh ? k : sh;
+  }
+  return k;
+}
+
+// split_node, cache_tree.cpp:68-92 (offset in pages). Returns the suffix.
+__device__ u32 t_split(const SimDev& D, Lead& L, u32 id, u64 off) {
+  const u32 sid = t_alloc(D, L);
+  if (sid == 0) return id;
+  TNodeDev* N = D.tnodes;
+  TNodeDev n = N[id];
+  TNodeDev s;
+  s.start = n.start + static_cast<u32>(off);
+  s.npages = n.npages - static_cast<u32>(off);
+  s.tail = n.tail;
+  s.first_child = n.first_child;
+  s.parent = id;
+  s.next_sib = s.prev_sib = 0;
+  s.last_access = n.last_access;
+  s.ordinal = L.t_next_ord++;
+  s.host = n.host;
+  s.pin_count = n.pin_count;
+  s.cwd = n.cwd;
+  s.alive = 1;
+  s.device_slots = 0;
+  if (!n.host) {
+    s.device_slots = n.device_slots - static_cast<u32>(off);
+    N[id].device_slots = static_cast<u32>(off);
+  }
+  N[sid] = s;
+  for (u32 c = s.first_child; c != 0; c = N[c].next_sib) N[c].parent = sid;
+  N[id].npages = static_cast<u32>(off);
+  N[id].first_child = 0;
+  N[id].cwd = t_subdev(s) ? 1 : 0;
+  t_add_child(D, id, sid);
+  h_insert(D, t_nkey(L, s, s.start), sid);
+  return sid;
+}
+
+__device__ void t_gain(const SimDev& D, u32 id) {  // propagate_gain, cache_tree.cpp:94-102
+  TNodeDev* N = D.tnodes;
+  u32 p = N[id].parent;
+  for (;;) {
+    const bool had = t_subdev(N[p]);
+    N[p].cwd += 1;
+    if (had || p == 0) break;
+    p = N[p].parent;
+  }
+}
+__device__ void t_loss(const SimDev& D, u32 id) {  // propagate_loss, cache_tree.cpp:104-112
+  TNodeDev* N = D.tnodes;
+  u32 p = N[id].parent;
+  for (;;) {
+    N[p].cwd -= 1;
+    if (t_subdev(N[p]) || p == 0) break;
+    p = N[p].parent;
+  }
+}
+
+__device__ __forceinline__ bool t_frontier(const TNodeDev& n) {  // cache_tree.cpp:230-234
+  return n.alive && !n.host && n.device_slots > 0 && n.pin_count == 0 && n.cwd == 0;
+}
+
+// OP_FRONTIER: every warp sweeps the node pool, one lane per 64 B record
+// (coalesced), and compacts the frontier nodes into op.fr with one atomic per
+// warp (ballot + rank).
+__device__ __noinline__ void coop_frontier(Op& op, int warp, int lane, int nw) {
+  const TNodeDev* N = op.tnodes;
+  const u32 n = op.t_n;
+  for (u32 base = static_cast<u32>(warp) * 32u; base < n; base += static_cast<u32>(nw) * 32u) {
+    const u32 i = base + lane;
+    bool f = false;
+    u64 la = 0, ord = 0;
+    if (i < n) {
+      const TNodeDev& x = N[i];
+      f = t_frontier(x);
+      la = x.last_access;
+      ord = x.ordinal;
+    }
+    const unsigned m = __ballot_sync(FULL, f);
+    if (m == 0) continue;
+    u32 b0 = 0;
+    if (lane == 0) b0 = atomicAdd(&op.fr_n, static_cast<unsigned>(__popc(m)));
+    b0 = __shfl_sync(FULL, b0, 0);
+    if (f) op.fr[b0 + __popc(m & ((1u << lane) - 1u))] = FrEnt{la, ord, i, 0};
+  }
+}
+
+// ------------------------------------------------------------ operations
+
+// match_prefix, cache_tree.cpp:114-142. Returns matched tokens.
+__device__ __noinline__ u64 t_match(const SimDev& D, Lead& L, u32 a, u64 len, u64* host_matched) {
+  const u64 now = ++L.cclock;
+  const u64 n = len / L.ps;
+  TNodeDev* N = D.tnodes;
+  u32 node = 0;
+  u64 pos = 0, matched = 0, hm = 0;
+  bool host_phase = false;
+  while (pos < n) {
+    const u32 c = t_find_child(D, L, node, a, pos, n);
+    if (c == 0) break;
+    if (N[c].host) host_phase = true;
+    const u64 ka = t_common(D, L, c, a, pos, n);
+    const bool full = ka == N[c].npages;
+    if (ka == 0) break;
+    if (!full) t_split(D, L, c, ka);
+    if (host_phase) {
+      hm += ka;
+    } else {
+      N[c].last_access = now;
+      matched += ka;
+    }
+    pos += ka;
+    node = c;
+    if (!full) break;
+  }
+  L.hit_m += static_cast<double>(matched * L.ps);
+  L.hit_r += static_cast<double>(len);
+  *host_matched = hm * L.ps;
+  return matched * L.ps;
+}
+
+// count_missing_slots, cache_tree.cpp:144-168 (pages).
+__device__ __noinline__ u64 t_missing(const SimDev& D, const Lead& L, u32 a, u64 n) {
+  const TNodeDev* N = D.tnodes;
+  u32 node = 0;
+  u64 pos = 0, m = 0;
+  while (pos < n) {
+    const u32 c = t_find_child(D, L, node, a, pos, n);
+    if (c == 0) return m + (n - pos);
+    const u64 ka = t_common(D, L, c, a, pos, n);
+    const bool full = ka == N[c].npages;
+    if (ka == 0) return m;
+    if (N[c].host) m += ka;
+    pos += ka;
+    node = c;
+    if (!full) return m + (n - pos);
+  }
+  return m;
+}
+
+// insert after the eviction loop (cache_tree.cpp:188-227): the clock bump,
+// the path walk (promoting host nodes) and the new leaf. Returns new device
+// slots.
+__device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64 n) {
+  const u64 now = ++L.cclock;
+  TNodeDev* N = D.tnodes;
+  u32 node = 0;
+  u64 pos = 0, inserted = 0;
+  while (pos < n) {
+    const u32 c = t_find_child(D, L, node, a, pos, n);
+    if (c == 0) {
+      const u32 l = t_alloc(D, L);
+      if (l == 0) return inserted;
+      TNodeDev ln;
+      ln.start = static_cast<u32>(pos);
+      ln.npages = static_cast<u32>(n - pos);
+      ln.tail = a + 1;
+      ln.parent = node;
+      ln.first_child = ln.next_sib = ln.prev_sib = 0;
+      ln.last_access = now;
+      ln.ordinal = L.t_next_ord++;
+      ln.device_slots = static_cast<u32>(n - pos);
+      ln.pin_count = 0;
+      ln.cwd = 0;
+      ln.host = 0;
+      ln.alive = 1;
+      N[l] = ln;
+      L.used += n - pos;
+      inserted += n - pos;
+      t_add_child(D, node, l);
+      h_insert(D, t_key(L, a, pos), l);
+      t_gain(D, l);
+      break;
+    }
+    const u64 ka = t_common(D, L, c, a, pos, n);
+    const bool full = ka == N[c].npages;
+    if (ka == 0) break;
+    if (!full) t_split(D, L, c, ka);
+    if (N[c].host) {
+      const u32 pages = N[c].npages;
+      N[c].host = 0;
+      N[c].device_slots = pages;
+      L.used += pages;
+      inserted += pages;
+      t_gain(D, c);
+    }
+    N[c].last_access = now;
+    pos += ka;
+    node = c;
+  }
+  return inserted;
+}
+
+// pin / unpin, cache_tree.cpp:370-402: every node covering [0, len).
+__device__ __noinline__ void t_pin(const SimDev& D, Lead& L, u32 a, u64 len, int delta) {
+  TNodeDev* N = D.tnodes;
+  const u64 nf = (len + L.ps - 1) / L.ps;
+  u32 node = 0;
+  u64 pos = 0;  // tokens
+  while (pos < len) {
+    const u32 c = (pos % L.ps == 0) ? t_find_child(D, L, node, a, pos / L.ps, nf) : 0;
+    if (c == 0 || pos + static_cast<u64>(N[c].npages) * L.ps > len) {
+      fail(L, E_PIN_MISSING);
+      return;
+    }
+    if (delta < 0 && N[c].pin_count == 0) {
+      fail(L, E_UNPIN_UNDERFLOW);
+      return;
+    }
+    N[c].pin_count += delta;
+    pos += static_cast<u64>(N[c].npages) * L.ps;
+    node = c;
+  }
+}
+
+// discard_suffix, cache_tree.cpp:404-437. Returns device slots freed; adds the
+// dropped tokens (device and host) to L.discarded.
+__device__ __noinline__ u64 t_discard(const SimDev& D, Lead& L, u32 a, u64 len, u64 from) {
+  TNodeDev* N = D.tnodes;
+  from = (from + L.ps - 1) / L.ps * L.ps;
+  if (from >= len) return 0;
+  const u64 n = len / L.ps;
+  u32 node = 0;
+  u64 pos = 0;  // tokens
+  while (pos < from) {
+    const u32 c = t_find_child(D, L, node, a, pos / L.ps, n);
+    if (c == 0) return 0;
+    const u64 kp = t_common(D, L, c, a, pos / L.ps, n);
+    if (kp < N[c].npages && pos + kp * L.ps < from) return 0;
+    if (static_cast<u64>(N[c].npages) * L.ps > from - pos) t_split(D, L, c, (from - pos) / L.ps);
+    pos += static_cast<u64>(N[c].npages) * L.ps;
+    node = c;
+  }
+  const u32 b = t_find_child(D, L, node, a, from / L.ps, n);
+  if (b == 0) return 0;
+  u64 slots = 0, toks = 0;
+  long long pins = 0;
+  u32 sp = 0;
+  D.tstack[sp++] = b;
+  while (sp > 0) {
+    const u32 x = D.tstack[--sp];
+    slots += N[x].device_slots;
+    toks += static_cast<u64>(N[x].npages) * L.ps;
+    pins += N[x].pin_count;
+    for (u32 c = N[x].first_child; c != 0; c = N[c].next_sib) D.tstack[sp++] = c;
+  }
+  if (pins > 0) {
+    fail(L, E_DISCARD_PINNED);
+    return 0;
+  }
+  if (t_subdev(N[b])) t_loss(D, b);
+  L.used -= slots;
+  L.discarded += toks;
+  t_remove_child(D, node, b);
+  // free the subtree: its head keys leave the hash, its nodes the pool
+  sp = 0;
+  D.tstack[sp++] = b;
+  while (sp > 0) {
+    const u32 x = D.tstack[--sp];
+    for (u32 c = N[x].first_child; c != 0; c = N[c].next_sib) D.tstack[sp++] = c;
+    h_erase(D, t_nkey(L, N[x], N[x].start));
+    N[x].alive = 0;
+    D.tfree[L.t_free_n++] = x;
+  }
+  return slots;
+}
+
+// ------------------------------------------------------------ eviction
+
+__device__ __forceinline__ bool fr_less(const FrEnt& x, const FrEnt& y) {
+  return x.la < y.la || (x.la == y.la && x.ord < y.ord);
+}
+__device__ void fr_sift_down(FrEnt* h, u32 n, u32 i) {
+  const FrEnt e = h[i];
+  for (;;) {
+    u32 c = 2 * i + 1;
+    if (c >= n) break;
+    if (c + 1 < n && fr_less(h[c + 1], h[c])) ++c;
+    if (!fr_less(h[c], e)) break;
+    h[i] = h[c];
+    i = c;
+  }
+  h[i] = e;
+}
+__device__ void fr_push(FrEnt* h, u32& n, const FrEnt& e) {
+  u32 i = n++;
+  while (i > 0) {
+    const u32 p = (i - 1) >> 1;
+    if (!fr_less(e, h[p])) break;
+    h[i] = h[p];
+    i = p;
+  }
+  h[i] = e;
+}
+
+// evict (cache_tree.cpp:270-319) after OP_FRONTIER compacted the initial
+// frontier into D.fr[0, nf): heap pops by (last_access, ordinal), tail splits,
+// offload to the host tier, parents pushed as they become frontier. Returns
+// reclaimed slots; offloaded tokens accumulate into *offl.
+__device__ __noinline__ u64 t_evict_pop(const SimDev& D, Lead& L, u32 nf, u64 needed, u64* offl) {
+  TNodeDev* N = D.tnodes;
+  FrEnt* h = D.fr;
+  for (u32 i = nf / 2; i-- > 0;) fr_sift_down(h, nf, i);
+  u64 reclaimed = 0;
+  const unsigned long long log0 = L.n_log;
+  log_rec(D, L, KVG_LOG_EVICT, L.m_id, needed, 0);
+  while (reclaimed < needed && nf > 0) {
+    const FrEnt e = h[0];
+    h[0] = h[--nf];
+    if (nf > 0) fr_sift_down(h, nf, 0);
+    const u32 id = e.id;
+    if (!t_frontier(N[id]) || N[id].last_access != e.la || N[id].ordinal != e.ord) continue;
+    const u64 slots = N[id].device_slots;
+    const u64 take = slots < needed - reclaimed ? slots : needed - reclaimed;
+    u32 v = id;
+    if (take < slots) v = t_split(D, L, id, N[id].npages - take);
+    const TNodeDev vn = N[v];
+    if (D.log != nullptr)
+      for (u64 k = static_cast<u64>(vn.start) + vn.npages; k-- > vn.start;)
+        log_rec(D, L, KVG_LOG_VICTIM, L.m_id, t_nkey(L, vn, k), vn.last_access);
+    L.used -= vn.device_slots;
+    reclaimed += vn.device_slots;
+    const u64 toks = static_cast<u64>(vn.npages) * L.ps;
+    L.offloaded += toks;
+    *offl += toks;
+    N[v].device_slots = 0;
+    N[v].host = 1;
+    t_loss(D, v);
+    const u32 parent = vn.parent;
+    if (parent != 0 && t_frontier(N[parent]))
+      fr_push(h, nf, FrEnt{N[parent].last_access, N[parent].ordinal, parent, 0});
+  }
+  if (D.log != nullptr && log0 < D.log_cap) D.log[log0].b = reclaimed;
+  ++L.evict_calls;
+  L.evicted += reclaimed;
+  return reclaimed;
+}
+
+// ------------------------------------------------------------ link queue
+
+// transfers_in_flight, engine.cpp:156-160. Transfer ends never decrease
+// (each starts at max(clock, pcie_busy_until) with a non-negative duration),
+// so the reference's multiset is a FIFO ring here.
+__device__ __forceinline__ u32 x_in_flight(const SimDev& D, Lead& L, double clock) {
+  while (L.x_size > 0 && D.xring[L.x_head] <= clock) {
+    L.x_head = L.x_head + 1 == D.xcap ? 0 : L.x_head + 1;
+    --L.x_size;
+  }
+  return L.x_size;
+}
+
+// enqueue_transfer, engine.cpp:164-174; transfer_time, cost_model.cpp:43-47.
+__device__ double x_enqueue(const SimDev& D, Lead& L, double bytes) {
+  const u32 depth = x_in_flight(D, L, L.clock) + 1;
+  const double dur = D.cost.transfer_sync_overhead +
+                     bytes * static_cast<double>(depth) / D.cost.pcie_bandwidth;
+  const double start = L.clock < L.pcie_busy ? L.pcie_busy : L.clock;
+  const double end = start + dur;
+  L.pcie_busy = end;
+  L.ledger.transfer += dur;
+  L.link_busy += dur;
+  if (L.x_size >= D.xcap) {
+    fail(L, E_TABLE_FULL);
+    return end;
+  }
+  u32 tail = L.x_head + L.x_size;
+  if (tail >= D.xcap) tail -= D.xcap;
+  D.xring[tail] = end;
+  ++L.x_size;
+  return end;
+}
+
+// account_evictions, engine.cpp:178-182
+__device__ __forceinline__ void x_account(const SimDev& D, Lead& L, u64 offl_tokens) {
+  if (offl_tokens > 0)
+    x_enqueue(D, L, static_cast<double>(offl_tokens) * D.cost.bytes_per_token);
+}
+
+__device__ void tree_init(const SimDev& D, Lead& L) {
+  TNodeDev r;
+  r.last_access = r.ordinal = 0;
+  r.parent = r.first_child = r.next_sib = r.prev_sib = 0;
+  r.start = r.npages = r.tail = r.device_slots = 0;
+  r.pin_count = r.cwd = 0;
+  r.host = 0;
+  r.alive = 0;  // the root is never a frontier candidate
+  D.tnodes[0] = r;
+  L.t_alloc = 1;
+  L.t_free_n = 0;
+  L.t_next_ord = 0;
+  L.x_head = L.x_size = 0;
+  L.pcie_busy = L.link_busy = 0.0;
+  L.offloaded = L.reloaded = 0;
+}
+
+}  // namespace kvg

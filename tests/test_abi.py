@@ -67,7 +67,6 @@ def _spec(**over):
     ({"engine.hit_window_decay": 1.0}, "hit_window_decay"),
     ({"controller.beta": 1.0}, "beta"),
     ({"controller.u_low": 0.9}, "thresholds"),
-    ({"engine.eviction": "offload"}, "offload"),
 ])
 def test_invalid_descriptors_are_config_errors(over, msg):
     with pytest.raises(engine.EngineError) as e:
