@@ -41,7 +41,7 @@ def parse_args():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--workload", default="c4", choices=["c4", "c2", "c1"])
+    p.add_argument("--workload", default="c4", choices=["c4", "c2", "c3", "c3off", "c1"])
     p.add_argument("--sims", type=int, default=4096)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
@@ -63,6 +63,12 @@ def build_scenarios(workload: str, rank: int, sims: int):
                 f"prompts, 12,629-page cache, Qwen3-32B KV sizing), workload seed {42 + rank}")
     elif workload == "c2":
         desc = "C2: 1024 agents x 16 steps, 4K->55.7K contexts, 2,038,926-page cache, aimd"
+    elif workload == "c3":
+        desc = ("C3: DeepSeek-V3 MLA sizing, 2048 agents x 10 steps, 613,697-page cache, "
+                "aimd h_thresh=0.3")
+    elif workload == "c3off":
+        desc = ("C3 shape, offload tier: 128 agents x 10 steps, scaled cache (peak/1.5), "
+                "uncontrolled admission + offload eviction (PCIe 25 GB/s link model)")
     else:
         desc = "C1 toy: 64 agents x 10 steps, aimd"
     return scen, desc
@@ -143,11 +149,12 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- helpers
 
-def algorithmic_bytes(results) -> dict:
-    """SURVEY.md §8(d) / BASELINE.md §2 per-unit byte counts."""
+def algorithmic_bytes(results, tree: bool = False) -> dict:
+    """SURVEY.md §8(d) / BASELINE.md §2 per-unit byte counts. Offload mode
+    (tree=True): an eviction select reads one 64 B node record per pool entry."""
     look = sum(16 * r.lookups + 8 * r.hit_pages for r in results)
     ins = sum(16 * r.created_pages + 8 * r.refreshed_pages for r in results)
-    ev = sum(8 * r.evict_scanned + 16 * r.evicted_pages for r in results)
+    ev = sum((64 if tree else 8) * r.evict_scanned + 16 * r.evicted_pages for r in results)
     state = sum(192 * r.agent_events for r in results)
     tick = sum(88 * r.ticks for r in results)
     return dict(lookup=look, insert=ins, evict=ev, state=state, tick=tick,
@@ -211,8 +218,8 @@ def run_reference(args):
     scen, desc = build_scenarios(args.workload, 0, args.sims)
     threads = os.cpu_count() or 1
     # bounded sample per step so --steps K --warmup W finishes within minutes
-    every = {"c4": 8, "c2": 1, "c1": 1}[args.workload]
-    for _ in range(args.warmup if args.workload != "c2" else 0):
+    every = {"c4": 8}.get(args.workload, 1)
+    for _ in range(args.warmup if args.workload in ("c4", "c1") else 0):
         cpu_reference(scen, threads, every)
     vals, walls = [], []
     steps = n = 0
@@ -289,7 +296,7 @@ def run_b200(args):
     summary = sweep.gather_records(sweep.records(results), dist, device="cuda")
     makespans = summary[:, 0].cpu().tolist()
     # ---- roofline of the engine kernel
-    ab = algorithmic_bytes(results)
+    ab = algorithmic_bytes(results, tree=args.workload == "c3off")
     kernel_s = (kern_ms / args.steps) / 1e3
     peak, peak_kind = load_peak()
     achieved = ab["total"] / kernel_s / 1e9
@@ -302,21 +309,26 @@ def run_b200(args):
     # ---- end to end through the C ABI with host buffers: every step creates
     # the batch from host populations (H2D), runs it, and the kernel streams
     # results / trace rows / agent stats into pinned host memory (D2H)
+    # the device-resident batch goes back to the workspace cache first, so the
+    # e2e batches reuse its HBM arena (and, after one untimed step, the pinned
+    # host block) like any repeated caller would
+    batch.close()
     e2e_ms = []
+    n_agents = sum(s.population.c.agents for s in specs)
     h2d = sum(p.c.agents * p.c.steps * C.sizeof(abi.StepPlan) for p in pops.values()) + \
         len(specs) * 512
     d2h = 0
-    for _ in range(args.e2e_steps):
+    for k in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         b2 = engine.Batch(specs, device=device, host_outputs=True)
         b2.run()
-        res2 = b2.results_raw()
-        d2h = sum(r.ticks * C.sizeof(abi.TraceRow) for r in res2) + \
-            sum(s.population.c.agents for s in specs) * C.sizeof(abi.AgentStats) + \
-            len(res2) * C.sizeof(abi.SimResult)
+        res2 = b2.results_array()
+        d2h = int(res2["ticks"].sum()) * C.sizeof(abi.TraceRow) + \
+            n_agents * C.sizeof(abi.AgentStats) + len(res2) * C.sizeof(abi.SimResult)
         b2.close()
-        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+        if k > 0:  # step 0 is the untimed warm-up (first pinned allocation)
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -355,7 +367,6 @@ def run_b200(args):
                        "makespan_min": min(makespans), "makespan_max": max(makespans)},
         }
         print(json.dumps(line), flush=True)
-    batch.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()

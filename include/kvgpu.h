@@ -302,6 +302,49 @@ KVG_API kvg_status kvg_classify_phases(const kvg_trace_row* rows, size_t n,
                                        size_t* n_out);
 
 /* ------------------------------------------------------------------ */
+/* Run artifacts (host-side), byte-identical to the reference's         */
+/* execute_run output (experiment.cpp:161-170).                        */
+/* ------------------------------------------------------------------ */
+
+/* Summary (metrics.hpp:85-118), computed by kvg_summarize exactly as
+ * summarize() does (engine.cpp:458-532). */
+typedef struct kvg_summary {
+  char name[128];
+  char policy[64];
+  uint64_t seed, agents;
+  double makespan, throughput;
+  uint64_t decoded_tokens, recompute_tokens, recompute_events, stall_events;
+  double recompute_fraction, mean_hit_rate, mean_usage;
+  kvg_ledger ledger;
+  double device_busy, device_idle, link_busy, link_idle;
+  uint64_t offloaded_tokens, reloaded_tokens, discarded_tokens;
+  double total_wait_time;
+  double warmup_duration, middle_duration, cooldown_duration, middle_fraction;
+  double warmup_hit_rate, middle_hit_rate, cooldown_hit_rate, middle_usage_mean;
+  uint64_t ticks, workload_hash;
+} kvg_summary;
+
+/* policy_name (controller.cpp:253-265). */
+KVG_API kvg_status kvg_policy_name(const kvg_policy* p, char* out, size_t cap);
+KVG_API kvg_status kvg_summarize(const kvg_sim_result* r, const kvg_trace_row* rows,
+                                 size_t n, const char* name,
+                                 const char* policy_label, uint64_t seed,
+                                 uint32_t agents, kvg_summary* out);
+/* export_trace (metrics.cpp:89-101), export_summary (:141-183),
+ * export_phases (:266-276). */
+KVG_API kvg_status kvg_write_trace_csv(const char* path, const kvg_trace_row* rows,
+                                       size_t n);
+KVG_API kvg_status kvg_write_summary(const char* path, const kvg_summary* s);
+KVG_API kvg_status kvg_write_phases_csv(const char* path, const kvg_phase_label* p,
+                                        size_t n);
+/* trace.csv + summary.txt + phases.csv of one run into an existing `dir`. */
+KVG_API kvg_status kvg_write_run_artifacts(const char* dir, const char* name,
+                                           const char* policy_label, uint64_t seed,
+                                           uint32_t agents, const kvg_sim_result* r,
+                                           const kvg_trace_row* rows, size_t n,
+                                           kvg_summary* out);
+
+/* ------------------------------------------------------------------ */
 /* Cache-policy seam: a device-resident paged prefix cache driven by a */
 /* batch of CacheTree-style operations (cache_tree.hpp:96-167).        */
 /* Sequences are owner-form: (agent, length) names the token sequence  */

@@ -14,6 +14,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <functional>
@@ -399,6 +400,33 @@ KVR_API int kvr_run_many(size_t n, const kvg_workload_config* wls,
     if (wall_s) *wall_s = std::chrono::duration<double>(t1 - t0).count();
     for (auto& e : errs)
       if (e) std::rethrow_exception(e);
+  });
+}
+
+/* ---------------- run artifacts through the reference's own writers ------- */
+
+/* execute_run's finalize (experiment.cpp:161-170) on a reference run:
+ * summarize + export_trace / export_summary / export_phases into `dir`. */
+KVR_API int kvr_run_artifacts(const kvg_workload_config* wl, uint64_t seed,
+                              const kvg_policy* policy, const kvg_cost_params* cost,
+                              const kvg_engine_params* engine, const char* name,
+                              const char* policy_label, const char* dir) {
+  return guarded([&] {
+    kvadmit::Population pop = kvadmit::build_population(to_workload(*wl), seed);
+    kvadmit::SimulationResult partial, result;
+    const kvadmit::Policy pol = to_policy(*policy);
+    try {
+      result = kvadmit::run_simulation(std::move(pop), pol, to_cost(*cost), to_engine(*engine),
+                                       &partial);
+    } catch (const kvadmit::HorizonError&) {
+      result = std::move(partial);
+    }
+    kvadmit::Summary s = kvadmit::summarize(result, name, pol, seed, wl->agents);
+    s.policy = policy_label;
+    const std::string d(dir);
+    kvadmit::export_trace(result.trace, d + "/trace.csv");
+    kvadmit::export_summary(s, d + "/summary.txt");
+    kvadmit::export_phases(result.phases, d + "/phases.csv");
   });
 }
 

@@ -129,6 +129,20 @@ class BatchOptions(C.Structure):
                 ("trace_capacity", u64), ("host_outputs", u32), ("_pad", u32)]
 
 
+class Summary(C.Structure):  # kvg_summary (metrics.hpp:85-118)
+    _fields_ = [("name", C.c_char * 128), ("policy", C.c_char * 64), ("seed", u64),
+                ("agents", u64), ("makespan", f64), ("throughput", f64),
+                ("decoded_tokens", u64), ("recompute_tokens", u64), ("recompute_events", u64),
+                ("stall_events", u64), ("recompute_fraction", f64), ("mean_hit_rate", f64),
+                ("mean_usage", f64), ("ledger", Ledger), ("device_busy", f64),
+                ("device_idle", f64), ("link_busy", f64), ("link_idle", f64),
+                ("offloaded_tokens", u64), ("reloaded_tokens", u64), ("discarded_tokens", u64),
+                ("total_wait_time", f64), ("warmup_duration", f64), ("middle_duration", f64),
+                ("cooldown_duration", f64), ("middle_fraction", f64), ("warmup_hit_rate", f64),
+                ("middle_hit_rate", f64), ("cooldown_hit_rate", f64),
+                ("middle_usage_mean", f64), ("ticks", u64), ("workload_hash", u64)]
+
+
 class CacheOp(C.Structure):
     _fields_ = [("kind", u32), ("agent", u32), ("len", u64), ("arg", u64), ("arg2", u64)]
 

@@ -55,6 +55,7 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
         "engine.o": (os.path.join(CSRC, "engine.cu"), "nvcc"),
         "capi.o": (os.path.join(CSRC, "capi.cu"), "nvcc"),
         "host.o": (os.path.join(CSRC, "host.cpp"), "cxx"),
+        "artifacts.o": (os.path.join(CSRC, "artifacts.cpp"), "cxx"),
     }
     logs: list[str] = []
     objs = []

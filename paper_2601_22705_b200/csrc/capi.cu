@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <unordered_map>
 #include <cstdint>
 #include <cstring>
 #include <string>

@@ -73,6 +73,12 @@ def lib():
     L.kvg_classify_phases.argtypes = [P(abi.TraceRow), C.c_size_t, C.c_double,
                                       P(abi.PhaseParams), P(abi.PhaseLabel), C.c_size_t,
                                       P(C.c_size_t)]
+    L.kvg_policy_name.argtypes = [P(abi.Policy), C.c_char_p, C.c_size_t]
+    L.kvg_summarize.argtypes = [P(abi.SimResult), P(abi.TraceRow), C.c_size_t, C.c_char_p,
+                                C.c_char_p, C.c_uint64, C.c_uint32, P(abi.Summary)]
+    L.kvg_write_run_artifacts.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint64,
+                                          C.c_uint32, P(abi.SimResult), P(abi.TraceRow),
+                                          C.c_size_t, P(abi.Summary)]
     L.kvg_cache_create.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64,
                                    C.c_uint32, C.c_uint32, P(C.c_void_p)]
     L.kvg_cache_exec.argtypes = [C.c_void_p, P(abi.CacheOp), C.c_size_t, P(abi.CacheOpResult)]
@@ -134,6 +140,16 @@ class SimSpec:
     cost: abi.CostParams
     engine: abi.EngineParams
 
+    @property
+    def desc(self) -> abi.SimDesc:
+        """The C descriptor of this simulation (built once, cached)."""
+        d = self.__dict__.get("_desc")
+        if d is None:
+            d = abi.SimDesc(population=C.pointer(self.population.c), policy=self.policy,
+                            cost=self.cost, engine=self.engine)
+            self.__dict__["_desc"] = d
+        return d
+
     @staticmethod
     def from_scenario(s: Scenario, policy_text: str | None = None,
                       population: Population | None = None) -> "SimSpec":
@@ -148,10 +164,10 @@ class Batch:
     def __init__(self, specs: list[SimSpec], device: int = 0, warps_per_sim: int = 0,
                  log_capacity: int = 0, trace_capacity: int = 0, host_outputs: bool = False):
         self.specs = specs
-        self.descs = (abi.SimDesc * max(1, len(specs)))()
-        for i, sp in enumerate(specs):
-            self.descs[i] = abi.SimDesc(population=C.pointer(sp.population.c), policy=sp.policy,
-                                        cost=sp.cost, engine=sp.engine)
+        if specs:
+            self.descs = (abi.SimDesc * len(specs))(*[sp.desc for sp in specs])
+        else:
+            self.descs = (abi.SimDesc * 1)()
         opt = abi.BatchOptions(warps_per_sim=warps_per_sim, log_capacity=log_capacity,
                                trace_capacity=trace_capacity, host_outputs=int(host_outputs))
         h = C.c_void_p()
@@ -183,6 +199,13 @@ class Batch:
         _check(lib().kvg_batch_results(self.h, arr, self.n))
         return list(arr)[: self.n]
 
+    def results_array(self) -> np.ndarray:
+        """Every simulation's result as one numpy structured array (no
+        per-simulation Python objects)."""
+        arr = (abi.SimResult * max(1, self.n))()
+        _check(lib().kvg_batch_results(self.h, arr, self.n))
+        return np.ctypeslib.as_array(arr)[: self.n]
+
     def trace(self, i: int) -> list[dict]:
         n = C.c_size_t()
         _check(lib().kvg_batch_trace(self.h, i, None, 0, C.byref(n)))
@@ -210,6 +233,25 @@ class Batch:
         recs = (abi.LogRecord * max(1, n.value))()
         _check(lib().kvg_batch_log(self.h, i, recs, n.value, C.byref(n)))
         return [(r.kind, r.agent, r.clock, r.a, r.b) for r in recs[: n.value]]
+
+    def write_artifacts(self, i: int, out_dir: str, name: str, policy_label: str,
+                        seed: int) -> dict:
+        """trace.csv, summary.txt and phases.csv of simulation i in `out_dir`,
+        byte-identical to the reference's execute_run (experiment.cpp:161-170).
+        Returns the Summary."""
+        os.makedirs(out_dir, exist_ok=True)
+        r = abi.SimResult()
+        _check(lib().kvg_batch_result(self.h, i, C.byref(r)))
+        n = C.c_size_t()
+        _check(lib().kvg_batch_trace(self.h, i, None, 0, C.byref(n)))
+        rows = (abi.TraceRow * max(1, n.value))()
+        _check(lib().kvg_batch_trace(self.h, i, rows, n.value, C.byref(n)))
+        s = abi.Summary()
+        _check(lib().kvg_write_run_artifacts(out_dir.encode(), name.encode(),
+                                             policy_label.encode(), seed,
+                                             self.specs[i].population.c.agents, C.byref(r),
+                                             rows, n.value, C.byref(s)))
+        return abi.struct_to_dict(s)
 
     def close(self):
         if getattr(self, "h", None):

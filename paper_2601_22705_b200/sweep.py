@@ -22,6 +22,18 @@ def weak_shard(workload: str, rank: int, sims: int):
         s = config.c2_qwen("aimd")
         s.seed = 7 + rank
         return [s]
+    if workload == "c3":  # DeepSeek-V3 MLA sizing, the controlled AIMD row (h_thresh 0.3)
+        s = config.c3_dsv3("aimd")
+        s.controller.h_thresh = 0.3
+        s.seed = 3 + rank
+        return [s]
+    if workload == "c3off":  # offload tier: the 128-agent C3 shape (full size exceeds the horizon)
+        s = config.c3_dsv3("offload", agents=128, capacity=1)
+        from . import engine
+        s.engine.capacity = config.scaled_capacity(
+            engine.Population(s.workload, s.seed).peak_aggregate_tokens)
+        s.seed = 3 + rank
+        return [s]
     s = config.c1_toy("aimd")
     s.seed = 42 + rank
     return [s]

@@ -24,6 +24,9 @@ _orc = None
 def ref_lib():
     global _ref
     if _ref is None:
+        # RTLD_GLOBAL: the reference's iostream writers (export_trace & co.)
+        # crash when libstdc++ arrives only as a dependency of a local library
+        C.CDLL("libstdc++.so.6", mode=C.RTLD_GLOBAL)
         lib = C.CDLL(REF_SO)
         P = C.POINTER
         lib.kvr_last_error.restype = C.c_char_p
@@ -38,6 +41,9 @@ def ref_lib():
         lib.kvr_run_many.argtypes = [C.c_size_t, P(abi.WorkloadConfig), P(C.c_uint64),
                                      P(abi.Policy), P(abi.CostParams), P(abi.EngineParams),
                                      C.c_uint, P(C.c_double), P(C.c_uint64), P(C.c_double)]
+        lib.kvr_run_artifacts.argtypes = [P(abi.WorkloadConfig), C.c_uint64, P(abi.Policy),
+                                          P(abi.CostParams), P(abi.EngineParams), C.c_char_p,
+                                          C.c_char_p, C.c_char_p]
         lib.kvr_cache_new.restype = C.c_void_p
         lib.kvr_cache_new.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32]
         lib.kvr_cache_free.argtypes = [C.c_void_p]
@@ -165,10 +171,23 @@ def oracle_run(s: Scenario, policy_text: str | None = None, digests: bool = Fals
     return dict(status=rc, result=abi.struct_to_dict(res), trace=_rows(trace, nt.value),
                 agents=_rows(agents, s.workload.agents),
                 digests=np.ctypeslib.as_array(dig)[:nd.value].copy() if digests else None,
-                log=[(r.kind, r.agent, r.clock, r.a, r.b) for r in lg[:nl.value]] if log else None)
+                log=[(r.kind, r.agent, r.clock, r.a, r.b) for r in lg[:nl.value]] if log else None,
+                raw_result=res, raw_trace=trace, n_trace=nt.value)
 
 
 def load_presets() -> dict:
     import json
     with open(os.path.join(GOLDEN, "scenarios.json")) as fh:
         return json.load(fh)
+
+
+def ref_artifacts(s: Scenario, policy_text: str | None, out_dir: str, label: str):
+    """The reference's own trace.csv / summary.txt / phases.csv for one run
+    (execute_run's finalize through the unmodified metrics.cpp writers)."""
+    lib = ref_lib()
+    os.makedirs(out_dir, exist_ok=True)
+    pol, eng = s.resolved(policy_text)
+    wl, cost, ep = s.workload.to_abi(), s.cost.to_abi(), eng.to_abi()
+    rc = lib.kvr_run_artifacts(C.byref(wl), s.seed, C.byref(pol), C.byref(cost), C.byref(ep),
+                               s.name.encode(), label.encode(), out_dir.encode())
+    assert rc == 0, lib.kvr_last_error()
