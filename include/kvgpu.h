@@ -345,6 +345,61 @@ KVG_API kvg_status kvg_write_run_artifacts(const char* dir, const char* name,
                                            kvg_summary* out);
 
 /* ------------------------------------------------------------------ */
+/* Device-backed admission controllers: the reference's standalone     */
+/* controller ABI (kvadmit.h:86-159) for N controllers at once, state   */
+/* in HBM, each call one kernel over all of them.                       */
+/* ------------------------------------------------------------------ */
+
+enum { KVG_CMD_ADMIT = 0, KVG_CMD_PAUSE = 1, KVG_CMD_RESUME = 2 };
+/* kva_command (kvadmit.h:123-126), same layout. */
+typedef struct kvg_command {
+  uint8_t kind; /* KVG_CMD_* */
+  uint8_t _pad[3];
+  uint32_t agent;
+} kvg_command;
+
+enum {
+  KVG_CTL_ADD_PENDING = 0,      /* kva_controller_add_pending        */
+  KVG_CTL_AGENT_FINISHED = 1,   /* kva_controller_on_agent_finished  */
+  KVG_CTL_REQUEST_COMPLETE = 2, /* kva_controller_on_request_complete */
+  KVG_CTL_TOOL_RETURN = 3       /* kva_controller_on_tool_return     */
+};
+typedef struct kvg_ctl_event {
+  uint32_t controller, kind, agent, _pad;
+} kvg_ctl_event;
+
+typedef struct kvg_controllers kvg_controllers;
+/* n controllers; controller i admits agents 0..total_agents[i]-1 under
+ * policies[i] (validated like Policy::validate, controller.cpp:24-52). */
+KVG_API kvg_status kvg_controllers_create(int device, size_t n, const kvg_policy* policies,
+                                          const uint32_t* total_agents,
+                                          kvg_controllers** out);
+KVG_API void kvg_controllers_free(kvg_controllers* c);
+/* update_window on every controller (usage[i], hit_rate[i]); window_out[i]
+ * receives the post-update window as kva_controller_update_window reports
+ * it (the display window). */
+KVG_API kvg_status kvg_controllers_update_window(kvg_controllers* c, const double* usage,
+                                                 const double* hit_rate, double* window_out);
+/* One admission pass on every controller. at_boundary and commands are
+ * concatenated per controller (controller i's slice starts at the sum of
+ * total_agents[0..i) and is total_agents[i] long); n_out[i] = commands
+ * controller i emitted. */
+KVG_API kvg_status kvg_controllers_admission_pass(kvg_controllers* c,
+                                                  const uint8_t* at_boundary,
+                                                  kvg_command* commands, size_t* n_out);
+/* Applies events in submission order per controller; status[i] (optional)
+ * is the kvg_status of event i (KVG_ERR_STATE for an unknown agent, like
+ * UnknownAgent). */
+KVG_API kvg_status kvg_controllers_apply(kvg_controllers* c, const kvg_ctl_event* events,
+                                         size_t n_events, int32_t* status);
+/* Per-controller state; any out-pointer may be NULL. */
+KVG_API kvg_status kvg_controllers_state(const kvg_controllers* c, double* window,
+                                         double* display_window, uint64_t* ticks,
+                                         size_t* active, size_t* pending, size_t* paused);
+KVG_API kvg_status kvg_controllers_active(const kvg_controllers* c, size_t i, uint32_t* out,
+                                          size_t cap, size_t* n_out);
+
+/* ------------------------------------------------------------------ */
 /* Cache-policy seam: a device-resident paged prefix cache driven by a */
 /* batch of CacheTree-style operations (cache_tree.hpp:96-167).        */
 /* Sequences are owner-form: (agent, length) names the token sequence  */

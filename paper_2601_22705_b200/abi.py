@@ -143,6 +143,18 @@ class Summary(C.Structure):  # kvg_summary (metrics.hpp:85-118)
                 ("middle_usage_mean", f64), ("ticks", u64), ("workload_hash", u64)]
 
 
+class Command(C.Structure):  # kvg_command == kva_command (kvadmit.h:123-126)
+    _fields_ = [("kind", C.c_uint8), ("_pad", C.c_uint8 * 3), ("agent", u32)]
+
+
+class CtlEvent(C.Structure):  # kvg_ctl_event
+    _fields_ = [("controller", u32), ("kind", u32), ("agent", u32), ("_pad", u32)]
+
+
+CMD_ADMIT, CMD_PAUSE, CMD_RESUME = 0, 1, 2
+CTL_ADD_PENDING, CTL_AGENT_FINISHED, CTL_REQUEST_COMPLETE, CTL_TOOL_RETURN = 0, 1, 2, 3
+
+
 class CacheOp(C.Structure):
     _fields_ = [("kind", u32), ("agent", u32), ("len", u64), ("arg", u64), ("arg2", u64)]
 

@@ -54,6 +54,7 @@ def build_native(force: bool = False, verbose: bool = False) -> str:
     srcs = {
         "engine.o": (os.path.join(CSRC, "engine.cu"), "nvcc"),
         "capi.o": (os.path.join(CSRC, "capi.cu"), "nvcc"),
+        "controllers.o": (os.path.join(CSRC, "controllers.cu"), "nvcc"),
         "host.o": (os.path.join(CSRC, "host.cpp"), "cxx"),
         "artifacts.o": (os.path.join(CSRC, "artifacts.cpp"), "cxx"),
     }

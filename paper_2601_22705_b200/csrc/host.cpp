@@ -90,20 +90,8 @@ bool dist_ok(const kvg_distribution& d, const char* what, std::string* why) {
 
 }  // namespace
 
-bool validate_sim(const kvg_sim_desc& d, std::string* why) {
-  const kvg_engine_params& e = d.engine;
-  if (d.population == nullptr) { *why = "null population"; return false; }
-  if (d.population->agents > 0 && d.population->plans == nullptr) { *why = "population has no plans"; return false; }
-  if (d.population->steps < 1) { *why = "workload.steps must be >= 1"; return false; }
-  if (e.capacity == 0) { *why = "cache.capacity must be positive"; return false; }
-  if (e.page_size == 0) { *why = "cache.page_size must be positive"; return false; }
-  if (!(e.hit_window_decay >= 0 && e.hit_window_decay < 1)) { *why = "cache.hit_window_decay must be in [0,1)"; return false; }
-  if (!(e.horizon > 0)) { *why = "horizon must be positive"; return false; }
-  if (!(e.phases.sat_threshold > 0 && e.phases.sat_threshold <= 1)) { *why = "phases.sat_threshold must be in (0,1]"; return false; }
-  if (!(e.phases.hit_threshold >= 0 && e.phases.hit_threshold <= 1)) { *why = "phases.hit_threshold must be in [0,1]"; return false; }
-  if (e.phases.hysteresis < 1) { *why = "phases.hysteresis must be >= 1"; return false; }
-  if (e.eviction != KVG_EVICT_DISCARD && e.eviction != KVG_EVICT_OFFLOAD) { *why = "unknown eviction mode"; return false; }
-  const kvg_policy& p = d.policy;
+/* Policy::validate + ControllerConfig::validate (controller.cpp:24-52). */
+bool validate_policy(const kvg_policy& p, std::string* why) {
   if (p.kind > KVG_POLICY_AIMD) { *why = "unknown policy"; return false; }
   if ((p.kind == KVG_POLICY_REQUEST_CAP || p.kind == KVG_POLICY_AGENT_CAP) && p.cap < 1) { *why = "fixed cap policies need cap >= 1"; return false; }
   if (p.kind == KVG_POLICY_AIMD) {
@@ -118,6 +106,24 @@ bool validate_sim(const kvg_sim_desc& d, std::string* why) {
     if (!(c.control_interval > 0)) { *why = "controller.control_interval must be > 0"; return false; }
     if (!(c.signal_smoothing >= 0 && c.signal_smoothing < 1)) { *why = "controller.signal_smoothing must be in [0,1)"; return false; }
   }
+  return true;
+}
+
+bool validate_sim(const kvg_sim_desc& d, std::string* why) {
+  const kvg_engine_params& e = d.engine;
+  if (d.population == nullptr) { *why = "null population"; return false; }
+  if (d.population->agents > 0 && d.population->plans == nullptr) { *why = "population has no plans"; return false; }
+  if (d.population->steps < 1) { *why = "workload.steps must be >= 1"; return false; }
+  if (e.capacity == 0) { *why = "cache.capacity must be positive"; return false; }
+  if (e.page_size == 0) { *why = "cache.page_size must be positive"; return false; }
+  if (!(e.hit_window_decay >= 0 && e.hit_window_decay < 1)) { *why = "cache.hit_window_decay must be in [0,1)"; return false; }
+  if (!(e.horizon > 0)) { *why = "horizon must be positive"; return false; }
+  if (!(e.phases.sat_threshold > 0 && e.phases.sat_threshold <= 1)) { *why = "phases.sat_threshold must be in (0,1]"; return false; }
+  if (!(e.phases.hit_threshold >= 0 && e.phases.hit_threshold <= 1)) { *why = "phases.hit_threshold must be in [0,1]"; return false; }
+  if (e.phases.hysteresis < 1) { *why = "phases.hysteresis must be >= 1"; return false; }
+  if (e.eviction != KVG_EVICT_DISCARD && e.eviction != KVG_EVICT_OFFLOAD) { *why = "unknown eviction mode"; return false; }
+  const kvg_policy& p = d.policy;
+  if (!validate_policy(p, why)) return false;
   const kvg_cost_params& c = d.cost;
   if (c.prefill_linear < 0 || c.prefill_quadratic < 0 || c.decode_base < 0 || c.decode_context < 0 ||
       c.bytes_per_token < 0 || c.transfer_sync_overhead < 0) { *why = "cost parameters must be non-negative"; return false; }

@@ -79,6 +79,20 @@ def lib():
     L.kvg_write_run_artifacts.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_uint64,
                                           C.c_uint32, P(abi.SimResult), P(abi.TraceRow),
                                           C.c_size_t, P(abi.Summary)]
+    L.kvg_controllers_create.argtypes = [C.c_int, C.c_size_t, P(abi.Policy), P(C.c_uint32),
+                                         P(C.c_void_p)]
+    L.kvg_controllers_free.argtypes = [C.c_void_p]
+    L.kvg_controllers_free.restype = None
+    L.kvg_controllers_update_window.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double),
+                                                P(C.c_double)]
+    L.kvg_controllers_admission_pass.argtypes = [C.c_void_p, P(C.c_uint8), P(abi.Command),
+                                                 P(C.c_size_t)]
+    L.kvg_controllers_apply.argtypes = [C.c_void_p, P(abi.CtlEvent), C.c_size_t, P(C.c_int32)]
+    L.kvg_controllers_state.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double),
+                                        P(C.c_uint64), P(C.c_size_t), P(C.c_size_t),
+                                        P(C.c_size_t)]
+    L.kvg_controllers_active.argtypes = [C.c_void_p, C.c_size_t, P(C.c_uint32), C.c_size_t,
+                                         P(C.c_size_t)]
     L.kvg_cache_create.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64,
                                    C.c_uint32, C.c_uint32, P(C.c_void_p)]
     L.kvg_cache_exec.argtypes = [C.c_void_p, P(abi.CacheOp), C.c_size_t, P(abi.CacheOpResult)]
@@ -319,6 +333,75 @@ class DeviceCache:
     def close(self):
         if getattr(self, "h", None):
             lib().kvg_cache_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DeviceControllers:
+    """N admission controllers with their state in HBM: the reference's
+    standalone controller ABI (kvadmit.h:86-159) batched, one kernel per call
+    over all controllers (csrc/controllers.cu)."""
+
+    def __init__(self, policies: list, total_agents: list[int], device: int = 0):
+        n = len(policies)
+        self.n = n
+        self.total = list(total_agents)
+        self.off = [0]
+        for t in self.total:
+            self.off.append(self.off[-1] + t)
+        pol = (abi.Policy * max(1, n))(*policies)
+        tot = (C.c_uint32 * max(1, n))(*self.total)
+        h = C.c_void_p()
+        _check(lib().kvg_controllers_create(device, n, pol, tot, C.byref(h)))
+        self.h = h
+
+    def update_window(self, usage: list[float], hit: list[float]) -> list[float]:
+        u = (C.c_double * max(1, self.n))(*usage)
+        r = (C.c_double * max(1, self.n))(*hit)
+        w = (C.c_double * max(1, self.n))()
+        _check(lib().kvg_controllers_update_window(self.h, u, r, w))
+        return list(w)[: self.n]
+
+    def admission_pass(self, at_boundary: list[list[bool]]) -> list[list[tuple[int, int]]]:
+        flat = [int(b) for row in at_boundary for b in row]
+        bnd = (C.c_uint8 * max(1, len(flat)))(*flat)
+        cmds = (abi.Command * max(1, self.off[-1]))()
+        nout = (C.c_size_t * max(1, self.n))()
+        _check(lib().kvg_controllers_admission_pass(self.h, bnd, cmds, nout))
+        return [[(cmds[self.off[i] + k].kind, cmds[self.off[i] + k].agent)
+                 for k in range(nout[i])] for i in range(self.n)]
+
+    def apply(self, events: list[tuple[int, int, int]]) -> list[int]:
+        """events: (controller, kind, agent); returns per-event statuses."""
+        ev = (abi.CtlEvent * max(1, len(events)))(
+            *[abi.CtlEvent(controller=c, kind=k, agent=a) for c, k, a in events])
+        st = (C.c_int32 * max(1, len(events)))()
+        lib().kvg_controllers_apply(self.h, ev, len(events), st)
+        return list(st)[: len(events)]
+
+    def state(self) -> list[dict]:
+        n = max(1, self.n)
+        w, dw = (C.c_double * n)(), (C.c_double * n)()
+        t = (C.c_uint64 * n)()
+        a, p, q = (C.c_size_t * n)(), (C.c_size_t * n)(), (C.c_size_t * n)()
+        _check(lib().kvg_controllers_state(self.h, w, dw, t, a, p, q))
+        return [dict(window=w[i], display_window=dw[i], ticks=t[i], active=a[i], pending=p[i],
+                     paused=q[i]) for i in range(self.n)]
+
+    def active(self, i: int) -> list[int]:
+        out = (C.c_uint32 * max(1, self.total[i]))()
+        n = C.c_size_t()
+        _check(lib().kvg_controllers_active(self.h, i, out, self.total[i], C.byref(n)))
+        return list(out)[: n.value]
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().kvg_controllers_free(self.h)
             self.h = None
 
     def __del__(self):
