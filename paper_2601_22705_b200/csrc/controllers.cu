@@ -33,10 +33,13 @@ struct CtlDev {
   double window, su, sh;
   u64 ticks;
   u32 total, act_n, pend_head, pend_n, paus_head, paus_n;
+  u32 cap;  // list capacity: the reference's vector / deques are unbounded and
+            // misuse (re-queueing an admitted agent) can hold an id twice, so
+            // lists get max(4 x total, total + 256) slots; overflow = KVG_ERR_STATE
   int have_s, err;
-  u32* active;  // [total] insertion-ordered
-  u32* pend;    // [total] FIFO ring
-  u32* paus;    // [total] FIFO ring
+  u32* active;  // [cap] insertion-ordered
+  u32* pend;    // [cap] FIFO ring
+  u32* paus;    // [cap] FIFO ring
 };
 
 constexpr unsigned FULLM = 0xffffffffu;
@@ -101,12 +104,13 @@ __global__ void k_admission(CtlDev* cs, u32 n, const uint8_t* at_boundary, const
   u32* const active = c.active;
   u32 act = c.act_n, paus_n = c.paus_n, paus_head = c.paus_head;
   u32 pend_n = c.pend_n, pend_head = c.pend_head;
-  const u32 total = c.total;
+  const u32 total = c.cap;
   u64 k = 0;
+  const u64 kcap = agent_off[ci + 1] - agent_off[ci];  // commands buffer: total_agents
   const u64 limit = admission_limit(c);
   const bool gated = c.policy.kind == KVG_POLICY_AGENT_CAP || c.policy.kind == KVG_POLICY_AIMD;
   if (gated) {
-    while (act > limit) {
+    while (act > limit && k < kcap) {
       // newest active agent at a step boundary: reverse scan, 32 at a time
       long long victim = -1;
       for (long long base = static_cast<long long>(act) - 1; base >= 0 && victim < 0;
@@ -139,6 +143,10 @@ __global__ void k_admission(CtlDev* cs, u32 n, const uint8_t* at_boundary, const
   }
   if (lane == 0) {
     while (act < limit) {
+      if (k >= kcap) {  // more commands than agents: only after API misuse
+        c.err = KVG_ERR_STATE;
+        break;
+      }
       u32 id;
       uint8_t kind;
       if (gated && paus_n > 0) {
@@ -154,7 +162,7 @@ __global__ void k_admission(CtlDev* cs, u32 n, const uint8_t* at_boundary, const
       } else {
         break;
       }
-      if (act >= total) {  // an agent would be active twice: API misuse
+      if (act >= total) {  // list full (API misuse re-queued ids)
         c.err = KVG_ERR_STATE;
         break;
       }
@@ -181,8 +189,8 @@ __device__ bool erase_active(CtlDev& c, u32 id) {
 }
 
 __device__ bool add_pending(CtlDev& c, u32 id) {
-  if (c.pend_n >= c.total) return false;
-  c.pend[ring(c.pend_head, c.pend_n, c.total)] = id;
+  if (c.pend_n >= c.cap) return false;
+  c.pend[ring(c.pend_head, c.pend_n, c.cap)] = id;
   ++c.pend_n;
   return true;
 }
@@ -237,6 +245,7 @@ struct kvg_controllers {
   kvg::u32* lists = nullptr;
   kvg::u64* agent_off = nullptr;  // device [n+1]
   std::vector<kvg::u64> h_off;    // host copy
+  std::vector<kvg::u64> l_off;    // list offsets (capacity per controller)
   std::vector<kvg::u32> total;
 };
 
@@ -267,8 +276,13 @@ KVG_API kvg_status kvg_controllers_create(int device, size_t n, const kvg_policy
   h->n = n;
   h->h_off.assign(n + 1, 0);
   h->total.assign(total_agents, total_agents + n);
-  for (size_t i = 0; i < n; ++i) h->h_off[i + 1] = h->h_off[i] + total_agents[i];
-  const kvg::u64 slots = h->h_off[n];
+  h->l_off.assign(n + 1, 0);
+  auto list_cap = [](kvg::u32 t) { return std::max<kvg::u64>(4ull * t, t + 256ull); };
+  for (size_t i = 0; i < n; ++i) {
+    h->h_off[i + 1] = h->h_off[i] + total_agents[i];
+    h->l_off[i + 1] = h->l_off[i] + list_cap(total_agents[i]);
+  }
+  const kvg::u64 slots = h->l_off[n];
   std::vector<kvg::CtlDev> hs(n);
   cudaError_t e = cudaMalloc(&h->d, std::max<size_t>(1, n) * sizeof(kvg::CtlDev));
   if (e == cudaSuccess) e = cudaMalloc(&h->lists, std::max<kvg::u64>(1, 3 * slots) * 4);
@@ -289,9 +303,10 @@ KVG_API kvg_status kvg_controllers_create(int device, size_t n, const kvg_policy
       if (cfg.initial_window == 0) cfg.initial_window = cfg.w_min;
       c.window = cfg.initial_window;
     }
-    c.active = h->lists + h->h_off[i];
-    c.pend = h->lists + slots + h->h_off[i];
-    c.paus = h->lists + 2 * slots + h->h_off[i];
+    c.cap = static_cast<kvg::u32>(list_cap(c.total));
+    c.active = h->lists + h->l_off[i];
+    c.pend = h->lists + slots + h->l_off[i];
+    c.paus = h->lists + 2 * slots + h->l_off[i];
   }
   if (n) {
     e = cudaMemcpy(h->d, hs.data(), n * sizeof(kvg::CtlDev), cudaMemcpyHostToDevice);

@@ -778,3 +778,13 @@ __global__ void __launch_bounds__(256) pack_traces(const SimDev* __restrict__ si
 }
 
 }  // namespace kvg
+
+#ifdef KVG_PROFILE
+// dev-only: read and clear the phase profile (tools/probe_phases.py)
+extern "C" __attribute__((visibility("default"))) int kvg_debug_profile(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, kvg::g_prof, sizeof(kvg::g_prof));
+  static const unsigned long long zero[48] = {0};
+  cudaMemcpyToSymbol(kvg::g_prof, zero, sizeof(zero));
+  return 0;
+}
+#endif

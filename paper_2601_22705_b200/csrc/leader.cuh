@@ -96,7 +96,27 @@ struct Lead {
   u64 t_next_ord, offloaded, reloaded;
   double pcie_busy, link_busy;
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
+#ifdef KVG_PROFILE
+  // dev-only phase profile (tools/probe_phases.py): cycles per leader phase,
+  // per cooperative op kind, in fast_housekeeping
+  u64 prof[48];
+  long long prof_t;
+  int prof_ph;
+#endif
 };
+
+#ifdef KVG_PROFILE
+__device__ unsigned long long g_prof[48];
+__device__ __forceinline__ void prof_mark(Lead& L, int next_slot) {
+  const long long t = clock64();
+  L.prof[L.prof_ph] += static_cast<u64>(t - L.prof_t);
+  L.prof_t = t;
+  L.prof_ph = next_slot;
+}
+#define PROF_MARK(L, slot) prof_mark(L, slot)
+#else
+#define PROF_MARK(L, slot) ((void)0)
+#endif
 
 // ------------------------------------------------------------------ helpers
 
@@ -949,10 +969,13 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
   for (;;) {
     if (L.status == KVG_ERR_STATE && L.phase != PH_DONE && L.phase != PH_EXITED)
       L.phase = PH_DONE;
+    PROF_MARK(L, L.phase);
     switch (L.phase) {
       // ------------------------------------------------ event loop (98-136)
       case PH_EVENT: {
+        PROF_MARK(L, 40);
         fast_housekeeping(D, L);
+        PROF_MARK(L, PH_EVENT);
         int which = -1;  // 0 agent, 1 tick, 2 admission (the event ranks)
         double bt = 0;
         if (L.hsize > 0) {
@@ -1399,13 +1422,28 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   __syncthreads();
   if (tid == 0) lead_init(D, L, op);
   __syncthreads();
+#ifdef KVG_PROFILE
+  if (tid == 0) {
+    for (int i = 0; i < 48; ++i) L.prof[i] = 0;
+    L.prof_t = clock64();
+    L.prof_ph = 47;
+  }
+#endif
   for (;;) {
     if (tid == 0) leader_step(D, L, op);
     __syncthreads();
     if (op.kind == OP_EXIT) break;
+    if (tid == 0) PROF_MARK(L, 32 + op.kind);
     run_op<kDepth>(op, h, tid, warp, lane, nw);
     __syncthreads();
+    if (tid == 0) PROF_MARK(L, 46);
   }
+#ifdef KVG_PROFILE
+  if (tid == 0) {
+    PROF_MARK(L, 47);
+    for (int i = 0; i < 48; ++i) atomicAdd(&g_prof[i], L.prof[i]);
+  }
+#endif
 }
 
 // Throughput variant: one warp per simulation, register budget (72) sized so 28

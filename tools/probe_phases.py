@@ -1,0 +1,35 @@
+"""Dev probe: where a C4 launch spends its cycles (needs a -DKVG_PROFILE build:
+KVG_LIB=var_libs/libkvgpu_prof.so python tools/probe_phases.py)."""
+import ctypes as C
+import sys
+
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+from paper_2601_22705_b200 import config, engine  # noqa: E402
+
+PH = ["EVENT", "MEMBER", "M_MATCHED", "M_INSERT", "M_EVICTED", "M_COMMIT", "M_CREATED", "M_FAIL",
+      "M_RESTORED", "BATCH_END", "GEN_DISCARDED", "O_MEMBER", "O_RELOAD_CHUNK",
+      "O_RELOAD_EVICTED", "O_RELOAD_END", "O_INSERT_START", "O_INSERT_COUNT",
+      "O_INSERT_EVICTED", "O_INSERT_FAIL", "O_EVICT_POP", "DONE", "EXITED"]
+names = {i: "leader:" + n for i, n in enumerate(PH)}
+names.update({32 + k: "coop:" + n for k, n in enumerate(
+    ["NONE", "EXIT", "RANGE", "EVICT", "REBUILD", "SCANFREE", "FRONTIER"])})
+names.update({40: "fast_housekeeping", 46: "leader_step entry+sync", 47: "init/finalize"})
+which = sys.argv[1] if len(sys.argv) > 1 else "c4"
+if which == "c4":
+    pop = engine.Population(config.c1_toy().workload, 42)
+    specs = [engine.SimSpec.from_scenario(s, population=pop) for s in config.c4_sweep()]
+else:
+    specs = [engine.SimSpec.from_scenario(config.c2_qwen("aimd"))]
+lib = engine.lib()
+lib.kvg_debug_profile.argtypes = [C.POINTER(C.c_ulonglong)]
+b = engine.Batch(specs)
+b.run()
+buf = (C.c_ulonglong * 48)()
+lib.kvg_debug_profile(buf)  # clear (first run)
+b.run()
+lib.kvg_debug_profile(buf)
+tot = sum(buf)
+print(which, "kernel ms", b.timing()[1], "total sim-cycles", tot)
+for i in sorted(range(48), key=lambda i: -buf[i]):
+    if buf[i]:
+        print(f"{100 * buf[i] / tot:6.2f}%  {names.get(i, i)}")
