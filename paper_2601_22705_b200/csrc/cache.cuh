@@ -239,3 +239,155 @@ __global__ void __launch_bounds__(1024) cache_kernel(const CacheDev* __restrict_
 }
 
 }  // namespace kvg
+
+// ==========================================================================
+// Offload-mode CacheTree seam: the same node-level tree the engine runs
+// (tree.cuh), driven op by op. Leader-serial (one thread), the frontier scan
+// included: this is the parity / integration surface, not a throughput path.
+// ==========================================================================
+
+namespace kvg {
+
+struct TreeCacheDev {
+  SimDev sim;  // tree pointers; log = per-op victim scratch
+  Lead lead;   // persistent scalars between exec calls
+};
+
+__device__ u64 tc_evict(const SimDev& D, Lead& L, u64 needed, u64* offl) {
+  if (needed == 0) return 0;  // cache_tree.cpp:272
+  u32 nf = 0;
+  for (u32 i = 1; i < L.t_alloc; ++i)
+    if (t_frontier(D.tnodes[i]))
+      D.fr[nf++] = FrEnt{D.tnodes[i].last_access, D.tnodes[i].ordinal, i, 0};
+  return t_evict_pop(D, L, nf, needed, offl);
+}
+
+// reload, cache_tree.cpp:321-368 (mirrors the engine's reload phases)
+__device__ u64 tc_reload(const SimDev& D, Lead& L, u32 a, u64 len, u64 from, u64 maxt, u64* offl) {
+  if (from >= len || maxt == 0) return 0;
+  TNodeDev* N = D.tnodes;
+  const u64 n = len / L.ps;
+  u32 node = 0;
+  u64 pos = 0;
+  while (pos < from) {
+    const u32 c = (pos % L.ps == 0) ? t_find_child(D, L, node, a, pos / L.ps, n) : 0;
+    if (c == 0 || pos + static_cast<u64>(N[c].npages) * L.ps > from) {
+      fail(L, E_OFFLOAD);
+      return 0;
+    }
+    pos += static_cast<u64>(N[c].npages) * L.ps;
+    node = c;
+  }
+  const u64 now = ++L.cclock;
+  u64 promoted = 0;
+  while (pos < len && promoted < maxt) {
+    const u32 c = t_find_child(D, L, node, a, pos / L.ps, n);
+    if (c == 0 || !N[c].host) break;
+    u64 ka = t_common(D, L, c, a, pos / L.ps, n);
+    bool full = ka == N[c].npages;
+    const u64 want = (maxt - promoted) / L.ps;
+    if (ka > want) {
+      ka = want;
+      full = false;
+    }
+    if (ka == 0) break;
+    if (ka < N[c].npages) t_split(D, L, c, ka);
+    if (L.capacity - L.used < ka) {
+      tc_evict(D, L, ka - (L.capacity - L.used), offl);
+      if (L.capacity - L.used < ka) break;
+    }
+    N[c].host = 0;
+    N[c].device_slots = static_cast<u32>(ka);
+    N[c].last_access = now;
+    L.used += ka;
+    t_gain(D, c);
+    promoted += ka * L.ps;
+    pos += ka * L.ps;
+    node = c;
+    if (!full) break;
+  }
+  return promoted;
+}
+
+__global__ void cache_tree_kernel(TreeCacheDev* T, const kvg_cache_op* ops, u32 n_ops,
+                                  kvg_cache_op_result* res, kvg_victim* vic, u64 vic_cap,
+                                  u64* n_vic) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const SimDev& D = T->sim;
+  Lead& L = T->lead;
+  for (u32 i = 0; i < n_ops; ++i) {
+    const kvg_cache_op& o = ops[i];
+    kvg_cache_op_result r;
+    r.status = KVG_OK;
+    r._pad = 0;
+    r.r0 = r.r1 = 0;
+    r.victims_begin = *n_vic;
+    L.err = E_NONE;
+    L.status = KVG_OK;
+    L.n_log = 0;
+    L.m_id = o.agent;
+    u64 offl = 0;
+    switch (o.kind) {
+      case KVG_OP_MATCH: {
+        u64 hm = 0;
+        r.r0 = t_match(D, L, o.agent, o.len, &hm);
+        r.r1 = hm;
+        break;
+      }
+      case KVG_OP_INSERT: {  // cache_tree.cpp:170-228
+        const u64 n = o.len / L.ps;
+        if (n == 0) {
+          r.r0 = 1;
+          break;
+        }
+        bool ok = true;
+        for (;;) {
+          const u64 need = t_missing(D, L, o.agent, n);
+          const u64 free_slots = L.capacity - L.used;
+          if (need <= free_slots) break;
+          if (tc_evict(D, L, need - free_slots, &offl) == 0) {
+            ok = false;
+            break;
+          }
+        }
+        if (ok) {
+          r.r1 = t_insert_commit(D, L, o.agent, n);
+          r.r0 = 1;
+        }
+        break;
+      }
+      case KVG_OP_RELOAD:
+        r.r0 = tc_reload(D, L, o.agent, o.len, o.arg, o.arg2, &offl);
+        r.r1 = offl;
+        break;
+      case KVG_OP_EVICT: r.r0 = tc_evict(D, L, o.arg, &offl); break;
+      case KVG_OP_PIN:
+      case KVG_OP_UNPIN:
+        if (o.arg > o.len) fail(L, E_PIN_MISSING);
+        else t_pin(D, L, o.agent, o.arg, o.kind == KVG_OP_PIN ? 1 : -1);
+        break;
+      case KVG_OP_DISCARD: t_discard(D, L, o.agent, o.len, o.arg); break;
+      default: fail(L, E_PIN_MISSING); break;
+    }
+    if (L.err != E_NONE) r.status = KVG_ERR_STATE;
+    // victims of this op, in the order the tree evicted them
+    const u64 nl = L.n_log < D.log_cap ? L.n_log : D.log_cap;
+    for (u64 k = 0; k < nl; ++k) {
+      const kvg_log_record& lr = D.log[k];
+      if (lr.kind != KVG_LOG_VICTIM) continue;
+      if (*n_vic < vic_cap) vic[*n_vic] = kvg_victim{lr.a, lr.b};
+      ++*n_vic;
+    }
+    r.victims_end = *n_vic;
+    r.clock = L.cclock;
+    r.used = L.used;
+    res[i] = r;
+  }
+}
+
+__global__ void cache_tree_init(TreeCacheDev* T) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  tree_init(T->sim, T->lead);
+}
+
+}  // namespace kvg

@@ -99,8 +99,20 @@ size_t hot_smem(u64 n) {
 
 // ----------------------------------------------------------------- cache API
 
+namespace kvg_tree_seam {  // engine.cu
+size_t state_bytes();
+cudaError_t init(void* d_state, const kvg::SimDev& sim, unsigned long long capacity,
+                 unsigned long long page_size, unsigned long long shared_pages);
+cudaError_t exec(void* d_state, const kvg_cache_op* d_ops, unsigned n, kvg_cache_op_result* d_res,
+                 kvg_victim* d_vic, unsigned long long vic_cap, unsigned long long* d_nvic);
+cudaError_t hit_window(const void* d_state, double* m, double* r);
+}  // namespace kvg_tree_seam
+
 struct kvg_cache {
   int device = 0;
+  bool offload = false;
+  void* tree_state = nullptr;      // offload: kvg::TreeCacheDev (engine.cu)
+  unsigned long long* d_nvic = nullptr;
   u64 capacity = 0, page_size = 1, shared_pages = 0, buckets = 0;
   char* mem = nullptr;
   kvg::CacheDev h{};
@@ -120,8 +132,8 @@ KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity, uint64_t page
   if (out == nullptr) return (kvg_status)set_error(KVG_ERR_CONFIG, "null argument");
   if (capacity == 0 || page_size == 0)
     return (kvg_status)set_error(KVG_ERR_CONFIG, "capacity and page size must be > 0");
-  if (eviction != KVG_EVICT_DISCARD)
-    return (kvg_status)set_error(KVG_ERR_CONFIG, "offload eviction is not implemented on the device");
+  if (eviction != KVG_EVICT_DISCARD && eviction != KVG_EVICT_OFFLOAD)
+    return (kvg_status)set_error(KVG_ERR_CONFIG, "unknown eviction mode");
   int count = 0;
   if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
     return (kvg_status)set_error(KVG_ERR_CUDA, "no CUDA device: the B200 engine has no CPU fallback");
@@ -131,6 +143,51 @@ KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity, uint64_t page
   c->capacity = capacity;
   c->page_size = page_size;
   c->shared_pages = shared_prompt ? prompt_tokens / page_size : 0;
+  if (eviction == KVG_EVICT_OFFLOAD) {  // node-level tree (tree.cuh), leader-serial seam
+    c->offload = true;
+    c->victim_cap = 1 << 20;
+    // nodes partition the pages the tree holds; host pages are not bounded by
+    // the capacity, so size for 64 x capacity plus 4096 pages per agent
+    const u64 tcap = 64 * capacity + 4096ull * std::max<u32>(1, max_agents) + 2;
+    const u64 hslots = next_pow2(4 * tcap);
+    const u64 logcap = 2 * capacity + 64;
+    const u64 bytes = align_up(kvg_tree_seam::state_bytes()) + align_up(tcap * sizeof(kvg::TNodeDev)) +
+                      3 * align_up(tcap * 4) + align_up(tcap * sizeof(kvg::FrEnt)) +
+                      align_up(hslots * 8) + align_up(hslots * 4) +
+                      align_up(logcap * sizeof(kvg_log_record)) + 256;
+    CUDA_TRY(cudaMalloc(&c->mem, bytes));
+    CUDA_TRY(cudaMalloc(&c->d_victims, c->victim_cap * sizeof(kvg_victim) + 64));
+    c->d_nvic = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<char*>(c->d_victims) + c->victim_cap * sizeof(kvg_victim));
+    CUDA_TRY(cudaMemset(c->d_nvic, 0, 8));
+    char* p = c->mem;
+    c->tree_state = p;
+    p += align_up(kvg_tree_seam::state_bytes());
+    kvg::SimDev sim;
+    std::memset(&sim, 0, sizeof sim);
+    sim.tnodes = reinterpret_cast<kvg::TNodeDev*>(p);
+    p += align_up(tcap * sizeof(kvg::TNodeDev));
+    sim.tfree = reinterpret_cast<u32*>(p);
+    p += align_up(tcap * 4);
+    sim.tstack = reinterpret_cast<u32*>(p);
+    p += align_up(tcap * 4);
+    p += align_up(tcap * 4);
+    sim.fr = reinterpret_cast<kvg::FrEnt*>(p);
+    p += align_up(tcap * sizeof(kvg::FrEnt));
+    sim.hkeys = reinterpret_cast<u64*>(p);
+    CUDA_TRY(cudaMemset(p, 0xff, hslots * 8));
+    p += align_up(hslots * 8);
+    sim.hvals = reinterpret_cast<u32*>(p);
+    p += align_up(hslots * 4);
+    sim.log = reinterpret_cast<kvg_log_record*>(p);
+    sim.log_cap = logcap;
+    sim.tcap = static_cast<u32>(tcap);
+    sim.hmask = static_cast<u32>(hslots - 1);
+    sim.shared_pages = c->shared_pages;
+    CUDA_TRY(kvg_tree_seam::init(c->tree_state, sim, capacity, page_size, c->shared_pages));
+    *out = c;
+    return KVG_OK;
+  }
   c->buckets = bucket_count(capacity, max_agents);
   const u64 tb = c->buckets * kvg::kChunk * sizeof(kvg::Slot);
   const u64 ob = align_up(c->buckets * sizeof(u32));
@@ -173,6 +230,28 @@ KVG_API kvg_status kvg_cache_exec(kvg_cache* c, const kvg_cache_op* ops, size_t 
     return (kvg_status)set_error(KVG_ERR_CONFIG, "null argument");
   if (n == 0) return KVG_OK;
   CUDA_TRY(cudaSetDevice(c->device));
+  if (c->offload) {  // node-level tree: victims already in eviction order
+    kvg_cache_op* d_ops = nullptr;
+    kvg_cache_op_result* d_res = nullptr;
+    CUDA_TRY(cudaMalloc(&d_ops, n * sizeof(kvg_cache_op)));
+    CUDA_TRY(cudaMalloc(&d_res, n * sizeof(kvg_cache_op_result)));
+    CUDA_TRY(cudaMemcpy(d_ops, ops, n * sizeof(kvg_cache_op), cudaMemcpyHostToDevice));
+    unsigned long long base = 0, nv = 0;
+    CUDA_TRY(cudaMemcpy(&base, c->d_nvic, 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(kvg_tree_seam::exec(c->tree_state, d_ops, static_cast<unsigned>(n), d_res,
+                                 c->d_victims, c->victim_cap, c->d_nvic));
+    CUDA_TRY(cudaMemcpy(results, d_res, n * sizeof(kvg_cache_op_result), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(&nv, c->d_nvic, 8, cudaMemcpyDeviceToHost));
+    cudaFree(d_ops);
+    cudaFree(d_res);
+    if (nv > c->victim_cap) return (kvg_status)set_error(KVG_ERR_STATE, "victim list overflow");
+    c->victims.resize(nv);
+    if (nv > base)
+      CUDA_TRY(cudaMemcpy(c->victims.data() + base, c->d_victims + base,
+                          (nv - base) * sizeof(kvg_victim), cudaMemcpyDeviceToHost));
+    CUDA_TRY(kvg_tree_seam::hit_window(c->tree_state, &c->hit_m, &c->hit_r));
+    return KVG_OK;
+  }
   kvg_cache_op* d_ops = nullptr;
   kvg_cache_op_result* d_res = nullptr;
   CUDA_TRY(cudaMalloc(&d_ops, n * sizeof(kvg_cache_op)));

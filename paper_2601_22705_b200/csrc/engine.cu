@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstring>
+
 #include "kvg_device.h"
 
 namespace kvg {
@@ -788,3 +790,49 @@ extern "C" __attribute__((visibility("default"))) int kvg_debug_profile(unsigned
   return 0;
 }
 #endif
+
+// --------------------------------------------------------------------------
+// Host glue of the offload-mode CacheTree seam (used by capi.cu, which does
+// not see the Lead layout).
+namespace kvg_tree_seam {
+
+size_t state_bytes() { return sizeof(kvg::TreeCacheDev); }
+
+cudaError_t init(void* d_state, const kvg::SimDev& sim, unsigned long long capacity,
+                 unsigned long long page_size, unsigned long long shared_pages) {
+  kvg::TreeCacheDev h;
+  std::memset(&h, 0, sizeof h);
+  h.sim = sim;
+  h.lead.capacity = capacity;
+  h.lead.capacity_d = static_cast<double>(capacity);
+  h.lead.ps = page_size;
+  h.lead.S = shared_pages;
+  h.lead.offload = 1;
+  cudaError_t e = cudaMemcpy(d_state, &h, sizeof h, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  kvg::cache_tree_init<<<1, 1>>>(static_cast<kvg::TreeCacheDev*>(d_state));
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e;
+}
+
+cudaError_t exec(void* d_state, const kvg_cache_op* d_ops, unsigned n, kvg_cache_op_result* d_res,
+                 kvg_victim* d_vic, unsigned long long vic_cap, unsigned long long* d_nvic) {
+  kvg::cache_tree_kernel<<<1, 32>>>(static_cast<kvg::TreeCacheDev*>(d_state), d_ops, n, d_res,
+                                    d_vic, vic_cap, d_nvic);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e;
+}
+
+cudaError_t hit_window(const void* d_state, double* m, double* r) {
+  kvg::TreeCacheDev h;
+  cudaError_t e = cudaMemcpy(&h, d_state, sizeof h, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) {
+    *m = h.lead.hit_m;
+    *r = h.lead.hit_r;
+  }
+  return e;
+}
+
+}  // namespace kvg_tree_seam

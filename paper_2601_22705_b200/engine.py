@@ -298,9 +298,10 @@ class DeviceCache:
     """Device-resident paged prefix cache driven through CacheTree-style ops."""
 
     def __init__(self, capacity: int, page_size: int = 1, prompt_tokens: int = 0,
-                 shared_prompt: bool = False, max_agents: int = 64, device: int = 0):
+                 shared_prompt: bool = False, max_agents: int = 64, device: int = 0,
+                 eviction: int = abi.EVICT_DISCARD):
         h = C.c_void_p()
-        _check(lib().kvg_cache_create(device, capacity, page_size, abi.EVICT_DISCARD,
+        _check(lib().kvg_cache_create(device, capacity, page_size, eviction,
                                       prompt_tokens, int(shared_prompt), max_agents,
                                       C.byref(h)))
         self.h = h
@@ -310,8 +311,9 @@ class DeviceCache:
         ordered as the reference evicts them."""
         n = len(ops)
         arr = (abi.CacheOp * max(1, n))()
-        for i, (k, a, ln, arg) in enumerate(ops):
-            arr[i] = abi.CacheOp(kind=k, agent=a, len=ln, arg=arg)
+        for i, op in enumerate(ops):
+            k, a, ln, arg = op[:4]
+            arr[i] = abi.CacheOp(kind=k, agent=a, len=ln, arg=arg, arg2=op[4] if len(op) > 4 else 0)
         res = (abi.CacheOpResult * max(1, n))()
         _check(lib().kvg_cache_exec(self.h, arr, n, res))
         out = []
