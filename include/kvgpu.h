@@ -383,10 +383,13 @@ KVG_API kvg_status kvg_controllers_update_window(kvg_controllers* c, const doubl
 /* One admission pass on every controller. at_boundary and commands are
  * concatenated per controller (controller i's slice starts at the sum of
  * total_agents[0..i) and is total_agents[i] long); n_out[i] = commands
- * controller i emitted. */
+ * controller i emitted. status[i] (optional) is KVG_ERR_STATE when the pass
+ * emitted more commands than agents (possible only after API misuse put an
+ * id on two lists; the reference fails that call, capi.cpp:228-236). */
 KVG_API kvg_status kvg_controllers_admission_pass(kvg_controllers* c,
                                                   const uint8_t* at_boundary,
-                                                  kvg_command* commands, size_t* n_out);
+                                                  kvg_command* commands, size_t* n_out,
+                                                  int32_t* status);
 /* Applies events in submission order per controller; status[i] (optional)
  * is the kvg_status of event i (KVG_ERR_STATE for an unknown agent, like
  * UnknownAgent). */

@@ -94,19 +94,19 @@ __device__ __forceinline__ u32 ring(u32 head, u32 k, u32 cap) {
 // admission_pass, controller.cpp:124-160. One warp per controller; every
 // lane tracks the list sizes in registers (identical values), lane 0 writes.
 __global__ void k_admission(CtlDev* cs, u32 n, const uint8_t* at_boundary, const u64* agent_off,
-                            kvg_command* cmds, u64* n_out) {
+                            const u64* cmd_off, kvg_command* cmds, u64* n_out) {
   const u32 ci = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
   if (ci >= n) return;
   CtlDev& c = cs[ci];
   const uint8_t* bnd = at_boundary + agent_off[ci];
-  kvg_command* out = cmds + agent_off[ci];
+  kvg_command* out = cmds + cmd_off[ci];
   u32* const active = c.active;
   u32 act = c.act_n, paus_n = c.paus_n, paus_head = c.paus_head;
   u32 pend_n = c.pend_n, pend_head = c.pend_head;
   const u32 total = c.cap;
   u64 k = 0;
-  const u64 kcap = agent_off[ci + 1] - agent_off[ci];  // commands buffer: total_agents
+  const u64 kcap = cmd_off[ci + 1] - cmd_off[ci];  // scratch: the list capacity
   const u64 limit = admission_limit(c);
   const bool gated = c.policy.kind == KVG_POLICY_AGENT_CAP || c.policy.kind == KVG_POLICY_AIMD;
   if (gated) {
@@ -244,6 +244,7 @@ struct kvg_controllers {
   kvg::CtlDev* d = nullptr;
   kvg::u32* lists = nullptr;
   kvg::u64* agent_off = nullptr;  // device [n+1]
+  kvg::u64* list_off = nullptr;   // device [n+1]
   std::vector<kvg::u64> h_off;    // host copy
   std::vector<kvg::u64> l_off;    // list offsets (capacity per controller)
   std::vector<kvg::u32> total;
@@ -287,6 +288,7 @@ KVG_API kvg_status kvg_controllers_create(int device, size_t n, const kvg_policy
   cudaError_t e = cudaMalloc(&h->d, std::max<size_t>(1, n) * sizeof(kvg::CtlDev));
   if (e == cudaSuccess) e = cudaMalloc(&h->lists, std::max<kvg::u64>(1, 3 * slots) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&h->agent_off, (n + 1) * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&h->list_off, (n + 1) * 8);
   if (e != cudaSuccess) {
     kvg_controllers_free(h);
     return (kvg_status)set_error(KVG_ERR_CUDA, cudaGetErrorString(e));
@@ -312,6 +314,8 @@ KVG_API kvg_status kvg_controllers_create(int device, size_t n, const kvg_policy
     e = cudaMemcpy(h->d, hs.data(), n * sizeof(kvg::CtlDev), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
       e = cudaMemcpy(h->agent_off, h->h_off.data(), (n + 1) * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(h->list_off, h->l_off.data(), (n + 1) * 8, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
       kvg_controllers_free(h);
       return (kvg_status)set_error(KVG_ERR_CUDA, cudaGetErrorString(e));
@@ -327,6 +331,7 @@ KVG_API void kvg_controllers_free(kvg_controllers* h) {
   cudaFree(h->d);
   cudaFree(h->lists);
   cudaFree(h->agent_off);
+  cudaFree(h->list_off);
   delete h;
 }
 
@@ -355,32 +360,53 @@ KVG_API kvg_status kvg_controllers_update_window(kvg_controllers* h, const doubl
 }
 
 KVG_API kvg_status kvg_controllers_admission_pass(kvg_controllers* h, const uint8_t* at_boundary,
-                                                  kvg_command* commands, size_t* n_out) {
+                                                  kvg_command* commands, size_t* n_out,
+                                                  int32_t* status) {
   if (h == nullptr || (h->n > 0 && (at_boundary == nullptr || commands == nullptr ||
                                     n_out == nullptr)))
     return (kvg_status)set_error(KVG_ERR_CONFIG, "null argument");
   if (h->n == 0) return KVG_OK;
   CUDA_TRY2(cudaSetDevice(h->device));
-  const kvg::u64 slots = h->h_off[h->n];
+  const kvg::u64 slots = h->h_off[h->n], lslots = h->l_off[h->n];
   char* buf = nullptr;
   const size_t bb = (slots + 15) / 16 * 16;
-  CUDA_TRY2(cudaMalloc(&buf, bb + slots * sizeof(kvg_command) + h->n * 8 + 16));
+  CUDA_TRY2(cudaMalloc(&buf, bb + lslots * sizeof(kvg_command) + h->n * 8 + 16));
   uint8_t* d_b = reinterpret_cast<uint8_t*>(buf);
   kvg_command* d_c = reinterpret_cast<kvg_command*>(buf + bb);
-  kvg::u64* d_n = reinterpret_cast<kvg::u64*>(buf + bb + slots * sizeof(kvg_command));
+  kvg::u64* d_n = reinterpret_cast<kvg::u64*>(buf + bb + lslots * sizeof(kvg_command));
   cudaMemcpy(d_b, at_boundary, slots, cudaMemcpyHostToDevice);
   const unsigned warps_per_block = 4;
   kvg::k_admission<<<static_cast<unsigned>((h->n + warps_per_block - 1) / warps_per_block),
                      32 * warps_per_block>>>(h->d, static_cast<kvg::u32>(h->n), d_b,
-                                             h->agent_off, d_c, d_n);
+                                             h->agent_off, h->list_off, d_c, d_n);
   cudaError_t e = cudaGetLastError();
   std::vector<kvg::u64> nn(h->n);
+  std::vector<kvg_command> cc(lslots);
   if (e == cudaSuccess) e = cudaMemcpy(nn.data(), d_n, h->n * 8, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess)
-    e = cudaMemcpy(commands, d_c, slots * sizeof(kvg_command), cudaMemcpyDeviceToHost);
+    e = cudaMemcpy(cc.data(), d_c, lslots * sizeof(kvg_command), cudaMemcpyDeviceToHost);
   cudaFree(buf);
   if (e != cudaSuccess) return (kvg_status)set_error(KVG_ERR_CUDA, cudaGetErrorString(e));
-  for (size_t i = 0; i < h->n; ++i) n_out[i] = nn[i];
+  // A pass emits at most one command per agent unless the lists hold an id
+  // twice (API misuse): the reference then fails the call after the pass has
+  // run (capi.cpp:228-236); so does controller i here (status[i]).
+  int worst = KVG_OK;
+  for (size_t i = 0; i < h->n; ++i) {
+    const kvg::u64 cap = h->h_off[i + 1] - h->h_off[i];
+    int st = KVG_OK;
+    if (nn[i] > cap) {
+      st = KVG_ERR_STATE;
+      n_out[i] = 0;
+      if (worst == KVG_OK) worst = st;
+    } else {
+      n_out[i] = nn[i];
+      std::copy(cc.begin() + h->l_off[i], cc.begin() + h->l_off[i] + nn[i],
+                commands + h->h_off[i]);
+    }
+    if (status) status[i] = st;
+  }
+  if (worst != KVG_OK)
+    return (kvg_status)set_error(worst, "admission pass emitted more commands than agents");
   return KVG_OK;
 }
 

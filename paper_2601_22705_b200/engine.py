@@ -86,7 +86,7 @@ def lib():
     L.kvg_controllers_update_window.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double),
                                                 P(C.c_double)]
     L.kvg_controllers_admission_pass.argtypes = [C.c_void_p, P(C.c_uint8), P(abi.Command),
-                                                 P(C.c_size_t)]
+                                                 P(C.c_size_t), P(C.c_int32)]
     L.kvg_controllers_apply.argtypes = [C.c_void_p, P(abi.CtlEvent), C.c_size_t, P(C.c_int32)]
     L.kvg_controllers_state.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double),
                                         P(C.c_uint64), P(C.c_size_t), P(C.c_size_t),
@@ -369,12 +369,21 @@ class DeviceControllers:
         _check(lib().kvg_controllers_update_window(self.h, u, r, w))
         return list(w)[: self.n]
 
-    def admission_pass(self, at_boundary: list[list[bool]]) -> list[list[tuple[int, int]]]:
+    def admission_pass(self, at_boundary: list[list[bool]], statuses: list | None = None
+                       ) -> list[list[tuple[int, int]]]:
+        """Commands per controller. A controller whose pass emitted more
+        commands than agents (API misuse) reports status KVG_ERR_STATE in
+        `statuses` and no commands."""
         flat = [int(b) for row in at_boundary for b in row]
         bnd = (C.c_uint8 * max(1, len(flat)))(*flat)
         cmds = (abi.Command * max(1, self.off[-1]))()
         nout = (C.c_size_t * max(1, self.n))()
-        _check(lib().kvg_controllers_admission_pass(self.h, bnd, cmds, nout))
+        st = (C.c_int32 * max(1, self.n))()
+        rc = lib().kvg_controllers_admission_pass(self.h, bnd, cmds, nout, st)
+        if rc not in (abi.KVG_OK, abi.KVG_ERR_STATE):
+            _check(rc)
+        if statuses is not None:
+            statuses[:] = list(st)[: self.n]
         return [[(cmds[self.off[i] + k].kind, cmds[self.off[i] + k].agent)
                  for k in range(nout[i])] for i in range(self.n)]
 

@@ -49,12 +49,13 @@ class RefCtl:
         return w.value
 
     def admission(self, bnd):
+        """(status, commands); commands are empty when the call failed."""
         b = (C.c_uint8 * max(1, self.total))(*bnd)
         cmds = (abi.Command * max(1, self.total))()
         n = C.c_size_t()
-        assert self.lib.kva_controller_admission_pass(self.h, b, self.total, cmds, self.total,
-                                                      C.byref(n)) == 0
-        return [(cmds[k].kind, cmds[k].agent) for k in range(n.value)]
+        rc = self.lib.kva_controller_admission_pass(self.h, b, self.total, cmds, self.total,
+                                                    C.byref(n))
+        return rc, ([(cmds[k].kind, cmds[k].agent) for k in range(n.value)] if rc == 0 else [])
 
     def event(self, kind, agent):
         f = ["kva_controller_add_pending", "kva_controller_on_agent_finished",
@@ -110,7 +111,11 @@ def test_device_controllers_match_reference(seed):
                 assert [x.hex() for x in got] == [x.hex() for x in exp]
             elif roll < 0.7:
                 bnd = [[int(rng.random() < 0.6) for _ in range(n)] for _, _, n in specs]
-                assert dev.admission_pass(bnd) == [r.admission(bnd[i]) for i, r in enumerate(refs)]
+                st = []
+                got = dev.admission_pass(bnd, st)
+                exp = [r.admission(bnd[i]) for i, r in enumerate(refs)]
+                assert [s_ != 0 for s_ in st] == [e[0] != 0 for e in exp]
+                assert got == [e[1] for e in exp]
             else:
                 evs = []
                 for i, (_, _, n) in enumerate(specs):

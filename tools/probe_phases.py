@@ -18,8 +18,16 @@ which = sys.argv[1] if len(sys.argv) > 1 else "c4"
 if which == "c4":
     pop = engine.Population(config.c1_toy().workload, 42)
     specs = [engine.SimSpec.from_scenario(s, population=pop) for s in config.c4_sweep()]
-else:
+elif which == "c2":
     specs = [engine.SimSpec.from_scenario(config.c2_qwen("aimd"))]
+elif which.startswith("c5s"):  # scaled C5 shape: c5s<agents>
+    ag = int(which[3:])
+    s = config.c5_stress("aimd", agents=ag, capacity=1)
+    s.engine.capacity = config.scaled_capacity(engine.Population(s.workload, s.seed).peak_aggregate_tokens)
+    specs = [engine.SimSpec.from_scenario(s)]
+else:
+    s = config.c3_dsv3("aimd", agents=int(which[3:]) if which[3:] else 2048)
+    specs = [engine.SimSpec.from_scenario(s)]
 lib = engine.lib()
 lib.kvg_debug_profile.argtypes = [C.POINTER(C.c_ulonglong)]
 b = engine.Batch(specs)
@@ -29,7 +37,8 @@ lib.kvg_debug_profile(buf)  # clear (first run)
 b.run()
 lib.kvg_debug_profile(buf)
 tot = sum(buf)
-print(which, "kernel ms", b.timing()[1], "total sim-cycles", tot)
+r = b.result(0)
+print(which, "kernel ms", b.timing()[1], "total sim-cycles", tot, "events", r["events"], "stalls", r["stall_events"], "evict_calls", r["evict_calls"], "agent_steps", r["agent_steps"], "status", r["status"])
 for i in sorted(range(48), key=lambda i: -buf[i]):
     if buf[i]:
         print(f"{100 * buf[i] / tot:6.2f}%  {names.get(i, i)}")
