@@ -72,6 +72,7 @@ enum OpKind : int {
   OP_REBUILD,    // rehash live buckets into the alternate table
   OP_SCANFREE,   // free pages by (owner, min index) over the whole table
   OP_FRONTIER,   // offload tree: compact eviction-frontier nodes (tree.cuh)
+  OP_TICKS,      // warp 0: pipelined control ticks + no-op admission checks
 };
 
 enum RangeFlags : u32 {
@@ -378,26 +379,22 @@ __device__ __noinline__ void coop_range(Op& op, int warp, int lane, int nw) {
       range_chunk(op, tag, shared ? s_lo : q_lo, shared ? s_hi : q_hi, cb, cur, found, lane, acc);
     }
   }
-  // warp reductions, then one shared atomic per warp
-  for (int o = 16; o > 0; o >>= 1) {
-    acc.created += __shfl_down_sync(FULL, acc.created, o);
-    acc.freed += __shfl_down_sync(FULL, acc.freed, o);
-    acc.up += __shfl_down_sync(FULL, acc.up, o);
-    acc.down += __shfl_down_sync(FULL, acc.down, o);
-    acc.resident += __shfl_down_sync(FULL, acc.resident, o);
-    const u64 om = __shfl_down_sync(FULL, acc.miss, o);
-    acc.miss = om < acc.miss ? om : acc.miss;
-    const int oe = __shfl_down_sync(FULL, acc.err, o);
-    acc.err = oe > acc.err ? oe : acc.err;
-  }
+  // warp reductions (one REDUX each), then one shared atomic per warp
+  const u32 created = __reduce_add_sync(FULL, acc.created);
+  const u32 freed = __reduce_add_sync(FULL, acc.freed);
+  const u32 up = __reduce_add_sync(FULL, acc.up);
+  const u32 down = __reduce_add_sync(FULL, acc.down);
+  const u32 resident = __reduce_add_sync(FULL, acc.resident);
+  const u32 miss = __reduce_min_sync(FULL, acc.miss == ~0ull ? NIL32 : static_cast<u32>(acc.miss));
+  const u32 err = __reduce_max_sync(FULL, static_cast<u32>(acc.err));
   if (lane == 0) {
-    if (acc.created) atomicAdd(&op.created, acc.created);
-    if (acc.freed) atomicAdd(&op.freed, acc.freed);
-    if (acc.up) atomicAdd(&op.pin_up, acc.up);
-    if (acc.down) atomicAdd(&op.pin_down, acc.down);
-    if (acc.resident) atomicAdd(&op.resident, acc.resident);
-    if (acc.miss != ~0ull) atomicMin(&op.first_miss, acc.miss);
-    if (acc.err) atomicMax(&op.err, acc.err);
+    if (created) atomicAdd(&op.created, created);
+    if (freed) atomicAdd(&op.freed, freed);
+    if (up) atomicAdd(&op.pin_up, up);
+    if (down) atomicAdd(&op.pin_down, down);
+    if (resident) atomicAdd(&op.resident, resident);
+    if (miss != NIL32) atomicMin(&op.first_miss, static_cast<unsigned long long>(miss));
+    if (err) atomicMax(&op.err, static_cast<int>(err));
   }
 }
 
@@ -676,7 +673,7 @@ __device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int 
     }
     __stcg(&op.summ[b].dev, e.dev & ~v);
   });
-  for (int o = 16; o > 0; o >>= 1) freed += __shfl_down_sync(FULL, freed, o);
+  freed = __reduce_add_sync(FULL, freed);
   if (lane == 0 && freed) atomicAdd(&op.freed, freed);
 }
 

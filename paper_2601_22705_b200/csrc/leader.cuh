@@ -740,6 +740,134 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   L.n_trace = n_trace;
 }
 
+// Whether the warp-pipelined tick op applies: the next housekeeping event is
+// a control tick well before the next agent event, with no admission check
+// pending in front of it (the steady state between agent events). Smoothed
+// signals (an EMA chain per tick) and offload mode (a link-queue purge per
+// tick) stay on the scalar path.
+__device__ __forceinline__ bool ticks_apply(const Lead& L) {
+  if (L.offload || L.status != KVG_OK || L.finished == L.n || !L.tick_on || L.adm_on) return false;
+  if (L.kind == KVG_POLICY_AIMD && L.cfg.signal_smoothing > 0) return false;
+  const double t_agent = L.hsize > 0 ? L.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
+  return L.tick_t < t_agent && !(L.tick_t > L.horizon) &&
+         L.tick_t + 4.0 * L.interval < t_agent;  // enough ticks to pay for the op
+}
+
+// OP_TICKS (warp 0): the same event sequence as fast_housekeeping — control
+// tick k at t_k, then the admission check it schedules at t_k, repeated —
+// 32 ticks per round. Lane k computes tick k's own chain values exactly as
+// the scalar loop would (t_{k+1} = t_k + interval, hit_m / hit_r decayed by
+// k repeated multiplications, hit = m / r): independent per lane, so the
+// divisions and the trace-row stores run in parallel. The window recurrence
+// (controller.cpp:67-91) stays sequential but is a few flops per tick with
+// every hit rate already in a register. Stops exactly where the scalar loop
+// stops: before a tick that is not earlier than the next agent event or is
+// past the horizon, or after a tick whose admission check would act
+// (engine.cpp:245-291, controller.cpp:124-160).
+__device__ __noinline__ void coop_ticks(const SimDev& D, Lead& L, int lane) {
+  const double t_agent = L.hsize > 0 ? L.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
+  const double horizon = L.horizon, interval = L.interval, decay = L.decay;
+  const double usage = static_cast<double>(L.used) / L.capacity_d;
+  const bool nready0 = L.n_ready == 0;
+  const u64 act = L.act_size;
+  const bool admit_src = L.pend_size > 0 || (L.gated && L.paus_size > 0);
+  const u32 kind = L.kind;
+  const kvg_controller_config c = L.cfg;
+  const u64 pending = static_cast<u64>(L.pend_size) + L.paus_size;
+  const u64 dec = L.decoded_cum, rec = L.rec_cum;
+  const double fixed_window = kind == KVG_POLICY_UNCONTROLLED ? static_cast<double>(L.n)
+                                                              : static_cast<double>(L.cap);
+  double t0 = L.tick_t, m0 = L.hit_m, r0 = L.hit_r, w = L.window;
+  u64 ord = L.ord, events = L.events, ticks = L.ticks;
+  unsigned long long n_trace = L.n_trace;
+  bool done = false, adm_pending = false;
+  double clock = L.clock;
+  while (!done) {
+    // lane k: tick k's time and hit window (sequential chains, exact order)
+    double t = t0, m = m0, r = r0;
+    for (int i = 0; i < lane; ++i) {
+      t = t + interval;
+      m = m * decay;
+      r = r * decay;
+    }
+    const double hit = r > 0 ? m / r : 1.0;
+    const bool in_time = t < t_agent && !(t > horizon);
+    // window recurrence, every lane in lockstep; lane k keeps w_k
+    double wk = w;
+    for (int k = 0; k < 32; ++k) {
+      const double h = __shfl_sync(FULL, hit, k);
+      if (kind == KVG_POLICY_AIMD) {
+        double x = w;
+        if (usage < c.u_low) x = x + c.alpha;
+        else if (usage > c.u_high && h < c.h_thresh) x = x * c.beta;
+        w = x < c.w_min ? c.w_min : (c.w_max < x ? c.w_max : x);
+      }
+      if (lane == k) wk = w;
+    }
+    const u64 limit = kind == KVG_POLICY_UNCONTROLLED ? ~0ull
+                      : kind == KVG_POLICY_AIMD ? static_cast<u64>(floor(wk))
+                                                : static_cast<u64>(L.cap);
+    const bool noop = nready0 && !(act < limit && admit_src);
+    // processed ticks: [0, K); tick K-1's admission stays pending if it acts
+    const unsigned late = __ballot_sync(FULL, !in_time);
+    const unsigned acts = __ballot_sync(FULL, !noop);
+    const int k_time = late ? __ffs(late) - 1 : 32;  // first tick not taken
+    const int k_act = acts ? __ffs(acts) - 1 : 32;   // first tick whose check acts
+    int K = k_time;
+    if (k_act < K) {
+      K = k_act + 1;
+      adm_pending = true;
+      done = true;
+    }
+    if (k_time < 32) done = true;
+    if (K == 0) break;
+    if (lane < K && n_trace + lane < D.trace_cap) {
+      kvg_trace_row row;
+      row.time = t;
+      row.usage = usage;
+      row.hit_rate = hit;
+      row.window = kind == KVG_POLICY_AIMD ? wk : fixed_window;
+      row.active = act;
+      row.pending = pending;
+      row.decoded_cum = dec;
+      row.recompute_cum = rec;
+      row.transfers = 0;
+      row.hit_matched = m;
+      row.hit_requested = r;
+      D.trace[n_trace + lane] = row;
+    }
+    // carry the state of the last processed tick
+    const int last = K - 1;
+    clock = __shfl_sync(FULL, t, last);
+    const double m_last = __shfl_sync(FULL, m, last), r_last = __shfl_sync(FULL, r, last);
+    m0 = m_last * decay;
+    r0 = r_last * decay;
+    t0 = clock + interval;
+    w = __shfl_sync(FULL, wk, last);
+    n_trace += K;
+    ticks += K;
+    ord += 2 * K;
+    events += 2 * K - (adm_pending ? 1 : 0);
+  }
+  if (lane == 0) {
+    L.clock = clock;
+    L.tick_t = t0;
+    L.hit_m = m0;
+    L.hit_r = r0;
+    L.window = w;
+    L.tick_o = ord - 2;
+    if (adm_pending) {
+      L.adm_on = 1;
+      L.adm_t = clock;
+      L.adm_o = ord - 1;
+    }
+    L.ord = ord;
+    L.events = events;
+    L.ticks = ticks;
+    L.n_trace = n_trace;
+  }
+}
+
 // The successful tail of dispatch_member (engine.cpp:378-395): recompute
 // attribution, the member's cost-model times, InFlight, wait time, state.
 __device__ __forceinline__ void member_success(const SimDev& D, Lead& L, u32 id, u64 ctx0,
@@ -973,6 +1101,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
     switch (L.phase) {
       // ------------------------------------------------ event loop (98-136)
       case PH_EVENT: {
+        if (ticks_apply(L)) {  // pipelined ticks on warp 0, then back here
+          op.kind = OP_TICKS;
+          return;
+        }
         PROF_MARK(L, 40);
         fast_housekeeping(D, L);
         PROF_MARK(L, PH_EVENT);
@@ -1434,7 +1566,11 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     __syncthreads();
     if (op.kind == OP_EXIT) break;
     if (tid == 0) PROF_MARK(L, 32 + op.kind);
-    run_op<kDepth>(op, h, tid, warp, lane, nw);
+    if (op.kind == OP_TICKS) {
+      if (warp == 0) coop_ticks(D, L, lane);
+    } else {
+      run_op<kDepth>(op, h, tid, warp, lane, nw);
+    }
     __syncthreads();
     if (tid == 0) PROF_MARK(L, 46);
   }

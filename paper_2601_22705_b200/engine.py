@@ -405,9 +405,10 @@ class DeviceControllers:
                      paused=q[i]) for i in range(self.n)]
 
     def active(self, i: int) -> list[int]:
-        out = (C.c_uint32 * max(1, self.total[i]))()
+        cap = max(4 * self.total[i], self.total[i] + 256)  # list capacity (controllers.cu)
+        out = (C.c_uint32 * cap)()
         n = C.c_size_t()
-        _check(lib().kvg_controllers_active(self.h, i, out, self.total[i], C.byref(n)))
+        _check(lib().kvg_controllers_active(self.h, i, out, cap, C.byref(n)))
         return list(out)[: n.value]
 
     def close(self):

@@ -12,7 +12,7 @@ PH = ["EVENT", "MEMBER", "M_MATCHED", "M_INSERT", "M_EVICTED", "M_COMMIT", "M_CR
       "O_INSERT_EVICTED", "O_INSERT_FAIL", "O_EVICT_POP", "DONE", "EXITED"]
 names = {i: "leader:" + n for i, n in enumerate(PH)}
 names.update({32 + k: "coop:" + n for k, n in enumerate(
-    ["NONE", "EXIT", "RANGE", "EVICT", "REBUILD", "SCANFREE", "FRONTIER"])})
+    ["NONE", "EXIT", "RANGE", "EVICT", "REBUILD", "SCANFREE", "FRONTIER", "TICKS"])})
 names.update({40: "fast_housekeeping", 46: "leader_step entry+sync", 47: "init/finalize"})
 which = sys.argv[1] if len(sys.argv) > 1 else "c4"
 if which == "c4":
