@@ -251,7 +251,9 @@ typedef struct kvg_batch_options {
                              stats and (densely packed) trace rows into
                              pinned host memory before returning; 0: they
                              stay in HBM until first accessed */
-  uint32_t _pad;
+  uint32_t verify;        /* 1: every prefix match is also re-derived by the
+                             block-hash probe and checked (a mismatch fails
+                             the simulation with KVG_ERR_STATE) */
 } kvg_batch_options;
 
 KVG_API void kvg_batch_options_init(kvg_batch_options* o);

@@ -126,7 +126,7 @@ class LogRecord(C.Structure):
 
 class BatchOptions(C.Structure):
     _fields_ = [("warps_per_sim", u32), ("log_capacity", u32),
-                ("trace_capacity", u64), ("host_outputs", u32), ("_pad", u32)]
+                ("trace_capacity", u64), ("host_outputs", u32), ("verify", u32)]
 
 
 class Summary(C.Structure):  # kvg_summary (metrics.hpp:85-118)

@@ -109,7 +109,9 @@ struct Op {
   int log_victims;      // 1: append victims to the log / victim list
   int implicit_pins;    // engine mode: pins derived from per-agent pinned prefixes
   u64 pin_max;          // engine mode: shared-prompt pages [0, pin_max) are pinned
-  const AgentDev* agents;
+  u64 lazy_sh;          // engine mode: stamp of every resident shared page
+  unsigned int l0_min;  // engine mode: smallest shared page an eviction freed
+  AgentDev* agents;
   u64 p0, p1;
   u64 stamp;
   u64 k;                // EVICT: pages needed
@@ -484,6 +486,16 @@ __device__ __forceinline__ u32 cand_of(const Op& op, const Summ& e) {
   return e.dev & ge_mask(e.tag & 0xffffffffull, pin_thr(op, e.tag >> 32));
 }
 
+// Stamp of a summarised bucket's resident pages. Engine mode: every
+// resident page of a chain carries its chain's latest refresh stamp (the
+// shared chain: op.lazy_sh; agent a's private chain: agents[a].lazy), so raw
+// page stamps are never consulted.
+__device__ __forceinline__ u64 stamp_of(const Op& op, const Summ& e) {
+  if (!op.implicit_pins) return e.sf & kStampMask;
+  const u64 owner = e.tag >> 32;
+  return owner == 0 ? op.lazy_sh : op.agents[owner - 1].lazy;
+}
+
 // Per-page candidate test (mixed buckets).
 __device__ __forceinline__ bool page_cand(const Op& op, u64 key, u64 meta) {
   if (!(meta & kResident)) return false;
@@ -617,12 +629,12 @@ __device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int 
       __syncthreads();
       const u64 prefix = op.prefix;
       scan_summ(op, warp, lane, nw, [&](bool valid, u32 b, const Summ& e) {
-        const bool mixed = valid && (e.sf & kMixed);
+        const bool mixed = valid && !op.implicit_pins && (e.sf & kMixed);
         u32 c = 0;
         u64 st = 0;
         if (valid && !mixed) {
           c = cand_of(op, e);
-          st = e.sf & kStampMask;
+          st = stamp_of(op, e);
         }
         const bool act = c != 0 && (st >> lo_bits) == prefix;
         const u32 bin = act ? static_cast<u32>((st >> shift) & (nbins - 1)) : 0xffffffffu;
@@ -655,16 +667,22 @@ __device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int 
   unsigned int freed = 0;
   scan_summ(op, warp, lane, nw, [&](bool valid, u32 b, const Summ& e) {
     if (!valid) return;
-    if (e.sf & kMixed) {
+    if (!op.implicit_pins && (e.sf & kMixed)) {
       freed += scatter_mixed(op, b, all, T, cut);
       return;
     }
     const u32 c = cand_of(op, e);
     if (c == 0) return;
-    const u64 st = e.sf & kStampMask;
+    const u64 st = stamp_of(op, e);
     const u32 v = (all || st < T) ? c : (st == T ? c & ge_mask(e.tag & 0xffffffffull, cut) : 0u);
     if (v == 0) return;
     freed += __popc(v);
+    if (op.implicit_pins) {  // chains lose tails: the lowest victim is the new length
+      const u64 owner = e.tag >> 32;
+      const u32 low = static_cast<u32>(e.tag & 0xffffffffull) + static_cast<u32>(__ffs(v) - 1);
+      if (owner == 0) atomicMin(&op.l0_min, low);
+      else atomicMin(&op.agents[owner - 1].priv, low - static_cast<u32>(op.shared_pages));
+    }
     Slot* bk = &op.table[(size_t)b * kChunk];
     for (u32 m = v; m != 0; m &= m - 1) {
       const int l = __ffs(m) - 1;

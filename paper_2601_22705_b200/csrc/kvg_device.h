@@ -57,8 +57,11 @@ enum AgentState : uint8_t { S_PENDING, S_AWAIT, S_GEN, S_TOOL, S_PAUSED, S_DONE 
 enum EventKind : uint8_t { EV_NONE = 0, EV_GEN = 1, EV_TOOL = 2, EV_XFER = 3 };
 
 struct AgentDev {     // 64 B: two agents per 128 B line
-  u64 ctx;            // context length in tokens
-  u64 high_water;
+  u32 ctx;            // context length in tokens (< 2^32: checked at batch create)
+  u32 high_water;
+  u64 lazy;           // discard mode: stamp of this agent's latest path refresh
+                      // (match or insert); every resident page of its private
+                      // chain carries it
   double ready_since;
   double f_tool;      // InFlight (engine.cpp:71-77)
   u32 pinned_pg;      // pinned_len / page_size: pages [0, pinned_pg) of this
@@ -66,7 +69,7 @@ struct AgentDev {     // 64 B: two agents per 128 B line
   u32 f_gen, f_rec, f_obs;
   u32 act_seq;        // admission order: active_ is insertion ordered
                       // (controller.hpp:122); larger = newer
-  u32 pad0;
+  u32 priv;           // discard mode: resident private pages [S, S+priv) of its path
   uint16_t step;
   uint8_t state, ev_kind, f_has_tool, in_active;
   uint8_t ready;      // mirror of this agent's bit in the ready bitmap
@@ -130,7 +133,7 @@ struct SimDev {
   Summ* summ;
   Summ* alt_summ;
   u32 bucket_mask;    // buckets - 1 (power of two)
-  u32 pad0;
+  u32 verify;         // 1: re-derive every match by a block-hash probe and check it
   AgentDev* agents;
   u32* pend;
   u32* paus;

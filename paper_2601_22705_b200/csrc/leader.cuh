@@ -65,6 +65,8 @@ struct Lead {
   // cache scalars (cache_tree.hpp:187-197)
   u64 used, cclock, discarded, lookups, agent_steps, events, evict_calls, evicted;
   u64 pin_max, pin_priv;  // implicit pins: shared prefix max, private pinned pages
+  u64 L0, lazy_sh;        // discard mode: resident shared pages, their stamp
+  int verify, pad4;
   u64 hit_pages, created_pages, refreshed_pages, evict_scanned, agent_events;
   long long t_start;
   double hit_m, hit_r;
@@ -540,6 +542,8 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.used = L.cclock = L.discarded = L.lookups = 0;
   L.agent_steps = L.events = L.evict_calls = L.evicted = 0;
   L.pin_max = L.pin_priv = 0;
+  L.L0 = L.lazy_sh = 0;
+  L.verify = D.verify != 0;
   L.hit_pages = L.created_pages = L.refreshed_pages = L.evict_scanned = L.agent_events = 0;
   L.hit_m = L.hit_r = 0.0;
   L.n = D.n_agents;
@@ -1265,26 +1269,35 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         L.m_ctx0 = a.ctx;
         L.m_nctx = a.ctx / L.ps;
         L.m_now = ++L.cclock;  // match_prefix clock bump (cache_tree.cpp:115)
-        // match_prefix: one pipelined probe pass over the context's pages
-        // stamps the resident prefix with the stamp it will END UP with: the
-        // insert's (now+1) if the insert is predicted to succeed, the match's
-        // (now) if this is the retry of a stalled agent. A misprediction costs
-        // one extra pass (restore, or refresh inside the create); while this
-        // agent pins the prefix its stamp is invisible to eviction, so the
-        // final state is identical either way.
-        L.m_stamp = a.stalled ? L.m_now : L.m_now + 1;
-        post_range(op, id, 0, L.m_nctx, RF_STAMP, 0, L.m_stamp);
-        L.phase = PH_M_MATCHED;
-        if (L.m_nctx == 0) {
-          op.kind = OP_NONE;
-          continue;
+        // match_prefix (cache_tree.cpp:114-142). Residency is prefix-closed
+        // along a path and chains only gain pages at their ends (insert) and
+        // lose tails (eviction, discard), so the first miss is held
+        // incrementally: L0 resident shared pages, a.priv resident private
+        // ones. The refresh stamps the whole resident path; every resident
+        // page of a chain carries its chain's latest stamp, so the refresh is
+        // two scalar writes. verify=1 re-derives f with the
+        // block-hash probe (kernel 1) and checks it.
+        {
+          const u64 fres = L.L0 < L.S ? L.L0 : L.S + a.priv;
+          L.m_f = fres < L.m_nctx ? fres : L.m_nctx;
         }
-        return;
+        a.lazy = L.m_now;
+        L.lazy_sh = L.m_now;
+        L.phase = PH_M_MATCHED;
+        if (L.verify && L.m_nctx > 0) {
+          post_range(op, id, 0, L.m_nctx, 0, 0, 0);
+          return;
+        }
+        op.err = E_NONE;
+        continue;
       }
       case PH_M_MATCHED: {
-        if (op.err) fail(L, op.err);
-        const u64 f = op.first_miss < L.m_nctx ? op.first_miss : L.m_nctx;
-        if (op.resident != f) fail(L, E_PREFIX_BROKEN);
+        const u64 f = L.m_f;
+        if (L.verify && L.m_nctx > 0) {  // the probe must agree with the held state
+          if (op.err) fail(L, op.err);
+          const u64 fp = op.first_miss < L.m_nctx ? op.first_miss : L.m_nctx;
+          if (fp != f || op.resident != f) fail(L, E_PREFIX_BROKEN);
+        }
         const u64 matched = f * L.ps;
         L.lookups += f + (f < L.m_nctx ? 1 : 0);
         L.hit_pages += f;
@@ -1331,6 +1344,8 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         op.agent = L.m_id;
         op.log_clock = L.cclock;
         op.pin_max = L.pin_max;
+        op.lazy_sh = L.lazy_sh;
+        op.l0_min = NIL;
         op.err = E_NONE;
         L.phase = PH_M_EVICTED;
         return;
@@ -1339,6 +1354,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         const u64 r = op.freed;
         const u64 expect = L.m_k < L.m_e ? L.m_k : L.m_e;
         if (r != expect || op.err) fail(L, E_EVICT_MISMATCH);
+        if (op.l0_min < L.L0) L.L0 = op.l0_min;  // (private tails: a.priv, in the scatter)
         L.used -= r;
         L.discarded += r * L.ps;
         L.evicted += r;
@@ -1358,18 +1374,19 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           return;
         }
         ++L.cclock;  // insert clock bump (cache_tree.cpp:188) == m_now + 1
-        if (L.m_stamp == L.cclock) {  // prefix already carries the insert stamp
-          post_range(op, L.m_id, L.m_f, L.m_nafter, RF_CREATE, 0, L.cclock);
-          if (L.m_f == L.m_nafter) {
-            op.kind = OP_NONE;
-            L.phase = PH_M_CREATED;
-            continue;
-          }
-        } else {  // predicted stall did not happen: refresh the prefix too
-          post_range(op, L.m_id, 0, L.m_nafter, RF_STAMP | RF_CREATE, 0, L.cclock);
-        }
+        // the walk refreshes the whole path (chain stamps) and a leaf holds
+        // the missing pages [f, n_after): kernel 1 creates them
+        L.ag[L.m_id].lazy = L.cclock;
+        L.lazy_sh = L.cclock;
         L.phase = PH_M_CREATED;
-        return;
+        if (L.m_f < L.m_nafter) {
+          post_range(op, L.m_id, L.m_f, L.m_nafter, RF_CREATE, 0, L.cclock);
+          return;
+        }
+        op.kind = OP_NONE;
+        op.created = 0;
+        op.err = E_NONE;
+        continue;
       }
       case PH_M_CREATED: {
         if (op.err) fail(L, op.err);
@@ -1377,6 +1394,11 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         L.created_pages += op.created;
         if (L.m_nafter > 0) L.refreshed_pages += L.m_f;
         AgentDev& a = L.ag[L.m_id];
+        if (L.m_nafter > 0) {  // the whole path [0, n_after) is resident now
+          const u64 sh = L.m_nafter < L.S ? L.m_nafter : L.S;
+          if (sh > L.L0) L.L0 = sh;
+          a.priv = static_cast<u32>(L.m_nafter > L.S ? L.m_nafter - L.S : 0);
+        }
         const u64 stored = a.ctx - a.ctx % L.ps;
         const u64 matched = L.m_f * L.ps;
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 1, stored);
@@ -1388,16 +1410,11 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       }
       case PH_M_FAIL: {  // insert failed: engine.cpp:366-373
         AgentDev& a = L.ag[L.m_id];
-        a.ctx = L.m_ctx0;  // context.resize + token_counter rollback
+        a.ctx = static_cast<u32>(L.m_ctx0);  // context.resize + token_counter rollback
         a.stalled = 1;
-        post_range(op, L.m_id, 0, L.m_f, RF_STAMP, 0, L.m_now);
+        op.err = E_NONE;  // the path keeps the match's stamp (a.lazy, lazy_sh)
         L.phase = PH_M_RESTORED;
-        if (L.m_f == 0 || L.m_stamp == L.m_now) {  // nothing to restore
-          op.kind = OP_NONE;
-          op.err = E_NONE;
-          continue;
-        }
-        return;
+        continue;
       }
       case PH_M_RESTORED: {
         if (op.err) fail(L, op.err);
@@ -1439,6 +1456,11 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         if (!L.offload) {  // (the tree discard accounted for itself)
           L.used -= op.freed;
           L.discarded += static_cast<u64>(op.freed) * L.ps;
+          // pages from page_ceil(shared_len) on are gone (a straddling page stays, Q2)
+          const u64 fp = (L.shared_len + L.ps - 1) / L.ps;
+          const u64 keep = fp > L.S ? fp - L.S : 0;
+          AgentDev& a = L.ag[id];
+          if (a.priv > keep) a.priv = static_cast<u32>(keep);
         }
         log_rec(D, L, KVG_LOG_DISCARD, id, 0, op.freed);
         act_erase(D, L, id);  // on_request_complete / on_agent_finished
@@ -1528,8 +1550,10 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   AgentDev* const ag = L.ag;
   for (u32 i = tid; i < n; i += blockDim.x) {
     AgentDev a;
-    a.ctx = D.prompt_tokens;
+    a.ctx = static_cast<u32>(D.prompt_tokens);
     a.high_water = 0;
+    a.lazy = 0;
+    a.priv = 0;
     a.pinned_pg = 0;
     a.ready_since = 0;
     a.f_gen = a.f_rec = a.f_obs = 0;
@@ -1541,7 +1565,6 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     a.f_has_tool = 0;
     a.in_active = 0;
     a.act_seq = 0;
-    a.pad0 = 0;
     a.ready = 0;
     ag[i] = a;
     D.pend[i] = i;

@@ -176,14 +176,21 @@ class Batch:
     """A set of independent simulations executed on one GPU in one launch."""
 
     def __init__(self, specs: list[SimSpec], device: int = 0, warps_per_sim: int = 0,
-                 log_capacity: int = 0, trace_capacity: int = 0, host_outputs: bool = False):
+                 log_capacity: int = 0, trace_capacity: int = 0, host_outputs: bool = False,
+                 verify: bool | None = None):
+        """verify: re-derive every prefix match with the block-hash probe and
+        check it against the incrementally held state (default: the
+        KVG_VERIFY environment variable; the GPU test suite sets it)."""
+        if verify is None:
+            verify = os.environ.get("KVG_VERIFY", "0") == "1"
         self.specs = specs
         if specs:
             self.descs = (abi.SimDesc * len(specs))(*[sp.desc for sp in specs])
         else:
             self.descs = (abi.SimDesc * 1)()
         opt = abi.BatchOptions(warps_per_sim=warps_per_sim, log_capacity=log_capacity,
-                               trace_capacity=trace_capacity, host_outputs=int(host_outputs))
+                               trace_capacity=trace_capacity, host_outputs=int(host_outputs),
+                               verify=int(bool(verify)))
         h = C.c_void_p()
         _check(lib().kvg_batch_create(device, self.descs, len(specs), C.byref(opt), C.byref(h)))
         self.h = h

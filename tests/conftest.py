@@ -7,6 +7,10 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if REPO not in sys.path:
     sys.path.insert(0, REPO)
 
+# every engine batch in the suite also re-derives each prefix match with the
+# block-hash probe (kernel 1) and checks the incrementally held prefix state
+os.environ.setdefault("KVG_VERIFY", "1")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (run with -m gpu)")
