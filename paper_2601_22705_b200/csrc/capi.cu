@@ -87,10 +87,18 @@ u64 xfer_ring(const kvg_sim_desc& d) {
 
 // Dynamic shared memory holding a small simulation's hot agent records,
 // event heap and ready bitmaps (leader.cuh engine_body); 0 = keep in HBM.
-size_t hot_smem(u64 n) {
-  if (n > 128) return 0;
+// The 1-warp kernel keeps up to 128 agents there (28 CTAs share an SM); the
+// big-sim kernel runs one CTA per SM and keeps up to ~200 KB of them (2,048
+// agents = 160 KB), so a lone C2 / C3 leader never leaves shared memory.
+constexpr size_t kBigSmemMax = 200 * 1024;
+size_t hot_smem_bytes(u64 n) {
   const u64 nwords = (n + 31) / 32;
   return n * (sizeof(kvg::AgentDev) + sizeof(kvg::HeapEnt)) + (nwords + (nwords + 31) / 32) * 4;
+}
+size_t hot_smem(u64 n, bool big = false) {
+  if (!big) return n > 128 ? 0 : hot_smem_bytes(n);
+  const size_t b = hot_smem_bytes(n);
+  return b <= kBigSmemMax ? b : 0;
 }
 
 }  // namespace

@@ -1512,8 +1512,8 @@ __device__ __forceinline__ void run_op(Op& op, Hist& h, int tid, int warp, int l
   }
 }
 
-// Agents whose hot records fit in shared memory (per-CTA dynamic smem).
-constexpr u32 kSmemAgents = 128;
+// Hot agent records / event heap / ready bitmaps go to dynamic shared memory
+// when the host sized it for them (capi.cu hot_smem).
 
 __device__ __forceinline__ size_t smem_bytes_for(u32 n) {
   const u32 nwords = (n + 31) / 32;
@@ -1534,7 +1534,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   if (tid == 0) {
     unsigned int dyn_bytes;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_bytes));
-    if (n <= kSmemAgents && smem_bytes_for(n) <= dyn_bytes) {
+    if (n > 0 && smem_bytes_for(n) <= dyn_bytes) {  // the host sized it (capi.cu hot_smem)
       L.ag = reinterpret_cast<AgentDev*>(dyn);
       L.heap = reinterpret_cast<HeapEnt*>(dyn + static_cast<size_t>(n) * sizeof(AgentDev));
       L.rbits = reinterpret_cast<u32*>(dyn + static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt)));
