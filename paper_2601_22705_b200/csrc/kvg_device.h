@@ -73,7 +73,7 @@ struct AgentDev {     // 64 B: two agents per 128 B line
   uint16_t step;
   uint8_t state, ev_kind, f_has_tool, in_active;
   uint8_t ready;      // mirror of this agent's bit in the ready bitmap
-  uint8_t stalled;    // last dispatch attempt stalled (predicts the retry)
+  uint8_t stalled;    // last dispatch attempt stalled
 };
 static_assert(sizeof(AgentDev) == 64, "AgentDev must stay 64 B");
 

@@ -81,7 +81,7 @@ struct Lead {
   unsigned long long n_trace, n_log;
   // dispatch context
   u32 batch_n, m_id, m_next, pad1;
-  u64 m_ctx0, m_f, m_nctx, m_nafter, m_now, m_k, m_e, m_stamp;
+  u64 m_ctx0, m_f, m_nctx, m_nafter, m_now, m_k, m_e;
   // hot per-agent structures: shared memory for small sims, else HBM
   AgentDev* ag;
   HeapEnt* heap;
@@ -898,7 +898,7 @@ __device__ __forceinline__ void member_success(const SimDev& D, Lead& L, u32 id,
   a.f_tool = plan.tool_latency;
   D.stats[id].wait_time += L.clock - a.ready_since;
   set_state(D, L, id, S_GEN);
-  a.stalled = 0;
+  a.stalled = 0;  // (stall bookkeeping, informational)
   ++L.agent_steps;
 }
 

@@ -25,6 +25,10 @@ elif which.startswith("c5s"):  # scaled C5 shape: c5s<agents>
     s = config.c5_stress("aimd", agents=ag, capacity=1)
     s.engine.capacity = config.scaled_capacity(engine.Population(s.workload, s.seed).peak_aggregate_tokens)
     specs = [engine.SimSpec.from_scenario(s)]
+elif which == "c3h":
+    s = config.c3_dsv3("aimd")
+    s.controller.h_thresh = 0.3
+    specs = [engine.SimSpec.from_scenario(s)]
 else:
     s = config.c3_dsv3("aimd", agents=int(which[3:]) if which[3:] else 2048)
     specs = [engine.SimSpec.from_scenario(s)]
