@@ -453,20 +453,87 @@ __device__ __noinline__ void on_tick(const SimDev& D, Lead& L) {
   sched_admission(L);
 }
 
+__device__ __forceinline__ void pause_one(const SimDev& D, Lead& L, u32 id) {
+  act_erase(D, L, id);
+  paus_push(D, L, id);
+  set_state(D, L, id, S_PAUSED);
+  ++D.stats[id].pause_events;
+}
+
+// Pauses the K ready agents with the largest admission sequence numbers, in
+// descending order (= K successive pause_victim calls). D.batch is free
+// scratch here (dispatch_batch has not started).
+__device__ __noinline__ void pause_top_k(const SimDev& D, Lead& L, u32 K) {
+  u64* h = reinterpret_cast<u64*>(D.batch);  // key = act_seq << 32 | id (seqs are unique)
+  u32 m = 0;
+  for (u32 id = ready_next(D, L, 0); id != NIL; id = ready_next(D, L, id + 1)) {
+    const u64 key = (static_cast<u64>(L.ag[id].act_seq) << 32) | id;
+    if (m < K) {  // min-heap of the K largest keys
+      u32 i = m++;
+      while (i > 0) {
+        const u32 p = (i - 1) >> 1;
+        if (h[p] <= key) break;
+        h[i] = h[p];
+        i = p;
+      }
+      h[i] = key;
+    } else if (key > h[0]) {
+      u32 i = 0;
+      for (;;) {
+        u32 c = 2 * i + 1;
+        if (c >= K) break;
+        if (c + 1 < K && h[c + 1] < h[c]) ++c;
+        if (h[c] >= key) break;
+        h[i] = h[c];
+        i = c;
+      }
+      h[i] = key;
+    }
+  }
+  // in-place heapsort: each pop moves the current minimum to the end of the
+  // shrinking heap, leaving h[0..m) in descending key order
+  for (u32 n = m; n > 0; --n) {
+    const u64 top = h[0], last = h[n - 1];
+    u32 i = 0;
+    for (;;) {
+      u32 c = 2 * i + 1;
+      if (c >= n - 1) break;
+      if (c + 1 < n - 1 && h[c + 1] < h[c]) ++c;
+      if (h[c] >= last) break;
+      h[i] = h[c];
+      i = c;
+    }
+    if (n > 1) h[i] = last;
+    h[n - 1] = top;
+  }
+  for (u32 k = 0; k < m; ++k) pause_one(D, L, static_cast<u32>(h[k] & 0xffffffffu));
+}
+
 // Controller::admission_pass (controller.cpp:124-160) with the commands
 // applied as Engine::on_admission_check does (engine.cpp:268-291). Commands
 // can be applied immediately: pausing only removes agents from active_ and
 // happens before any admit, which never reads agent state.
 __device__ __noinline__ void admission_pass(const SimDev& D, Lead& L) {
   const u64 limit = adm_limit(L);
-  if (L.gated) {
-    while (L.act_size > limit) {
-      const u32 id = pause_victim(D, L);
-      if (id == NIL) break;
-      act_erase(D, L, id);
-      paus_push(D, L, id);
-      set_state(D, L, id, S_PAUSED);
-      ++D.stats[id].pause_events;
+  if (L.gated && L.act_size > limit) {
+    // The reference pauses the newest at-boundary active agent until the
+    // limit holds or none is left: the victims are the ready agents in
+    // descending admission order, at most K of them. Few: scan per victim.
+    // Many (an AIMD cut in a big simulation): one gather + top-K selection
+    // instead of K scans (O(n_ready log K), not O(K n_ready)).
+    const u64 over = L.act_size - limit;
+    const u64 K = over < L.n_ready ? over : L.n_ready;
+#ifndef KVG_TOPK_MIN
+#define KVG_TOPK_MIN 3
+#endif
+    if (K < KVG_TOPK_MIN) {
+      while (L.act_size > limit) {
+        const u32 id = pause_victim(D, L);
+        if (id == NIL) break;
+        pause_one(D, L, id);
+      }
+    } else {
+      pause_top_k(D, L, static_cast<u32>(K));
     }
   }
   while (L.act_size < limit) {
@@ -1096,6 +1163,9 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
 }
 
 // Runs the state machine until a cooperative op is posted in `op`.
+// kOff = false compiles the discard-only state machine: no offload phases,
+// no tree code, a smaller hot loop for sweeps of discard-mode simulations.
+template <bool kOff>
 __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
   op.kind = OP_NONE;
   for (;;) {
@@ -1157,7 +1227,9 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           continue;
         }
         if (which == 2) {  // on_admission_check (engine.cpp:268-291)
+          PROF_MARK(L, 41);
           admission_pass(D, L);
+          PROF_MARK(L, PH_EVENT);
           if (L.n_ready == 0) {  // dispatch_batch with an empty ready set
             ++L.events;
             continue;
@@ -1172,7 +1244,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         AgentDev& a = L.ag[agent];
         if (kind == EV_GEN) {  // on_generation_complete (engine.cpp:184-222)
           L.makespan = L.makespan < L.clock ? L.clock : L.makespan;
-          if (!L.offload) {
+          if (!(kOff && L.offload)) {
             set_pinned(D, L, agent, 0);  // unpin(pinned_len) — implicit pins
           } else if (a.pinned_pg > 0) {  // engine.cpp:188-191 on the tree
             t_pin(D, L, agent, static_cast<u64>(a.pinned_pg) * L.ps, -1);
@@ -1187,7 +1259,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           ++a.step;
           if (a.step >= L.steps) {
             set_state(D, L, agent, S_DONE);
-            if (L.offload) {  // discard_suffix on the tree (device and host pages)
+            if (kOff && L.offload) {  // discard_suffix on the tree (device and host pages)
               op.freed = static_cast<unsigned int>(t_discard(D, L, agent, a.ctx, L.shared_len));
               op.err = E_NONE;
               L.phase = PH_GEN_DISCARDED;
@@ -1251,7 +1323,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       }
       // --------------------------------------------- dispatch_member (337-396)
       case PH_MEMBER: {
-        if (L.offload) {
+        if (kOff && L.offload) {
           L.phase = PH_O_MEMBER;
           continue;
         }
@@ -1453,7 +1525,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       case PH_GEN_DISCARDED: {
         if (op.err) fail(L, op.err);
         const u32 id = L.ev_agent;
-        if (!L.offload) {  // (the tree discard accounted for itself)
+        if (!(kOff && L.offload)) {  // (the tree discard accounted for itself)
           L.used -= op.freed;
           L.discarded += static_cast<u64>(op.freed) * L.ps;
           // pages from page_ceil(shared_len) on are gone (a straddling page stays, Q2)
@@ -1482,7 +1554,9 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       case PH_O_INSERT_EVICTED:
       case PH_O_INSERT_FAIL:
       case PH_O_EVICT_POP:
-        if (offload_step(D, L, op)) return;
+        if constexpr (kOff) {
+          if (offload_step(D, L, op)) return;
+        }
         continue;
       case PH_DONE:
         finalize(D, L);
@@ -1521,7 +1595,7 @@ __device__ __forceinline__ size_t smem_bytes_for(u32 n) {
          (nwords + (nwords + 31) / 32) * sizeof(u32);
 }
 
-template <int kDepth>
+template <int kDepth, bool kOff>
 __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   __shared__ Lead L;
   __shared__ Op op;
@@ -1585,7 +1659,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   }
 #endif
   for (;;) {
-    if (tid == 0) leader_step(D, L, op);
+    if (tid == 0) leader_step<kOff>(D, L, op);
     __syncthreads();
     if (op.kind == OP_EXIT) break;
     if (tid == 0) PROF_MARK(L, 32 + op.kind);
@@ -1616,12 +1690,17 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
 #define KVG_SMALL_MINB 28
 #endif
 __global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small(const SimDev* __restrict__ sims) {
-  engine_body<KVG_SMALL_DEPTH>(sims);
+  engine_body<KVG_SMALL_DEPTH, false>(sims);
+}
+
+// The same with the offload tier compiled in (batches holding offload sims).
+__global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small_off(const SimDev* __restrict__ sims) {
+  engine_body<KVG_SMALL_DEPTH, true>(sims);
 }
 
 // Latency variant: up to 32 warps cooperate on one big simulation.
 __global__ void __launch_bounds__(1024, 1) engine_kernel_big(const SimDev* __restrict__ sims) {
-  engine_body<8>(sims);
+  engine_body<8, true>(sims);
 }
 
 }  // namespace kvg

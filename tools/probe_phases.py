@@ -13,13 +13,15 @@ PH = ["EVENT", "MEMBER", "M_MATCHED", "M_INSERT", "M_EVICTED", "M_COMMIT", "M_CR
 names = {i: "leader:" + n for i, n in enumerate(PH)}
 names.update({32 + k: "coop:" + n for k, n in enumerate(
     ["NONE", "EXIT", "RANGE", "EVICT", "REBUILD", "SCANFREE", "FRONTIER", "TICKS"])})
-names.update({40: "fast_housekeeping", 46: "leader_step entry+sync", 47: "init/finalize"})
+names.update({41: "admission_pass", 40: "fast_housekeeping", 46: "leader_step entry+sync", 47: "init/finalize"})
 which = sys.argv[1] if len(sys.argv) > 1 else "c4"
 if which == "c4":
     pop = engine.Population(config.c1_toy().workload, 42)
     specs = [engine.SimSpec.from_scenario(s, population=pop) for s in config.c4_sweep()]
 elif which == "c2":
     specs = [engine.SimSpec.from_scenario(config.c2_qwen("aimd"))]
+elif which == "c5":
+    specs = [engine.SimSpec.from_scenario(config.c5_stress("aimd"))]
 elif which.startswith("c5s"):  # scaled C5 shape: c5s<agents>
     ag = int(which[3:])
     s = config.c5_stress("aimd", agents=ag, capacity=1)
@@ -35,9 +37,8 @@ else:
 lib = engine.lib()
 lib.kvg_debug_profile.argtypes = [C.POINTER(C.c_ulonglong)]
 b = engine.Batch(specs)
-b.run()
 buf = (C.c_ulonglong * 48)()
-lib.kvg_debug_profile(buf)  # clear (first run)
+lib.kvg_debug_profile(buf)  # clear
 b.run()
 lib.kvg_debug_profile(buf)
 tot = sum(buf)
