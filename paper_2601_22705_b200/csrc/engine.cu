@@ -472,6 +472,20 @@ __device__ __forceinline__ u32 ge_mask(u64 base, u64 thr) {  // slots with page 
   return d >= 32 ? 0u : (FULL << d);
 }
 
+__device__ __forceinline__ u32 lt_mask(u64 base, u64 lim) {  // slots with page index < lim
+  if (lim <= base) return 0u;
+  const u64 d = lim - base;
+  return d >= 32 ? FULL : ((1u << d) - 1u);
+}
+
+// Engine mode: a private chain's pages at or beyond its held length (the
+// finished agent's discarded suffix) are absent even if still in the table.
+__device__ __forceinline__ u32 held_mask(const Op& op, u64 tag) {
+  const u64 owner = tag >> 32;
+  if (owner == 0) return FULL;
+  return lt_mask(tag & 0xffffffffull, op.shared_pages + op.agents[owner - 1].priv);
+}
+
 __device__ __forceinline__ u64 pin_thr(const Op& op, u64 owner) {
   // plain load: the records may live in shared memory (the leader wrote them
   // before the barrier that started this op)
@@ -483,7 +497,7 @@ __device__ __forceinline__ u64 pin_thr(const Op& op, u64 owner) {
 // is pinned iff idx < its owner's pinned prefix.
 __device__ __forceinline__ u32 cand_of(const Op& op, const Summ& e) {
   if (!op.implicit_pins) return e.dev;  // explicit pins make a bucket mixed
-  return e.dev & ge_mask(e.tag & 0xffffffffull, pin_thr(op, e.tag >> 32));
+  return e.dev & ge_mask(e.tag & 0xffffffffull, pin_thr(op, e.tag >> 32)) & held_mask(op, e.tag);
 }
 
 // Stamp of a summarised bucket's resident pages. Engine mode: every
@@ -742,17 +756,16 @@ __device__ __noinline__ void coop_rebuild(Op& op, int tid, int warp, int lane, i
   for (u32 i = warp; i < n_occ; i += nw) {
     const u32 b = __ldcg(&op.occ[i]);
     const Slot s = ld_slot(&op.table[(size_t)b * kChunk + lane]);
-    if (!__any_sync(FULL, (s.meta & kResident) != 0)) continue;
     const u64 tag = __shfl_sync(FULL, s.key, 0);
+    // engine mode: pages beyond their chain's held length are not copied
+    const bool live = (s.meta & kResident) != 0 &&
+                      (!op.implicit_pins || ((held_mask(op, tag) >> lane) & 1u));
+    if (!__any_sync(FULL, live)) continue;
     u32 nb = static_cast<u32>(hash64(tag)) & op.mask;
     nb = claim(op.alt, op.alt_summ, op.alt_occ, &op.alt_n, op.mask, tag, nb, lane);
-    __stcg(&op.alt[(size_t)nb * kChunk + lane].meta, s.meta);
-    if (lane == 0) {
-      const ulonglong2* src = reinterpret_cast<const ulonglong2*>(&op.summ[b]);
-      ulonglong2* dst = reinterpret_cast<ulonglong2*>(&op.alt_summ[nb]);
-      __stcg(dst, __ldcg(src));
-      __stcg(dst + 1, __ldcg(src + 1));
-    }
+    const u64 m = live ? s.meta : 0ull;
+    __stcg(&op.alt[(size_t)nb * kChunk + lane].meta, m);
+    summ_write(op.alt_summ, nb, m, lane);
   }
   __syncthreads();
   if (tid == 0) {

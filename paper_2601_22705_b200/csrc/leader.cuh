@@ -1265,16 +1265,17 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
               L.phase = PH_GEN_DISCARDED;
               continue;
             }
-            // discard_suffix(context, shared_len) (cache_tree.cpp:404-437):
-            // page_ceil(shared_len) keeps a straddling page (quirk Q2)
-            const u64 fp = (L.shared_len + L.ps - 1) / L.ps;
-            const u64 np = a.ctx / L.ps;
-            if (fp * L.ps < a.ctx && fp < np) {
-              post_range(op, agent, fp, np, RF_FREE, 0, 0);
-              L.phase = PH_GEN_DISCARDED;
-              return;
+            // discard_suffix(context, shared_len) (cache_tree.cpp:404-437) on
+            // the held state: the finished agent's private pages from
+            // page_ceil(shared_len) on leave the cache (a straddling page
+            // stays, quirk Q2). Its chain only shrinks to `keep`; the pages
+            // left in the table beyond a chain's held length are absent to
+            // every reader (eviction candidates, rehash).
+            {
+              const u64 fp = (L.shared_len + L.ps - 1) / L.ps;
+              const u64 keep = fp > L.S ? fp - L.S : 0;
+              op.freed = a.priv > keep ? static_cast<unsigned int>(a.priv - keep) : 0u;
             }
-            op.freed = 0;
             op.err = E_NONE;
             L.phase = PH_GEN_DISCARDED;
             continue;
