@@ -334,17 +334,24 @@ def run_b200(args):
     h2d = sum(p.c.agents * p.c.steps * C.sizeof(abi.StepPlan) for p in pops.values()) + \
         len(specs) * 512
     d2h = 0
+    phases = {"create_ms": 0.0, "run_ms": 0.0, "results_ms": 0.0}
     for k in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         b2 = engine.Batch(specs, device=device, host_outputs=True)
+        t1 = time.perf_counter()
         b2.run()
+        t2 = time.perf_counter()
         res2 = b2.results_array()
         d2h = int(res2["ticks"].sum()) * C.sizeof(abi.TraceRow) + \
             n_agents * C.sizeof(abi.AgentStats) + len(res2) * C.sizeof(abi.SimResult)
         b2.close()
+        t3 = time.perf_counter()
         if k > 0:  # step 0 is the untimed warm-up (first pinned allocation)
-            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+            e2e_ms.append(1e3 * (t3 - t0))
+            phases["create_ms"] += 1e3 * (t1 - t0) / args.e2e_steps
+            phases["run_ms"] += 1e3 * (t2 - t1) / args.e2e_steps
+            phases["results_ms"] += 1e3 * (t3 - t2) / args.e2e_steps
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -378,7 +385,8 @@ def run_b200(args):
             "lookups_per_s": all_lookups * args.steps / (max_ms / 1e3),
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "phases_ms": {k: round(v, 2) for k, v in phases.items()}},
             "gpu_launches": args.steps * launches_per_step(specs),
             "clocks": sampler.summary(),
             "parity": {"sims": len(summary), "nonzero_status": len(bad),

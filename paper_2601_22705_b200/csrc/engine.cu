@@ -478,12 +478,18 @@ __device__ __forceinline__ u32 lt_mask(u64 base, u64 lim) {  // slots with page 
   return d >= 32 ? FULL : ((1u << d) - 1u);
 }
 
-// Engine mode: a private chain's pages at or beyond its held length (the
-// finished agent's discarded suffix) are absent even if still in the table.
+// Engine mode: a finished agent's private pages at or beyond its held length
+// (the discarded suffix) are absent even if still in the table. Only finished
+// agents hold such pages (evictions free pages physically), and their held
+// length is at most one page past the shared prompt, so the eviction
+// scatter's concurrent atomicMin on live agents' lengths never feeds back
+// into a candidate mask.
 __device__ __forceinline__ u32 held_mask(const Op& op, u64 tag) {
   const u64 owner = tag >> 32;
   if (owner == 0) return FULL;
-  return lt_mask(tag & 0xffffffffull, op.shared_pages + op.agents[owner - 1].priv);
+  const AgentDev& a = op.agents[owner - 1];
+  if (a.state != S_DONE) return FULL;
+  return lt_mask(tag & 0xffffffffull, op.shared_pages + a.priv);
 }
 
 __device__ __forceinline__ u64 pin_thr(const Op& op, u64 owner) {
