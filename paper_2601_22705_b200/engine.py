@@ -21,6 +21,7 @@ from . import abi
 from .config import Scenario
 
 _lib = None
+_RESULT_DTYPE = None
 
 
 class EngineError(RuntimeError):
@@ -222,10 +223,14 @@ class Batch:
 
     def results_array(self) -> np.ndarray:
         """Every simulation's result as one numpy structured array (no
-        per-simulation Python objects)."""
-        arr = (abi.SimResult * max(1, self.n))()
-        _check(lib().kvg_batch_results(self.h, arr, self.n))
-        return np.ctypeslib.as_array(arr)[: self.n]
+        per-simulation Python objects; the dtype is built once)."""
+        global _RESULT_DTYPE
+        if _RESULT_DTYPE is None:
+            _RESULT_DTYPE = np.ctypeslib.as_array((abi.SimResult * 1)()).dtype
+        out = np.empty(max(1, self.n), dtype=_RESULT_DTYPE)
+        _check(lib().kvg_batch_results(self.h, out.ctypes.data_as(C.POINTER(abi.SimResult)),
+                                       self.n))
+        return out[: self.n]
 
     def trace(self, i: int) -> list[dict]:
         n = C.c_size_t()
