@@ -73,6 +73,7 @@ enum OpKind : int {
   OP_SCANFREE,   // free pages by (owner, min index) over the whole table
   OP_FRONTIER,   // offload tree: compact eviction-frontier nodes (tree.cuh)
   OP_TICKS,      // warp 0: pipelined control ticks + no-op admission checks
+  OP_PHASES,     // warp 0: phase labels over the trace rows
 };
 
 enum RangeFlags : u32 {

@@ -52,6 +52,7 @@ enum Phase : int {
   PH_O_INSERT_FAIL,
   PH_O_EVICT_POP,
   PH_DONE,
+  PH_FINAL,
   PH_EXITED,
 };
 
@@ -66,6 +67,8 @@ struct Lead {
   u64 used, cclock, discarded, lookups, agent_steps, events, evict_calls, evicted;
   u64 pin_max, pin_priv;  // implicit pins: shared prefix max, private pinned pages
   u64 L0, lazy_sh;        // discard mode: resident shared pages, their stamp
+  kvg_phase_label ph[3];  // classify_phases result (coop_phases)
+  u32 n_ph, pad5;
   int verify, pad4;
   u64 hit_pages, created_pages, refreshed_pages, evict_scanned, agent_events;
   long long t_start;
@@ -554,7 +557,8 @@ __device__ __noinline__ void admission_pass(const SimDev& D, Lead& L) {
 __device__ __noinline__ void finalize(const SimDev& D, Lead& L) {
   kvg_sim_result* r = D.result;
   r->status = L.status;
-  r->n_phases = 0;
+  r->n_phases = L.n_ph;  // classify_phases (metrics.cpp:41-81), coop_phases
+  for (u32 k = 0; k < 3; ++k) r->phases[k] = L.ph[k];
   r->ledger = L.ledger;
   r->makespan = L.makespan < L.pcie_busy ? L.pcie_busy : L.makespan;  // engine.cpp:400
   r->device_busy = L.device_busy;
@@ -821,7 +825,7 @@ __device__ __forceinline__ bool ticks_apply(const Lead& L) {
   if (L.kind == KVG_POLICY_AIMD && L.cfg.signal_smoothing > 0) return false;
   const double t_agent = L.hsize > 0 ? L.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
   return L.tick_t < t_agent && !(L.tick_t > L.horizon) &&
-         L.tick_t + 4.0 * L.interval < t_agent;  // enough ticks to pay for the op
+         L.tick_t + 3.0 * L.interval < t_agent;  // >= 4 ticks: cheaper than the scalar loop
 }
 
 // OP_TICKS (warp 0): the same event sequence as fast_housekeeping — control
@@ -854,18 +858,24 @@ __device__ __noinline__ void coop_ticks(const SimDev& D, Lead& L, int lane) {
   bool done = false, adm_pending = false;
   double clock = L.clock;
   while (!done) {
+    // ticks that can precede the next agent event this round (an upper
+    // bound: validity is still checked per lane), so short runs do not pay
+    // for 32 chain steps
+    const double span = (t_agent - t0) / interval;
+    const int kmax = span >= 30.0 ? 32 : static_cast<int>(span) + 2;
     // lane k: tick k's time and hit window (sequential chains, exact order)
     double t = t0, m = m0, r = r0;
-    for (int i = 0; i < lane; ++i) {
+    const int steps = lane < kmax ? lane : kmax;
+    for (int i = 0; i < steps; ++i) {
       t = t + interval;
       m = m * decay;
       r = r * decay;
     }
     const double hit = r > 0 ? m / r : 1.0;
-    const bool in_time = t < t_agent && !(t > horizon);
+    const bool in_time = lane < kmax && t < t_agent && !(t > horizon);
     // window recurrence, every lane in lockstep; lane k keeps w_k
     double wk = w;
-    for (int k = 0; k < 32; ++k) {
+    for (int k = 0; k < kmax; ++k) {
       const double h = __shfl_sync(FULL, hit, k);
       if (kind == KVG_POLICY_AIMD) {
         double x = w;
@@ -936,6 +946,66 @@ __device__ __noinline__ void coop_ticks(const SimDev& D, Lead& L, int lane) {
     L.events = events;
     L.ticks = ticks;
     L.n_trace = n_trace;
+  }
+}
+
+// classify_phases (metrics.cpp:41-81, called by finish_result,
+// engine.cpp:413) over this simulation's own trace rows, on warp 0: rows are
+// read 32 at a time (one per lane) and reduced to a hot-tick ballot; lane 0
+// walks the bits. Warmup until the first saturated cache-cold tick, middle
+// until `hysteresis` consecutive ticks leave that state, then cooldown.
+__device__ __noinline__ void coop_phases(const SimDev& D, Lead& L, int lane) {
+  const kvg_phase_params& pp = D.engine.phases;
+  const double mk = L.makespan < L.pcie_busy ? L.pcie_busy : L.makespan;
+  const u64 n = L.n_trace < D.trace_cap ? L.n_trace : D.trace_cap;
+  u32 np = 0;
+  kvg_phase_label ph[3];
+  if (mk > 0) {
+    u64 enter = n, leave = n;  // first hot row; row that ends the middle
+    int bad = 0;
+    for (u64 base = 0; base < n && leave == n; base += 32) {
+      const u64 i = base + lane;
+      bool hot = false;
+      if (i < n) {
+        const kvg_trace_row& r = D.trace[i];
+        hot = r.usage >= pp.sat_threshold && r.hit_rate < pp.hit_threshold;
+      }
+      const unsigned m = __ballot_sync(FULL, hot);
+      if (lane == 0) {
+        const u32 cnt = n - base < 32 ? static_cast<u32>(n - base) : 32u;
+        for (u32 k = 0; k < cnt; ++k) {
+          const bool h = (m >> k) & 1u;
+          if (enter == n) {
+            if (h) enter = base + k;
+            continue;
+          }
+          if (h) {
+            bad = 0;
+            continue;
+          }
+          if (++bad >= pp.hysteresis) {
+            leave = base + k + 1 - static_cast<u64>(pp.hysteresis);
+            break;
+          }
+        }
+      }
+      leave = __shfl_sync(FULL, leave, 0);
+    }
+    if (lane == 0) {
+      if (enter == n) {
+        ph[np++] = kvg_phase_label{KVG_PHASE_WARMUP, 0, 0.0, mk};
+      } else {
+        const double ms = D.trace[enter].time;
+        const double me = leave < n ? D.trace[leave].time : mk;
+        if (ms > 0) ph[np++] = kvg_phase_label{KVG_PHASE_WARMUP, 0, 0.0, ms};
+        ph[np++] = kvg_phase_label{KVG_PHASE_MIDDLE, 0, ms, me};
+        if (me < mk) ph[np++] = kvg_phase_label{KVG_PHASE_COOLDOWN, 0, me, mk};
+      }
+    }
+  }
+  if (lane == 0) {
+    L.n_ph = np;
+    for (u32 k = 0; k < 3; ++k) L.ph[k] = k < np ? ph[k] : kvg_phase_label{0, 0, 0.0, 0.0};
   }
 }
 
@@ -1559,7 +1629,11 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           if (offload_step(D, L, op)) return;
         }
         continue;
-      case PH_DONE:
+      case PH_DONE:  // phase labels over the trace rows (warp 0), then the result
+        op.kind = OP_PHASES;
+        L.phase = PH_FINAL;
+        return;
+      case PH_FINAL:
         finalize(D, L);
         L.phase = PH_EXITED;
         op.kind = OP_EXIT;
@@ -1666,6 +1740,8 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     if (tid == 0) PROF_MARK(L, 32 + op.kind);
     if (op.kind == OP_TICKS) {
       if (warp == 0) coop_ticks(D, L, lane);
+    } else if (op.kind == OP_PHASES) {
+      if (warp == 0) coop_phases(D, L, lane);
     } else {
       run_op<kDepth>(op, h, tid, warp, lane, nw);
     }
