@@ -67,7 +67,7 @@ def build_scenarios(workload: str, rank: int, sims: int):
         desc = ("C3: DeepSeek-V3 MLA sizing, 2048 agents x 10 steps, 613,697-page cache, "
                 "aimd h_thresh=0.3")
     elif workload == "c3off":
-        desc = ("C3 shape, offload tier: 128 agents x 10 steps, scaled cache (peak/1.5), "
+        desc = ("C3 shape, offload tier: 32 agents x 10 steps, scaled cache (peak/1.5), "
                 "uncontrolled admission + offload eviction (PCIe 25 GB/s link model)")
     else:
         desc = "C1 toy: 64 agents x 10 steps, aimd"
@@ -179,16 +179,8 @@ def load_traffic(workload):
 
 
 def cpu_sample(workload: str, scen):
-    """Bounded CPU sample of a workload: the offload tier's 128-agent C3 shape
-    takes ~3 min in the reference, so its sample is the 32-agent shape
-    (agent-steps/s is per-step throughput either way)."""
-    if workload != "c3off":
-        return scen, None
-    from paper_2601_22705_b200 import config, engine
-    s = config.c3_dsv3("offload", agents=32, capacity=1)
-    s.engine.capacity = config.scaled_capacity(
-        engine.Population(s.workload, s.seed).peak_aggregate_tokens)
-    return [s], "C3 shape with 32 agents (offload tier), scaled cache"
+    """Bounded CPU sample of a workload (all current workloads run whole)."""
+    return scen, None
 
 
 def cpu_reference(scen, threads: int, sample_every: int = 1):

@@ -219,15 +219,18 @@ __device__ __forceinline__ bool probe_from(const Op& op, u64 tag, u32 b, int lan
 // Claims an empty bucket for `tag`, starting at bucket `b`; returns it. The
 // bucket's summary starts empty.
 __device__ __noinline__ u32 claim(Slot* table, Summ* summ, u32* occ, unsigned int* occ_n,
-                                  u32 mask, u64 tag, u32 b, int lane) {
+                                  u32 mask, u64 tag, u32 b, int lane, bool seen_empty = false) {
   for (;;) {
     int won = 0;
     if (lane == 0) {
-      u64 k0 = __ldcg(&table[(size_t)b * kChunk].key);
+      // the probe that led here already saw bucket b empty: go straight to
+      // the CAS (one DRAM round trip less); a lost race falls back to the scan
+      const u64 k0 = seen_empty ? kEmptyKey : __ldcg(&table[(size_t)b * kChunk].key);
       if (k0 == kEmptyKey)
         won = atomicCAS(reinterpret_cast<unsigned long long*>(&table[(size_t)b * kChunk].key),
                         kEmptyKey, tag) == kEmptyKey;
     }
+    seen_empty = false;
     won = __shfl_sync(FULL, won, 0);
     if (won) {
       Slot* s = &table[(size_t)b * kChunk + lane];
@@ -263,7 +266,7 @@ __device__ __forceinline__ void range_chunk(Op& op, u64 tag, u64 lo, u64 hi, u32
   const u64 page = (tag & 0xffffffffull) + lane;
   const bool in = page >= lo && page < hi;
   if (!found && (flags & RF_CREATE) && __any_sync(FULL, in)) {
-    b = claim(op.table, op.summ, op.occ, &op.occ_n, op.mask, tag, b, lane);
+    b = claim(op.table, op.summ, op.occ, &op.occ_n, op.mask, tag, b, lane, true);
     found = true;
     s = Slot{tag + lane, 0};
   }

@@ -9,10 +9,10 @@ from paper_2601_22705_b200 import config, engine  # noqa: E402
 PH = ["EVENT", "MEMBER", "M_MATCHED", "M_INSERT", "M_EVICTED", "M_COMMIT", "M_CREATED", "M_FAIL",
       "M_RESTORED", "BATCH_END", "GEN_DISCARDED", "O_MEMBER", "O_RELOAD_CHUNK",
       "O_RELOAD_EVICTED", "O_RELOAD_END", "O_INSERT_START", "O_INSERT_COUNT",
-      "O_INSERT_EVICTED", "O_INSERT_FAIL", "O_EVICT_POP", "DONE", "EXITED"]
+      "O_INSERT_EVICTED", "O_INSERT_FAIL", "O_EVICT_POP", "DONE", "FINAL", "EXITED"]
 names = {i: "leader:" + n for i, n in enumerate(PH)}
 names.update({32 + k: "coop:" + n for k, n in enumerate(
-    ["NONE", "EXIT", "RANGE", "EVICT", "REBUILD", "SCANFREE", "FRONTIER", "TICKS"])})
+    ["NONE", "EXIT", "RANGE", "EVICT", "REBUILD", "SCANFREE", "FRONTIER", "TICKS", "PHASES"])})
 names.update({41: "admission_pass", 40: "fast_housekeeping", 46: "leader_step entry+sync", 47: "init/finalize"})
 which = sys.argv[1] if len(sys.argv) > 1 else "c4"
 if which == "c4":
