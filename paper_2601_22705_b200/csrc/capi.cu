@@ -102,6 +102,18 @@ size_t hot_smem(u64 n, bool big = false) {
   return b <= kBigSmemMax ? b : 0;
 }
 
+// Big-kernel offload sims also keep the tree's walk mirror (tree.cuh tw) in
+// the shared memory the hot records leave free: node ids [0, k) for the
+// largest k that fits (leader.cuh engine_body derives k the same way).
+size_t big_smem(const kvg_sim_desc& d) {
+  const size_t hot = hot_smem(d.population->agents, true);
+  const u64 tn = tree_nodes(d);
+  if (tn == 0) return hot;
+  const size_t base = (hot + 15) / 16 * 16;
+  const size_t room = kBigSmemMax > base ? kBigSmemMax - base : 0;
+  return base + std::min<size_t>(room / sizeof(kvg::TWalk) * sizeof(kvg::TWalk), tn * sizeof(kvg::TWalk));
+}
+
 }  // namespace
 
 #include "capi_batch.inc"
@@ -161,7 +173,8 @@ KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity, uint64_t page
     const u64 hslots = next_pow2(4 * tcap);
     const u64 logcap = 2 * capacity + 64;
     const u64 bytes = align_up(kvg_tree_seam::state_bytes()) + align_up(tcap * sizeof(kvg::TNodeDev)) +
-                      3 * align_up(tcap * 4) + align_up(tcap * sizeof(kvg::FrEnt)) +
+                      align_up(tcap * sizeof(kvg::TWalk)) + 2 * align_up(tcap * 4) +
+                      align_up(tcap * sizeof(kvg::FrEnt)) +
                       align_up(hslots * 8) + align_up(hslots * 4) +
                       align_up(logcap * sizeof(kvg_log_record)) + 256;
     CUDA_TRY(cudaMalloc(&c->mem, bytes));
@@ -176,10 +189,11 @@ KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity, uint64_t page
     std::memset(&sim, 0, sizeof sim);
     sim.tnodes = reinterpret_cast<kvg::TNodeDev*>(p);
     p += align_up(tcap * sizeof(kvg::TNodeDev));
+    sim.twalk = reinterpret_cast<kvg::TWalk*>(p);
+    p += align_up(tcap * sizeof(kvg::TWalk));
     sim.tfree = reinterpret_cast<u32*>(p);
     p += align_up(tcap * 4);
     sim.tstack = reinterpret_cast<u32*>(p);
-    p += align_up(tcap * 4);
     p += align_up(tcap * 4);
     sim.fr = reinterpret_cast<kvg::FrEnt*>(p);
     p += align_up(tcap * sizeof(kvg::FrEnt));

@@ -95,6 +95,17 @@ struct TNodeDev {
 };
 static_assert(sizeof(TNodeDev) == 64, "TNodeDev must stay 64 B");
 
+// Mirror of the node fields the path walks read (find_child / common_len /
+// host / pin): 20 B per node, kept in shared memory for the low node ids (the
+// pool reuses freed ids first) and in HBM above. TNodeDev stays
+// authoritative; every write of a mirrored field writes both (tree.cuh).
+struct TWalk {
+  u32 first_child, start, npages;
+  u32 tailh;  // tail | host << 31
+  int pin_count;
+};
+static_assert(sizeof(TWalk) == 20, "TWalk must stay 20 B");
+
 struct FrEnt {  // eviction frontier heap entry: (last_access, ordinal) order
   u64 la, ord;
   u32 id, pad;
@@ -147,6 +158,7 @@ struct SimDev {
   u32* hist;          // [2 * 512]: eviction radix-select histogram scratch
   // ---- offload-mode tree (unused, 1-element regions, in discard mode)
   TNodeDev* tnodes;   // [tcap] node pool, node 0 = root
+  TWalk* twalk;       // [tcap] walk mirror for ids past the shared-memory part
   u32* tfree;         // [tcap] free-node stack
   u32* tstack;        // [tcap] DFS stack (subtree walks)
   FrEnt* fr;          // [tcap] frontier heap

@@ -99,6 +99,8 @@ struct Lead {
   int offload, o_full, o_then, pad3;
   u32 t_alloc, t_free_n, x_head, x_size, o_node, o_c;
   u64 t_next_ord, offloaded, reloaded;
+  TWalk* tw_s;  // walk mirror of node ids [0, tw_n) in shared memory (tree.cuh tw)
+  u32 tw_n, tw_pad;
   double pcie_busy, link_busy;
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
 #ifdef KVG_PROFILE
@@ -1068,12 +1070,13 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
           return false;
         }
         const u32 c = t_find_child(D, L, L.o_node, id, L.o_pos / L.ps, n);
-        if (c == 0 || !N[c].host) {
+        if (c == 0 || !tw_is_host(*tw(D, L, c))) {
           L.phase = PH_O_RELOAD_END;
           return false;
         }
         u64 ka = t_common(D, L, c, id, L.o_pos / L.ps, n);
-        bool full = ka == N[c].npages;
+        const u32 np = tw(D, L, c)->npages;
+        bool full = ka == np;
         const u64 want = (L.o_hm - L.o_promoted) / L.ps;
         if (ka > want) {
           ka = want;
@@ -1083,7 +1086,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
           L.phase = PH_O_RELOAD_END;
           return false;
         }
-        if (ka < N[c].npages) t_split(D, L, c, ka);
+        if (ka < np) t_split(D, L, c, ka);
         L.o_c = c;
         L.o_ka = ka;
         L.o_full = full;
@@ -1097,6 +1100,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
       }
       const u32 c = L.o_c;
       N[c].host = 0;
+      tw_host(D, L, c, 0);
       N[c].device_slots = static_cast<u32>(L.o_ka);
       N[c].last_access = L.o_now;
       L.used += L.o_ka;
@@ -1212,15 +1216,18 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
         L.phase = PH_O_RELOAD_END;
         return false;
       }
+      const TWc W = tw_ctx(D, L);
+      const u64 mp = matched / L.ps;  // matched is whole pages
       u32 node = 0;
-      u64 pos = 0;
-      while (pos < matched) {
-        const u32 c = t_find_child(D, L, node, nid, pos / L.ps, L.m_nctx);
-        if (c == 0 || pos + static_cast<u64>(N[c].npages) * L.ps > matched) {
+      u64 pp = 0;
+      while (pp < mp) {
+        const u32 c = w_find_child(D, W, node, nid, pp, L.m_nctx);
+        const u64 np = c == 0 ? 0 : twp(W, c)->npages;
+        if (c == 0 || pp + np > mp) {
           fail(L, E_OFFLOAD);
           return false;
         }
-        pos += static_cast<u64>(N[c].npages) * L.ps;
+        pp += np;
         node = c;
       }
       L.o_now = ++L.cclock;
@@ -1683,7 +1690,9 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   if (tid == 0) {
     unsigned int dyn_bytes;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_bytes));
+    size_t used = 0;
     if (n > 0 && smem_bytes_for(n) <= dyn_bytes) {  // the host sized it (capi.cu hot_smem)
+      used = (smem_bytes_for(n) + 15) / 16 * 16;
       L.ag = reinterpret_cast<AgentDev*>(dyn);
       L.heap = reinterpret_cast<HeapEnt*>(dyn + static_cast<size_t>(n) * sizeof(AgentDev));
       L.rbits = reinterpret_cast<u32*>(dyn + static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt)));
@@ -1694,6 +1703,11 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
       L.rbits = D.rbits;
       L.rl1 = D.rl1;
     }
+    // offload: the tree's walk mirror takes the rest (capi.cu big_smem)
+    const size_t room = used < dyn_bytes ? (dyn_bytes - used) / sizeof(TWalk) : 0;
+    L.tw_s = reinterpret_cast<TWalk*>(dyn + used);
+    L.tw_n = kOff && D.engine.eviction == KVG_EVICT_OFFLOAD
+                 ? static_cast<u32>(room < D.tcap ? room : D.tcap) : 0;
   }
   __syncthreads();
   AgentDev* const ag = L.ag;

@@ -21,9 +21,45 @@ __device__ __forceinline__ u64 t_key(const Lead& L, u32 a, u64 k) {
 __device__ __forceinline__ u64 t_nkey(const Lead& L, const TNodeDev& n, u64 k) {
   return ((k < L.S ? 0ull : static_cast<u64>(n.tail)) << 32) | k;
 }
+__device__ __forceinline__ u64 t_wkey(const Lead& L, const TWalk& w, u64 k) {
+  return ((k < L.S ? 0ull : static_cast<u64>(w.tailh & 0x7fffffffu)) << 32) | k;
+}
 __device__ __forceinline__ bool t_subdev(const TNodeDev& n) {
   return n.device_slots > 0 || n.cwd > 0;
 }
+
+// ------------------------------------------------------------ walk mirror
+
+__device__ __forceinline__ TWalk* tw(const SimDev& D, const Lead& L, u32 id) {
+  return id < L.tw_n ? L.tw_s + id : D.twalk + id;
+}
+__device__ __forceinline__ void tw_put(const SimDev& D, const Lead& L, u32 id, const TNodeDev& n) {
+  TWalk* w = tw(D, L, id);
+  w->first_child = n.first_child;
+  w->start = n.start;
+  w->npages = n.npages;
+  w->tailh = n.tail | (n.host ? 0x80000000u : 0u);
+  w->pin_count = n.pin_count;
+}
+__device__ __forceinline__ void tw_host(const SimDev& D, const Lead& L, u32 id, u32 host) {
+  TWalk* w = tw(D, L, id);
+  w->tailh = (w->tailh & 0x7fffffffu) | (host ? 0x80000000u : 0u);
+}
+__device__ __forceinline__ bool tw_is_host(const TWalk& w) { return (w.tailh >> 31) != 0; }
+
+// The walk loops keep the mirror's placement and the shared-prompt bound in
+// registers (stores through generic pointers would otherwise force the Lead
+// fields to be re-read from shared memory on every level).
+struct TWc {
+  TWalk* s;
+  TWalk* g;
+  u32 n, pad;
+  u64 S;
+};
+__device__ __forceinline__ TWc tw_ctx(const SimDev& D, const Lead& L) {
+  return TWc{L.tw_s, D.twalk, L.tw_n, 0, L.S};
+}
+__device__ __forceinline__ TWalk* twp(const TWc& W, u32 id) { return id < W.n ? W.s + id : W.g + id; }
 
 __device__ u32 h_find(const SimDev& D, u64 key) {
   u32 i = static_cast<u32>(hash64(key)) & D.hmask;
@@ -68,38 +104,62 @@ __device__ u32 t_alloc(const SimDev& D, Lead& L) {
   return L.t_alloc++;
 }
 
-__device__ void t_add_child(const SimDev& D, u32 p, u32 c) {
+__device__ void t_add_child(const SimDev& D, const Lead& L, u32 p, u32 c) {
   TNodeDev* N = D.tnodes;
   N[c].parent = p;
   N[c].prev_sib = 0;
   N[c].next_sib = N[p].first_child;
   if (N[p].first_child) N[N[p].first_child].prev_sib = c;
   N[p].first_child = c;
+  tw(D, L, p)->first_child = c;
 }
-__device__ void t_remove_child(const SimDev& D, u32 p, u32 c) {
+__device__ void t_remove_child(const SimDev& D, const Lead& L, u32 p, u32 c) {
   TNodeDev* N = D.tnodes;
-  if (N[c].prev_sib) N[N[c].prev_sib].next_sib = N[c].next_sib;
-  else N[p].first_child = N[c].next_sib;
+  if (N[c].prev_sib) {
+    N[N[c].prev_sib].next_sib = N[c].next_sib;
+  } else {
+    N[p].first_child = N[c].next_sib;
+    tw(D, L, p)->first_child = N[c].next_sib;
+  }
   if (N[c].next_sib) N[N[c].next_sib].prev_sib = N[c].prev_sib;
 }
 
 // find_child (cache_tree.cpp:56-66): a full page of the sequence is needed.
-__device__ u32 t_find_child(const SimDev& D, const Lead& L, u32 node, u32 a, u64 p, u64 n_full) {
+// Eviction tail-splits make the paths hundreds of nodes deep, nearly all of
+// them single-child links, so the first child is tried before the hash: one
+// dependent load per level instead of three. A node's children have distinct
+// head keys (the reference's per-node map), so a first child whose head key
+// matches IS the child; otherwise the head-key hash decides as before.
+__device__ __forceinline__ u32 w_find_child(const SimDev& D, const TWc& W, u32 node, u32 a, u64 p,
+                                             u64 n_full) {
   if (p >= n_full) return 0;
-  const u32 c = h_find(D, t_key(L, a, p));
+  const u64 owner = p < W.S ? 0ull : static_cast<u64>(a) + 1;
+  const u32 c0 = twp(W, node)->first_child;
+  if (c0 != 0) {
+    const TWalk* x = twp(W, c0);
+    const u32 st = x->start;
+    const u64 xo = st < W.S ? 0ull : static_cast<u64>(x->tailh & 0x7fffffffu);
+    if (st == p && xo == owner) return c0;
+  }
+  const u32 c = h_find(D, (owner << 32) | p);
   return (c != 0 && D.tnodes[c].parent == node) ? c : 0;
+}
+__device__ u32 t_find_child(const SimDev& D, const Lead& L, u32 node, u32 a, u64 p, u64 n_full) {
+  return w_find_child(D, tw_ctx(D, L), node, a, p, n_full);
 }
 
 // common_len in whole pages (a partial trailing page never counts).
-__device__ __forceinline__ u64 t_common(const SimDev& D, const Lead& L, u32 c, u32 a, u64 p,
-                                        u64 n_full) {
-  const TNodeDev& n = D.tnodes[c];
+__device__ __forceinline__ u64 w_common(const TWalk& n, u64 S, u32 a, u64 p, u64 n_full) {
   u64 k = n.npages < n_full - p ? n.npages : n_full - p;
-  if (n.tail != a + 1) {
-    const u64 sh = L.S > p ? L.S - p : 0;
+  if ((n.tailh & 0x7fffffffu) != a + 1) {
+    const u64 sh = S > p ? S - p : 0;
     k = k < sh ? k : sh;
   }
   return k;
+}
+__device__ __forceinline__ u64 t_common(const SimDev& D, const Lead& L, u32 c, u32 a, u64 p,
+                                        u64 n_full) {
+  return w_common(*tw(D, L, c), L.S, a, p, n_full);
 }
 
 // split_node, cache_tree.cpp:68-92 (offset in pages). Returns the suffix.
@@ -127,11 +187,15 @@ __device__ u32 t_split(const SimDev& D, Lead& L, u32 id, u64 off) {
     N[id].device_slots = static_cast<u32>(off);
   }
   N[sid] = s;
+  tw_put(D, L, sid, s);
   for (u32 c = s.first_child; c != 0; c = N[c].next_sib) N[c].parent = sid;
   N[id].npages = static_cast<u32>(off);
   N[id].first_child = 0;
   N[id].cwd = t_subdev(s) ? 1 : 0;
-  t_add_child(D, id, sid);
+  TWalk* w = tw(D, L, id);
+  w->npages = static_cast<u32>(off);
+  w->first_child = 0;
+  t_add_child(D, L, id, sid);
   h_insert(D, t_nkey(L, s, s.start), sid);
   return sid;
 }
@@ -192,15 +256,17 @@ __device__ __noinline__ u64 t_match(const SimDev& D, Lead& L, u32 a, u64 len, u6
   const u64 now = ++L.cclock;
   const u64 n = len / L.ps;
   TNodeDev* N = D.tnodes;
+  const TWc W = tw_ctx(D, L);
   u32 node = 0;
   u64 pos = 0, matched = 0, hm = 0;
   bool host_phase = false;
   while (pos < n) {
-    const u32 c = t_find_child(D, L, node, a, pos, n);
+    const u32 c = w_find_child(D, W, node, a, pos, n);
     if (c == 0) break;
-    if (N[c].host) host_phase = true;
-    const u64 ka = t_common(D, L, c, a, pos, n);
-    const bool full = ka == N[c].npages;
+    const TWalk w = *twp(W, c);
+    if (tw_is_host(w)) host_phase = true;
+    const u64 ka = w_common(w, W.S, a, pos, n);
+    const bool full = ka == w.npages;
     if (ka == 0) break;
     if (!full) t_split(D, L, c, ka);
     if (host_phase) {
@@ -221,16 +287,17 @@ __device__ __noinline__ u64 t_match(const SimDev& D, Lead& L, u32 a, u64 len, u6
 
 // count_missing_slots, cache_tree.cpp:144-168 (pages).
 __device__ __noinline__ u64 t_missing(const SimDev& D, const Lead& L, u32 a, u64 n) {
-  const TNodeDev* N = D.tnodes;
+  const TWc W = tw_ctx(D, L);
   u32 node = 0;
   u64 pos = 0, m = 0;
   while (pos < n) {
-    const u32 c = t_find_child(D, L, node, a, pos, n);
+    const u32 c = w_find_child(D, W, node, a, pos, n);
     if (c == 0) return m + (n - pos);
-    const u64 ka = t_common(D, L, c, a, pos, n);
-    const bool full = ka == N[c].npages;
+    const TWalk w = *twp(W, c);
+    const u64 ka = w_common(w, W.S, a, pos, n);
+    const bool full = ka == w.npages;
     if (ka == 0) return m;
-    if (N[c].host) m += ka;
+    if (tw_is_host(w)) m += ka;
     pos += ka;
     node = c;
     if (!full) return m + (n - pos);
@@ -244,10 +311,11 @@ __device__ __noinline__ u64 t_missing(const SimDev& D, const Lead& L, u32 a, u64
 __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64 n) {
   const u64 now = ++L.cclock;
   TNodeDev* N = D.tnodes;
+  const TWc W = tw_ctx(D, L);
   u32 node = 0;
   u64 pos = 0, inserted = 0;
   while (pos < n) {
-    const u32 c = t_find_child(D, L, node, a, pos, n);
+    const u32 c = w_find_child(D, W, node, a, pos, n);
     if (c == 0) {
       const u32 l = t_alloc(D, L);
       if (l == 0) return inserted;
@@ -265,20 +333,23 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
       ln.host = 0;
       ln.alive = 1;
       N[l] = ln;
+      tw_put(D, L, l, ln);
       L.used += n - pos;
       inserted += n - pos;
-      t_add_child(D, node, l);
+      t_add_child(D, L, node, l);
       h_insert(D, t_key(L, a, pos), l);
       t_gain(D, l);
       break;
     }
-    const u64 ka = t_common(D, L, c, a, pos, n);
-    const bool full = ka == N[c].npages;
+    const TWalk w = *twp(W, c);
+    const u64 ka = w_common(w, W.S, a, pos, n);
+    const bool full = ka == w.npages;
     if (ka == 0) break;
     if (!full) t_split(D, L, c, ka);
-    if (N[c].host) {
-      const u32 pages = N[c].npages;
+    if (tw_is_host(w)) {
+      const u32 pages = tw(D, L, c)->npages;
       N[c].host = 0;
+      tw_host(D, L, c, 0);
       N[c].device_slots = pages;
       L.used += pages;
       inserted += pages;
@@ -294,21 +365,31 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
 // pin / unpin, cache_tree.cpp:370-402: every node covering [0, len).
 __device__ __noinline__ void t_pin(const SimDev& D, Lead& L, u32 a, u64 len, int delta) {
   TNodeDev* N = D.tnodes;
-  const u64 nf = (len + L.ps - 1) / L.ps;
+  const TWc W = tw_ctx(D, L);
+  const u64 ps = L.ps;
+  const u64 nf = (len + ps - 1) / ps;
   u32 node = 0;
-  u64 pos = 0;  // tokens
-  while (pos < len) {
-    const u32 c = (pos % L.ps == 0) ? t_find_child(D, L, node, a, pos / L.ps, nf) : 0;
-    if (c == 0 || pos + static_cast<u64>(N[c].npages) * L.ps > len) {
+  u64 pp = 0;  // pages: the reference's token position pp * ps stays page aligned
+  while (pp * ps < len) {
+    const u32 c = w_find_child(D, W, node, a, pp, nf);
+    if (c == 0) {
       fail(L, E_PIN_MISSING);
       return;
     }
-    if (delta < 0 && N[c].pin_count == 0) {
+    TWalk* w = twp(W, c);
+    const u32 np = w->npages;
+    if ((pp + np) * ps > len) {
+      fail(L, E_PIN_MISSING);
+      return;
+    }
+    const int pc = w->pin_count;
+    if (delta < 0 && pc == 0) {
       fail(L, E_UNPIN_UNDERFLOW);
       return;
     }
-    N[c].pin_count += delta;
-    pos += static_cast<u64>(N[c].npages) * L.ps;
+    w->pin_count = pc + delta;
+    N[c].pin_count = pc + delta;
+    pp += np;
     node = c;
   }
 }
@@ -317,21 +398,23 @@ __device__ __noinline__ void t_pin(const SimDev& D, Lead& L, u32 a, u64 len, int
 // dropped tokens (device and host) to L.discarded.
 __device__ __noinline__ u64 t_discard(const SimDev& D, Lead& L, u32 a, u64 len, u64 from) {
   TNodeDev* N = D.tnodes;
-  from = (from + L.ps - 1) / L.ps * L.ps;
-  if (from >= len) return 0;
+  const u64 fp = (from + L.ps - 1) / L.ps;  // from, rounded up, in pages
+  if (fp * L.ps >= len) return 0;
   const u64 n = len / L.ps;
+  const TWc W = tw_ctx(D, L);
   u32 node = 0;
-  u64 pos = 0;  // tokens
-  while (pos < from) {
-    const u32 c = t_find_child(D, L, node, a, pos / L.ps, n);
+  u64 pp = 0;  // pages
+  while (pp < fp) {
+    const u32 c = w_find_child(D, W, node, a, pp, n);
     if (c == 0) return 0;
-    const u64 kp = t_common(D, L, c, a, pos / L.ps, n);
-    if (kp < N[c].npages && pos + kp * L.ps < from) return 0;
-    if (static_cast<u64>(N[c].npages) * L.ps > from - pos) t_split(D, L, c, (from - pos) / L.ps);
-    pos += static_cast<u64>(N[c].npages) * L.ps;
+    const TWalk w = *twp(W, c);
+    const u64 kp = w_common(w, W.S, a, pp, n);
+    if (kp < w.npages && pp + kp < fp) return 0;
+    if (w.npages > fp - pp) t_split(D, L, c, fp - pp);
+    pp += twp(W, c)->npages;
     node = c;
   }
-  const u32 b = t_find_child(D, L, node, a, from / L.ps, n);
+  const u32 b = w_find_child(D, W, node, a, fp, n);
   if (b == 0) return 0;
   u64 slots = 0, toks = 0;
   long long pins = 0;
@@ -351,7 +434,7 @@ __device__ __noinline__ u64 t_discard(const SimDev& D, Lead& L, u32 a, u64 len, 
   if (t_subdev(N[b])) t_loss(D, b);
   L.used -= slots;
   L.discarded += toks;
-  t_remove_child(D, node, b);
+  t_remove_child(D, L, node, b);
   // free the subtree: its head keys leave the hash, its nodes the pool
   sp = 0;
   D.tstack[sp++] = b;
@@ -425,6 +508,7 @@ __device__ __noinline__ u64 t_evict_pop(const SimDev& D, Lead& L, u32 nf, u64 ne
     *offl += toks;
     N[v].device_slots = 0;
     N[v].host = 1;
+    tw_host(D, L, v, 1);
     t_loss(D, v);
     const u32 parent = vn.parent;
     if (parent != 0 && t_frontier(N[parent]))
@@ -485,6 +569,7 @@ __device__ void tree_init(const SimDev& D, Lead& L) {
   r.host = 0;
   r.alive = 0;  // the root is never a frontier candidate
   D.tnodes[0] = r;
+  tw_put(D, L, 0, r);
   L.t_alloc = 1;
   L.t_free_n = 0;
   L.t_next_ord = 0;

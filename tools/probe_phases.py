@@ -27,6 +27,9 @@ elif which.startswith("c5s"):  # scaled C5 shape: c5s<agents>
     s = config.c5_stress("aimd", agents=ag, capacity=1)
     s.engine.capacity = config.scaled_capacity(engine.Population(s.workload, s.seed).peak_aggregate_tokens)
     specs = [engine.SimSpec.from_scenario(s)]
+elif which == "c3off":
+    from paper_2601_22705_b200 import sweep
+    specs = [engine.SimSpec.from_scenario(s) for s in sweep.weak_shard("c3off", 0, 1)]
 elif which == "c3h":
     s = config.c3_dsv3("aimd")
     s.controller.h_thresh = 0.3
@@ -35,13 +38,16 @@ else:
     s = config.c3_dsv3("aimd", agents=int(which[3:]) if which[3:] else 2048)
     specs = [engine.SimSpec.from_scenario(s)]
 lib = engine.lib()
-lib.kvg_debug_profile.argtypes = [C.POINTER(C.c_ulonglong)]
+prof = hasattr(lib, "kvg_debug_profile")  # only in -DKVG_PROFILE builds
 b = engine.Batch(specs)
 buf = (C.c_ulonglong * 48)()
-lib.kvg_debug_profile(buf)  # clear
+if prof:
+    lib.kvg_debug_profile.argtypes = [C.POINTER(C.c_ulonglong)]
+    lib.kvg_debug_profile(buf)  # clear
 b.run()
-lib.kvg_debug_profile(buf)
-tot = sum(buf)
+if prof:
+    lib.kvg_debug_profile(buf)
+tot = max(1, sum(buf))
 r = b.result(0)
 print(which, "kernel ms", b.timing()[1], "total sim-cycles", tot, "events", r["events"], "stalls", r["stall_events"], "evict_calls", r["evict_calls"], "agent_steps", r["agent_steps"], "status", r["status"])
 for i in sorted(range(48), key=lambda i: -buf[i]):
