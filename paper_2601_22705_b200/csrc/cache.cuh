@@ -297,7 +297,7 @@ __device__ u64 tc_reload(const SimDev& D, Lead& L, u32 a, u64 len, u64 from, u64
       if (L.capacity - L.used < ka) break;
     }
     N[c].host = 0;
-    tw_host(D, L, c, 0);
+    tw_host(tw_ctx(D, L), c, 0);
     N[c].device_slots = static_cast<u32>(ka);
     N[c].last_access = now;
     L.used += ka;

@@ -111,7 +111,7 @@ size_t big_smem(const kvg_sim_desc& d) {
   if (tn == 0) return hot;
   const size_t base = (hot + 15) / 16 * 16;
   const size_t room = kBigSmemMax > base ? kBigSmemMax - base : 0;
-  return base + std::min<size_t>(room / sizeof(kvg::TWalk) * sizeof(kvg::TWalk), tn * sizeof(kvg::TWalk));
+  return base + std::min<size_t>(room / kvg::kTWalkSmemBytes, tn) * kvg::kTWalkSmemBytes;
 }
 
 }  // namespace

@@ -96,15 +96,17 @@ struct TNodeDev {
 static_assert(sizeof(TNodeDev) == 64, "TNodeDev must stay 64 B");
 
 // Mirror of the node fields the path walks read (find_child / common_len /
-// host / pin): 20 B per node, kept in shared memory for the low node ids (the
-// pool reuses freed ids first) and in HBM above. TNodeDev stays
+// host): one 16 B record per node, so a walk level is one 128-bit load that
+// also yields the next level's first child. The low node ids (the pool reuses
+// freed ids first) live in shared memory together with a pin-count mirror;
+// higher ids use this HBM array (and TNodeDev.pin_count). TNodeDev stays
 // authoritative; every write of a mirrored field writes both (tree.cuh).
 struct TWalk {
   u32 first_child, start, npages;
   u32 tailh;  // tail | host << 31
-  int pin_count;
 };
-static_assert(sizeof(TWalk) == 20, "TWalk must stay 20 B");
+static_assert(sizeof(TWalk) == 16, "TWalk must stay 16 B");
+constexpr unsigned kTWalkSmemBytes = sizeof(TWalk) + sizeof(int);  // + the pin mirror
 
 struct FrEnt {  // eviction frontier heap entry: (last_access, ordinal) order
   u64 la, ord;

@@ -99,8 +99,7 @@ struct Lead {
   int offload, o_full, o_then, pad3;
   u32 t_alloc, t_free_n, x_head, x_size, o_node, o_c;
   u64 t_next_ord, offloaded, reloaded;
-  TWalk* tw_s;  // walk mirror of node ids [0, tw_n) in shared memory (tree.cuh tw)
-  u32 tw_n, tw_pad;
+  u32 tw_off, tw_n;  // walk mirror of node ids [0, tw_n) at this dynamic-smem offset (tree.cuh)
   double pcie_busy, link_busy;
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
 #ifdef KVG_PROFILE
@@ -1070,12 +1069,13 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
           return false;
         }
         const u32 c = t_find_child(D, L, L.o_node, id, L.o_pos / L.ps, n);
-        if (c == 0 || !tw_is_host(*tw(D, L, c))) {
+        const TWc W = tw_ctx(D, L);
+        if (c == 0 || !tw_is_host(tw_get(W, c))) {
           L.phase = PH_O_RELOAD_END;
           return false;
         }
         u64 ka = t_common(D, L, c, id, L.o_pos / L.ps, n);
-        const u32 np = tw(D, L, c)->npages;
+        const u32 np = tw_get(W, c).npages;
         bool full = ka == np;
         const u64 want = (L.o_hm - L.o_promoted) / L.ps;
         if (ka > want) {
@@ -1100,7 +1100,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
       }
       const u32 c = L.o_c;
       N[c].host = 0;
-      tw_host(D, L, c, 0);
+      tw_host(tw_ctx(D, L), c, 0);
       N[c].device_slots = static_cast<u32>(L.o_ka);
       N[c].last_access = L.o_now;
       L.used += L.o_ka;
@@ -1218,17 +1218,19 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
       }
       const TWc W = tw_ctx(D, L);
       const u64 mp = matched / L.ps;  // matched is whole pages
-      u32 node = 0;
+      u32 node = 0, fc = tw_get(W, 0).first_child;
       u64 pp = 0;
       while (pp < mp) {
-        const u32 c = w_find_child(D, W, node, nid, pp, L.m_nctx);
-        const u64 np = c == 0 ? 0 : twp(W, c)->npages;
-        if (c == 0 || pp + np > mp) {
+        const u32 c = w_find_child(D, W, node, fc, nid, static_cast<u32>(pp),
+                                   static_cast<u32>(L.m_nctx));
+        const TWalk w = c == 0 ? TWalk{0, 0, 0, 0} : tw_get(W, c);
+        if (c == 0 || pp + w.npages > mp) {
           fail(L, E_OFFLOAD);
           return false;
         }
-        pp += np;
+        pp += w.npages;
         node = c;
+        fc = w.first_child;
       }
       L.o_now = ++L.cclock;
       L.o_pos = matched;
@@ -1704,8 +1706,8 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
       L.rl1 = D.rl1;
     }
     // offload: the tree's walk mirror takes the rest (capi.cu big_smem)
-    const size_t room = used < dyn_bytes ? (dyn_bytes - used) / sizeof(TWalk) : 0;
-    L.tw_s = reinterpret_cast<TWalk*>(dyn + used);
+    const size_t room = used < dyn_bytes ? (dyn_bytes - used) / kTWalkSmemBytes : 0;
+    L.tw_off = static_cast<u32>(used);
     L.tw_n = kOff && D.engine.eviction == KVG_EVICT_OFFLOAD
                  ? static_cast<u32>(room < D.tcap ? room : D.tcap) : 0;
   }

@@ -21,45 +21,62 @@ __device__ __forceinline__ u64 t_key(const Lead& L, u32 a, u64 k) {
 __device__ __forceinline__ u64 t_nkey(const Lead& L, const TNodeDev& n, u64 k) {
   return ((k < L.S ? 0ull : static_cast<u64>(n.tail)) << 32) | k;
 }
-__device__ __forceinline__ u64 t_wkey(const Lead& L, const TWalk& w, u64 k) {
-  return ((k < L.S ? 0ull : static_cast<u64>(w.tailh & 0x7fffffffu)) << 32) | k;
-}
 __device__ __forceinline__ bool t_subdev(const TNodeDev& n) {
   return n.device_slots > 0 || n.cwd > 0;
 }
 
 // ------------------------------------------------------------ walk mirror
 
-__device__ __forceinline__ TWalk* tw(const SimDev& D, const Lead& L, u32 id) {
-  return id < L.tw_n ? L.tw_s + id : D.twalk + id;
-}
-__device__ __forceinline__ void tw_put(const SimDev& D, const Lead& L, u32 id, const TNodeDev& n) {
-  TWalk* w = tw(D, L, id);
-  w->first_child = n.first_child;
-  w->start = n.start;
-  w->npages = n.npages;
-  w->tailh = n.tail | (n.host ? 0x80000000u : 0u);
-  w->pin_count = n.pin_count;
-}
-__device__ __forceinline__ void tw_host(const SimDev& D, const Lead& L, u32 id, u32 host) {
-  TWalk* w = tw(D, L, id);
-  w->tailh = (w->tailh & 0x7fffffffu) | (host ? 0x80000000u : 0u);
-}
-__device__ __forceinline__ bool tw_is_host(const TWalk& w) { return (w.tailh >> 31) != 0; }
+extern __shared__ __align__(16) unsigned char kvg_tw_smem[];  // the dynamic smem (engine_body)
 
 // The walk loops keep the mirror's placement and the shared-prompt bound in
 // registers (stores through generic pointers would otherwise force the Lead
 // fields to be re-read from shared memory on every level).
 struct TWc {
-  TWalk* s;
-  TWalk* g;
-  u32 n, pad;
-  u64 S;
+  u32 off, n;   // shared-memory part: ids [0, n) at kvg_tw_smem + off, pins after
+  TWalk* g;     // HBM part
+  TNodeDev* N;  // pins of ids >= n: the authoritative records
+  u32 S, pad;   // shared-prompt pages
 };
 __device__ __forceinline__ TWc tw_ctx(const SimDev& D, const Lead& L) {
-  return TWc{L.tw_s, D.twalk, L.tw_n, 0, L.S};
+  return TWc{L.tw_off, L.tw_n, D.twalk, D.tnodes, static_cast<u32>(L.S), 0};
 }
-__device__ __forceinline__ TWalk* twp(const TWc& W, u32 id) { return id < W.n ? W.s + id : W.g + id; }
+__device__ __forceinline__ uint4* tw_sm(const TWc& W) {
+  return reinterpret_cast<uint4*>(kvg_tw_smem + W.off);
+}
+__device__ __forceinline__ int* tw_sm_pin(const TWc& W) {
+  return reinterpret_cast<int*>(kvg_tw_smem + W.off + static_cast<size_t>(W.n) * sizeof(TWalk));
+}
+__device__ __forceinline__ TWalk tw_get(const TWc& W, u32 id) {
+  uint4 v;
+  if (id < W.n) v = tw_sm(W)[id];
+  else v = reinterpret_cast<const uint4*>(W.g)[id];
+  return TWalk{v.x, v.y, v.z, v.w};
+}
+__device__ __forceinline__ void tw_set(const TWc& W, u32 id, const TWalk& t) {
+  const uint4 v = make_uint4(t.first_child, t.start, t.npages, t.tailh);
+  if (id < W.n) tw_sm(W)[id] = v;
+  else reinterpret_cast<uint4*>(W.g)[id] = v;
+}
+__device__ __forceinline__ TWalk* tw_ref(const TWc& W, u32 id) {  // single-field writes
+  return id < W.n ? reinterpret_cast<TWalk*>(tw_sm(W)) + id : W.g + id;
+}
+__device__ __forceinline__ int tw_pin(const TWc& W, u32 id) {
+  return id < W.n ? tw_sm_pin(W)[id] : W.N[id].pin_count;
+}
+__device__ __forceinline__ void tw_set_pin(const TWc& W, u32 id, int v) {
+  if (id < W.n) tw_sm_pin(W)[id] = v;
+  W.N[id].pin_count = v;
+}
+__device__ __forceinline__ void tw_put(const TWc& W, u32 id, const TNodeDev& n) {
+  tw_set(W, id, TWalk{n.first_child, n.start, n.npages, n.tail | (n.host ? 0x80000000u : 0u)});
+  if (id < W.n) tw_sm_pin(W)[id] = n.pin_count;
+}
+__device__ __forceinline__ void tw_host(const TWc& W, u32 id, u32 host) {
+  TWalk* w = tw_ref(W, id);
+  w->tailh = (w->tailh & 0x7fffffffu) | (host ? 0x80000000u : 0u);
+}
+__device__ __forceinline__ bool tw_is_host(const TWalk& w) { return (w.tailh >> 31) != 0; }
 
 __device__ u32 h_find(const SimDev& D, u64 key) {
   u32 i = static_cast<u32>(hash64(key)) & D.hmask;
@@ -111,7 +128,7 @@ __device__ void t_add_child(const SimDev& D, const Lead& L, u32 p, u32 c) {
   N[c].next_sib = N[p].first_child;
   if (N[p].first_child) N[N[p].first_child].prev_sib = c;
   N[p].first_child = c;
-  tw(D, L, p)->first_child = c;
+  tw_ref(tw_ctx(D, L), p)->first_child = c;
 }
 __device__ void t_remove_child(const SimDev& D, const Lead& L, u32 p, u32 c) {
   TNodeDev* N = D.tnodes;
@@ -119,7 +136,7 @@ __device__ void t_remove_child(const SimDev& D, const Lead& L, u32 p, u32 c) {
     N[N[c].prev_sib].next_sib = N[c].next_sib;
   } else {
     N[p].first_child = N[c].next_sib;
-    tw(D, L, p)->first_child = N[c].next_sib;
+    tw_ref(tw_ctx(D, L), p)->first_child = N[c].next_sib;
   }
   if (N[c].next_sib) N[N[c].next_sib].prev_sib = N[c].prev_sib;
 }
@@ -130,36 +147,42 @@ __device__ void t_remove_child(const SimDev& D, const Lead& L, u32 p, u32 c) {
 // dependent load per level instead of three. A node's children have distinct
 // head keys (the reference's per-node map), so a first child whose head key
 // matches IS the child; otherwise the head-key hash decides as before.
-__device__ __forceinline__ u32 w_find_child(const SimDev& D, const TWc& W, u32 node, u32 a, u64 p,
-                                             u64 n_full) {
-  if (p >= n_full) return 0;
-  const u64 owner = p < W.S ? 0ull : static_cast<u64>(a) + 1;
-  const u32 c0 = twp(W, node)->first_child;
-  if (c0 != 0) {
-    const TWalk* x = twp(W, c0);
-    const u32 st = x->start;
-    const u64 xo = st < W.S ? 0ull : static_cast<u64>(x->tailh & 0x7fffffffu);
-    if (st == p && xo == owner) return c0;
-  }
-  const u32 c = h_find(D, (owner << 32) | p);
+// Walk levels are 32-bit page arithmetic (contexts stay below 2^32 tokens:
+// checked at batch create). `fc` is the first child of `node`, carried from
+// the previous level's mirror load.
+__device__ __noinline__ u32 w_find_slow(const SimDev& D, u32 node, u64 key) {
+  const u32 c = h_find(D, key);
   return (c != 0 && D.tnodes[c].parent == node) ? c : 0;
 }
+__device__ __forceinline__ u32 w_find_child(const SimDev& D, const TWc& W, u32 node, u32 fc, u32 a,
+                                             u32 p, u32 n_full) {
+  if (p >= n_full) return 0;
+  if (fc != 0) {
+    const TWalk x = tw_get(W, fc);
+    if (x.start == p && (p < W.S || (x.tailh & 0x7fffffffu) == a + 1)) return fc;
+  }
+  const u64 owner = p < W.S ? 0ull : static_cast<u64>(a) + 1;
+  return w_find_slow(D, node, (owner << 32) | p);
+}
 __device__ u32 t_find_child(const SimDev& D, const Lead& L, u32 node, u32 a, u64 p, u64 n_full) {
-  return w_find_child(D, tw_ctx(D, L), node, a, p, n_full);
+  const TWc W = tw_ctx(D, L);
+  return w_find_child(D, W, node, tw_get(W, node).first_child, a, static_cast<u32>(p),
+                      static_cast<u32>(n_full));
 }
 
 // common_len in whole pages (a partial trailing page never counts).
-__device__ __forceinline__ u64 w_common(const TWalk& n, u64 S, u32 a, u64 p, u64 n_full) {
-  u64 k = n.npages < n_full - p ? n.npages : n_full - p;
+__device__ __forceinline__ u32 w_common(const TWalk& n, u32 S, u32 a, u32 p, u32 n_full) {
+  u32 k = n.npages < n_full - p ? n.npages : n_full - p;
   if ((n.tailh & 0x7fffffffu) != a + 1) {
-    const u64 sh = S > p ? S - p : 0;
+    const u32 sh = S > p ? S - p : 0;
     k = k < sh ? k : sh;
   }
   return k;
 }
 __device__ __forceinline__ u64 t_common(const SimDev& D, const Lead& L, u32 c, u32 a, u64 p,
                                         u64 n_full) {
-  return w_common(*tw(D, L, c), L.S, a, p, n_full);
+  const TWc W = tw_ctx(D, L);
+  return w_common(tw_get(W, c), W.S, a, static_cast<u32>(p), static_cast<u32>(n_full));
 }
 
 // split_node, cache_tree.cpp:68-92 (offset in pages). Returns the suffix.
@@ -187,12 +210,13 @@ __device__ u32 t_split(const SimDev& D, Lead& L, u32 id, u64 off) {
     N[id].device_slots = static_cast<u32>(off);
   }
   N[sid] = s;
-  tw_put(D, L, sid, s);
+  const TWc W = tw_ctx(D, L);
+  tw_put(W, sid, s);
   for (u32 c = s.first_child; c != 0; c = N[c].next_sib) N[c].parent = sid;
   N[id].npages = static_cast<u32>(off);
   N[id].first_child = 0;
   N[id].cwd = t_subdev(s) ? 1 : 0;
-  TWalk* w = tw(D, L, id);
+  TWalk* w = tw_ref(W, id);
   w->npages = static_cast<u32>(off);
   w->first_child = 0;
   t_add_child(D, L, id, sid);
@@ -225,27 +249,46 @@ __device__ __forceinline__ bool t_frontier(const TNodeDev& n) {  // cache_tree.c
 }
 
 // OP_FRONTIER: every warp sweeps the node pool, one lane per 64 B record
-// (coalesced), and compacts the frontier nodes into op.fr with one atomic per
-// warp (ballot + rank).
+// (coalesced 16 B loads), kFrU records per lane in flight so a sweep costs a
+// few L2 round trips instead of one per record, and compacts the frontier
+// nodes into op.fr with one atomic per warp (ballot + rank).
+constexpr int kFrU = 4;
 __device__ __noinline__ void coop_frontier(Op& op, int warp, int lane, int nw) {
-  const TNodeDev* N = op.tnodes;
+  static_assert(offsetof(TNodeDev, last_access) == 0 && offsetof(TNodeDev, ordinal) == 8 &&
+                    offsetof(TNodeDev, device_slots) == 44 && offsetof(TNodeDev, pin_count) == 48 &&
+                    offsetof(TNodeDev, cwd) == 52 && offsetof(TNodeDev, host) == 56 &&
+                    offsetof(TNodeDev, alive) == 60,
+                "coop_frontier reads TNodeDev as four 16 B quads");
+  const uint4* N = reinterpret_cast<const uint4*>(op.tnodes);
   const u32 n = op.t_n;
-  for (u32 base = static_cast<u32>(warp) * 32u; base < n; base += static_cast<u32>(nw) * 32u) {
-    const u32 i = base + lane;
-    bool f = false;
-    u64 la = 0, ord = 0;
-    if (i < n) {
-      const TNodeDev& x = N[i];
-      f = t_frontier(x);
-      la = x.last_access;
-      ord = x.ordinal;
+  const u32 stride = static_cast<u32>(nw) * 32u;
+  for (u32 base = static_cast<u32>(warp) * 32u; base < n; base += kFrU * stride) {
+    uint4 q0[kFrU], q2[kFrU], q3[kFrU];
+#pragma unroll
+    for (int u = 0; u < kFrU; ++u) {
+      const u32 i = base + u * stride + lane;
+      q0[u] = q2[u] = q3[u] = make_uint4(0, 0, 0, 0);
+      if (i < n) {
+        q0[u] = N[4 * static_cast<size_t>(i)];
+        q2[u] = N[4 * static_cast<size_t>(i) + 2];
+        q3[u] = N[4 * static_cast<size_t>(i) + 3];
+      }
     }
-    const unsigned m = __ballot_sync(FULL, f);
-    if (m == 0) continue;
-    u32 b0 = 0;
-    if (lane == 0) b0 = atomicAdd(&op.fr_n, static_cast<unsigned>(__popc(m)));
-    b0 = __shfl_sync(FULL, b0, 0);
-    if (f) op.fr[b0 + __popc(m & ((1u << lane) - 1u))] = FrEnt{la, ord, i, 0};
+#pragma unroll
+    for (int u = 0; u < kFrU; ++u) {
+      // t_frontier: alive && !host && device_slots > 0 && pin_count == 0 && cwd == 0
+      const bool f = q3[u].w != 0 && q3[u].z == 0 && q2[u].w != 0 && q3[u].x == 0 && q3[u].y == 0;
+      const unsigned m = __ballot_sync(FULL, f);
+      if (m == 0) continue;
+      u32 b0 = 0;
+      if (lane == 0) b0 = atomicAdd(&op.fr_n, static_cast<unsigned>(__popc(m)));
+      b0 = __shfl_sync(FULL, b0, 0);
+      if (f)
+        op.fr[b0 + __popc(m & ((1u << lane) - 1u))] =
+            FrEnt{static_cast<u64>(q0[u].x) | static_cast<u64>(q0[u].y) << 32,
+                  static_cast<u64>(q0[u].z) | static_cast<u64>(q0[u].w) << 32,
+                  base + u * stride + lane, 0};
+    }
   }
 }
 
@@ -254,18 +297,18 @@ __device__ __noinline__ void coop_frontier(Op& op, int warp, int lane, int nw) {
 // match_prefix, cache_tree.cpp:114-142. Returns matched tokens.
 __device__ __noinline__ u64 t_match(const SimDev& D, Lead& L, u32 a, u64 len, u64* host_matched) {
   const u64 now = ++L.cclock;
-  const u64 n = len / L.ps;
+  const u32 n = static_cast<u32>(len / L.ps);
   TNodeDev* N = D.tnodes;
   const TWc W = tw_ctx(D, L);
-  u32 node = 0;
-  u64 pos = 0, matched = 0, hm = 0;
+  u32 node = 0, fc = tw_get(W, 0).first_child;
+  u32 pos = 0, matched = 0, hm = 0;
   bool host_phase = false;
   while (pos < n) {
-    const u32 c = w_find_child(D, W, node, a, pos, n);
+    const u32 c = w_find_child(D, W, node, fc, a, pos, n);
     if (c == 0) break;
-    const TWalk w = *twp(W, c);
+    const TWalk w = tw_get(W, c);
     if (tw_is_host(w)) host_phase = true;
-    const u64 ka = w_common(w, W.S, a, pos, n);
+    const u32 ka = w_common(w, W.S, a, pos, n);
     const bool full = ka == w.npages;
     if (ka == 0) break;
     if (!full) t_split(D, L, c, ka);
@@ -277,29 +320,32 @@ __device__ __noinline__ u64 t_match(const SimDev& D, Lead& L, u32 a, u64 len, u6
     }
     pos += ka;
     node = c;
+    fc = w.first_child;
     if (!full) break;
   }
-  L.hit_m += static_cast<double>(matched * L.ps);
+  L.hit_m += static_cast<double>(static_cast<u64>(matched) * L.ps);
   L.hit_r += static_cast<double>(len);
-  *host_matched = hm * L.ps;
-  return matched * L.ps;
+  *host_matched = static_cast<u64>(hm) * L.ps;
+  return static_cast<u64>(matched) * L.ps;
 }
 
 // count_missing_slots, cache_tree.cpp:144-168 (pages).
-__device__ __noinline__ u64 t_missing(const SimDev& D, const Lead& L, u32 a, u64 n) {
+__device__ __noinline__ u64 t_missing(const SimDev& D, const Lead& L, u32 a, u64 n64) {
   const TWc W = tw_ctx(D, L);
-  u32 node = 0;
-  u64 pos = 0, m = 0;
+  const u32 n = static_cast<u32>(n64);
+  u32 node = 0, fc = tw_get(W, 0).first_child;
+  u32 pos = 0, m = 0;
   while (pos < n) {
-    const u32 c = w_find_child(D, W, node, a, pos, n);
+    const u32 c = w_find_child(D, W, node, fc, a, pos, n);
     if (c == 0) return m + (n - pos);
-    const TWalk w = *twp(W, c);
-    const u64 ka = w_common(w, W.S, a, pos, n);
+    const TWalk w = tw_get(W, c);
+    const u32 ka = w_common(w, W.S, a, pos, n);
     const bool full = ka == w.npages;
     if (ka == 0) return m;
     if (tw_is_host(w)) m += ka;
     pos += ka;
     node = c;
+    fc = w.first_child;
     if (!full) return m + (n - pos);
   }
   return m;
@@ -312,10 +358,10 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
   const u64 now = ++L.cclock;
   TNodeDev* N = D.tnodes;
   const TWc W = tw_ctx(D, L);
-  u32 node = 0;
+  u32 node = 0, fc = tw_get(W, 0).first_child;
   u64 pos = 0, inserted = 0;
   while (pos < n) {
-    const u32 c = w_find_child(D, W, node, a, pos, n);
+    const u32 c = w_find_child(D, W, node, fc, a, static_cast<u32>(pos), static_cast<u32>(n));
     if (c == 0) {
       const u32 l = t_alloc(D, L);
       if (l == 0) return inserted;
@@ -333,7 +379,7 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
       ln.host = 0;
       ln.alive = 1;
       N[l] = ln;
-      tw_put(D, L, l, ln);
+      tw_put(W, l, ln);
       L.used += n - pos;
       inserted += n - pos;
       t_add_child(D, L, node, l);
@@ -341,15 +387,16 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
       t_gain(D, l);
       break;
     }
-    const TWalk w = *twp(W, c);
-    const u64 ka = w_common(w, W.S, a, pos, n);
+    const TWalk w = tw_get(W, c);
+    const u64 ka = w_common(w, W.S, a, static_cast<u32>(pos), static_cast<u32>(n));
     const bool full = ka == w.npages;
     if (ka == 0) break;
     if (!full) t_split(D, L, c, ka);
+    fc = full ? w.first_child : tw_get(W, c).first_child;  // a split re-parented c's children
     if (tw_is_host(w)) {
-      const u32 pages = tw(D, L, c)->npages;
+      const u32 pages = tw_get(W, c).npages;
       N[c].host = 0;
-      tw_host(D, L, c, 0);
+      tw_host(W, c, 0);
       N[c].device_slots = pages;
       L.used += pages;
       inserted += pages;
@@ -364,33 +411,33 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
 
 // pin / unpin, cache_tree.cpp:370-402: every node covering [0, len).
 __device__ __noinline__ void t_pin(const SimDev& D, Lead& L, u32 a, u64 len, int delta) {
-  TNodeDev* N = D.tnodes;
   const TWc W = tw_ctx(D, L);
-  const u64 ps = L.ps;
-  const u64 nf = (len + ps - 1) / ps;
-  u32 node = 0;
-  u64 pp = 0;  // pages: the reference's token position pp * ps stays page aligned
-  while (pp * ps < len) {
-    const u32 c = w_find_child(D, W, node, a, pp, nf);
+  // the reference's token position pp * ps stays page aligned: pp * ps < len
+  // <=> pp < ceil(len / ps); (pp + np) * ps > len <=> pp + np > floor(len / ps)
+  const u32 nf = static_cast<u32>((len + L.ps - 1) / L.ps);
+  const u32 lf = static_cast<u32>(len / L.ps);
+  u32 node = 0, fc = tw_get(W, 0).first_child;
+  u32 pp = 0;
+  while (pp < nf) {
+    const u32 c = w_find_child(D, W, node, fc, a, pp, nf);
     if (c == 0) {
       fail(L, E_PIN_MISSING);
       return;
     }
-    TWalk* w = twp(W, c);
-    const u32 np = w->npages;
-    if ((pp + np) * ps > len) {
+    const TWalk w = tw_get(W, c);
+    if (pp + w.npages > lf) {
       fail(L, E_PIN_MISSING);
       return;
     }
-    const int pc = w->pin_count;
+    const int pc = tw_pin(W, c);
     if (delta < 0 && pc == 0) {
       fail(L, E_UNPIN_UNDERFLOW);
       return;
     }
-    w->pin_count = pc + delta;
-    N[c].pin_count = pc + delta;
-    pp += np;
+    tw_set_pin(W, c, pc + delta);
+    pp += w.npages;
     node = c;
+    fc = w.first_child;
   }
 }
 
@@ -402,19 +449,21 @@ __device__ __noinline__ u64 t_discard(const SimDev& D, Lead& L, u32 a, u64 len, 
   if (fp * L.ps >= len) return 0;
   const u64 n = len / L.ps;
   const TWc W = tw_ctx(D, L);
-  u32 node = 0;
+  u32 node = 0, fc = tw_get(W, 0).first_child;
   u64 pp = 0;  // pages
   while (pp < fp) {
-    const u32 c = w_find_child(D, W, node, a, pp, n);
+    const u32 c = w_find_child(D, W, node, fc, a, static_cast<u32>(pp), static_cast<u32>(n));
     if (c == 0) return 0;
-    const TWalk w = *twp(W, c);
-    const u64 kp = w_common(w, W.S, a, pp, n);
+    const TWalk w = tw_get(W, c);
+    const u64 kp = w_common(w, W.S, a, static_cast<u32>(pp), static_cast<u32>(n));
     if (kp < w.npages && pp + kp < fp) return 0;
     if (w.npages > fp - pp) t_split(D, L, c, fp - pp);
-    pp += twp(W, c)->npages;
+    const TWalk w2 = tw_get(W, c);
+    pp += w2.npages;
     node = c;
+    fc = w2.first_child;
   }
-  const u32 b = w_find_child(D, W, node, a, fp, n);
+  const u32 b = w_find_child(D, W, node, fc, a, static_cast<u32>(fp), static_cast<u32>(n));
   if (b == 0) return 0;
   u64 slots = 0, toks = 0;
   long long pins = 0;
@@ -508,7 +557,7 @@ __device__ __noinline__ u64 t_evict_pop(const SimDev& D, Lead& L, u32 nf, u64 ne
     *offl += toks;
     N[v].device_slots = 0;
     N[v].host = 1;
-    tw_host(D, L, v, 1);
+    tw_host(tw_ctx(D, L), v, 1);
     t_loss(D, v);
     const u32 parent = vn.parent;
     if (parent != 0 && t_frontier(N[parent]))
@@ -569,7 +618,7 @@ __device__ void tree_init(const SimDev& D, Lead& L) {
   r.host = 0;
   r.alive = 0;  // the root is never a frontier candidate
   D.tnodes[0] = r;
-  tw_put(D, L, 0, r);
+  tw_put(tw_ctx(D, L), 0, r);
   L.t_alloc = 1;
   L.t_free_n = 0;
   L.t_next_ord = 0;
