@@ -1116,8 +1116,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
       log_rec(D, L, KVG_LOG_RELOAD, id, L.o_promoted, L.o_offl);
       if (L.o_promoted > 0) {
         const u64 m = L.o_matched;
-        t_pin(D, L, id, m + L.o_promoted, +1);
-        t_pin(D, L, id, m, -1);
+        t_pin_move(D, L, id, m + L.o_promoted, m);
         a.pinned_pg = static_cast<u32>((m + L.o_promoted) / L.ps);
         L.reloaded += L.o_promoted;
         const double end =
@@ -1146,6 +1145,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
         return false;
       }
       u64 created = 0;
+      const u64 stored = a.ctx - a.ctx % L.ps;
       if (L.m_nafter > 0) {
         const u64 need = t_missing(D, L, id, L.m_nafter);
         const u64 free_slots = L.capacity - L.used;
@@ -1153,13 +1153,12 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
           post_frontier(need - free_slots, PH_O_INSERT_EVICTED);
           return true;
         }
-        created = t_insert_commit(D, L, id, L.m_nafter);
+        // insert, pin(+1, stored), unpin(-1, matched): one walk (tree.cuh)
+        created = t_insert_commit(D, L, id, L.m_nafter, static_cast<u32>(L.o_matched / L.ps), true);
       }
       x_account(D, L, L.o_offl);
-      const u64 stored = a.ctx - a.ctx % L.ps;
       log_rec(D, L, KVG_LOG_INSERT, id, 1, stored);
-      t_pin(D, L, id, stored, +1);
-      t_pin(D, L, id, L.o_matched, -1);
+      if (L.m_nafter == 0) t_pin_move(D, L, id, stored, L.o_matched);
       a.pinned_pg = static_cast<u32>(stored / L.ps);
       L.created_pages += created;
       if (L.m_nafter > 0) L.refreshed_pages += L.o_matched / L.ps;
@@ -1195,13 +1194,13 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
       L.m_ctx0 = b.ctx;
       L.m_nctx = b.ctx / L.ps;
       u64 hm = 0;
-      const u64 matched = t_match(D, L, nid, b.ctx, &hm);
+      // match, pin(+1, matched), unpin(-1, pinned_len): one walk (tree.cuh)
+      const u64 matched =
+          t_match_pin(D, L, nid, b.ctx, static_cast<u64>(b.pinned_pg) * L.ps, &hm);
       const u64 r = (matched + hm) / L.ps;
       L.lookups += r + (r < L.m_nctx ? 1 : 0);
       L.hit_pages += matched / L.ps;
       log_rec(D, L, KVG_LOG_MATCH, nid, matched, hm);
-      t_pin(D, L, nid, matched, +1);
-      if (b.pinned_pg > 0) t_pin(D, L, nid, static_cast<u64>(b.pinned_pg) * L.ps, -1);
       b.pinned_pg = static_cast<u32>(matched / L.ps);
       L.o_matched = matched;
       L.o_hm = hm;

@@ -351,10 +351,127 @@ __device__ __noinline__ u64 t_missing(const SimDev& D, const Lead& L, u32 a, u64
   return m;
 }
 
+// pin / unpin, cache_tree.cpp:370-402: every node covering [0, len); the walk
+// can start mid-path at (node, pp) (the fused walks below continue one).
+__device__ void t_pin_walk(const SimDev& D, Lead& L, const TWc& W, u32 a, u32 node, u32 pp, u64 len,
+                           int delta) {
+  // the reference's token position pp * ps stays page aligned: pp * ps < len
+  // <=> pp < ceil(len / ps); (pp + np) * ps > len <=> pp + np > floor(len / ps)
+  const u32 nf = static_cast<u32>((len + L.ps - 1) / L.ps);
+  const u32 lf = static_cast<u32>(len / L.ps);
+  u32 fc = tw_get(W, node).first_child;
+  while (pp < nf) {
+    const u32 c = w_find_child(D, W, node, fc, a, pp, nf);
+    if (c == 0) {
+      fail(L, E_PIN_MISSING);
+      return;
+    }
+    const TWalk w = tw_get(W, c);
+    if (pp + w.npages > lf) {
+      fail(L, E_PIN_MISSING);
+      return;
+    }
+    const int pc = tw_pin(W, c);
+    if (delta < 0 && pc == 0) {
+      fail(L, E_UNPIN_UNDERFLOW);
+      return;
+    }
+    tw_set_pin(W, c, pc + delta);
+    pp += w.npages;
+    node = c;
+    fc = w.first_child;
+  }
+}
+__device__ __noinline__ void t_pin(const SimDev& D, Lead& L, u32 a, u64 len, int delta) {
+  t_pin_walk(D, L, tw_ctx(D, L), a, 0, 0, len, delta);
+}
+
+// Pin moves fused into a path walk: the node [s, e) (pages) of a path that
+// gains a pin over [0, new) and loses one over [0, old) changes by +1 when
+// s >= old, by 0 when e <= old, and a node straddling old is the unpin's
+// E_PIN_MISSING. Same final pin counts as pin(+1, new) then unpin(-1, old).
+__device__ __forceinline__ bool pin_move(const SimDev& D, Lead& L, const TWc& W, u32 c, u32 s,
+                                         u32 e, u32 old_p) {
+  if (e <= old_p) return true;
+  if (s < old_p) {
+    fail(L, E_PIN_MISSING);
+    return false;
+  }
+  tw_set_pin(W, c, tw_pin(W, c) + 1);
+  return true;
+}
+
+// pin(+1, new_len) then unpin(-1, old_len), both whole pages, in one walk.
+__device__ __noinline__ void t_pin_move(const SimDev& D, Lead& L, u32 a, u64 new_len, u64 old_len) {
+  const TWc W = tw_ctx(D, L);
+  const u32 nf = static_cast<u32>(new_len / L.ps), old_p = static_cast<u32>(old_len / L.ps);
+  u32 node = 0, fc = tw_get(W, 0).first_child, pp = 0;
+  while (pp < nf) {
+    const u32 c = w_find_child(D, W, node, fc, a, pp, nf);
+    if (c == 0) {
+      fail(L, E_PIN_MISSING);
+      return;
+    }
+    const TWalk w = tw_get(W, c);
+    if (pp + w.npages > nf) {
+      fail(L, E_PIN_MISSING);
+      return;
+    }
+    if (!pin_move(D, L, W, c, pp, pp + w.npages, old_p)) return;
+    pp += w.npages;
+    node = c;
+    fc = w.first_child;
+  }
+  if (old_p > nf) t_pin_walk(D, L, W, a, node, nf, old_len, -1);
+}
+
+// match_prefix (cache_tree.cpp:114-142), then pin(+1, matched) and
+// unpin(-1, old_len) (engine.cpp:337-346) in one walk. Returns matched tokens.
+__device__ __noinline__ u64 t_match_pin(const SimDev& D, Lead& L, u32 a, u64 len, u64 old_len,
+                                        u64* host_matched) {
+  const u64 now = ++L.cclock;
+  const u32 n = static_cast<u32>(len / L.ps);
+  const u32 old_p = static_cast<u32>(old_len / L.ps);  // pinned lengths are whole pages
+  TNodeDev* N = D.tnodes;
+  const TWc W = tw_ctx(D, L);
+  u32 node = 0, fc = tw_get(W, 0).first_child, dnode = 0;
+  u32 pos = 0, matched = 0, hm = 0;
+  bool host_phase = false, ok = true;
+  while (pos < n) {
+    const u32 c = w_find_child(D, W, node, fc, a, pos, n);
+    if (c == 0) break;
+    const TWalk w = tw_get(W, c);
+    if (tw_is_host(w)) host_phase = true;
+    const u32 ka = w_common(w, W.S, a, pos, n);
+    const bool full = ka == w.npages;
+    if (ka == 0) break;
+    if (!full) t_split(D, L, c, ka);
+    if (host_phase) {
+      hm += ka;
+    } else {
+      N[c].last_access = now;
+      if (ok) ok = pin_move(D, L, W, c, pos, pos + ka, old_p);
+      matched += ka;
+      dnode = c;
+    }
+    pos += ka;
+    node = c;
+    fc = w.first_child;
+    if (!full) break;
+  }
+  // the unpin reaching past the match continues from the match's last node
+  if (ok && old_p > matched) t_pin_walk(D, L, W, a, dnode, matched, old_len, -1);
+  L.hit_m += static_cast<double>(static_cast<u64>(matched) * L.ps);
+  L.hit_r += static_cast<double>(len);
+  *host_matched = static_cast<u64>(hm) * L.ps;
+  return static_cast<u64>(matched) * L.ps;
+}
+
 // insert after the eviction loop (cache_tree.cpp:188-227): the clock bump,
 // the path walk (promoting host nodes) and the new leaf. Returns new device
 // slots.
-__device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64 n) {
+__device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64 n,
+                                            u32 old_p = 0, bool pins = false) {
   const u64 now = ++L.cclock;
   TNodeDev* N = D.tnodes;
   const TWc W = tw_ctx(D, L);
@@ -385,6 +502,9 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
       t_add_child(D, L, node, l);
       h_insert(D, t_key(L, a, pos), l);
       t_gain(D, l);
+      if (pins) pin_move(D, L, W, l, static_cast<u32>(pos), static_cast<u32>(n), old_p);
+      pos = n;
+      node = l;
       break;
     }
     const TWalk w = tw_get(W, c);
@@ -403,42 +523,14 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
       t_gain(D, c);
     }
     N[c].last_access = now;
+    if (pins && !pin_move(D, L, W, c, static_cast<u32>(pos), static_cast<u32>(pos + ka), old_p))
+      return inserted;
     pos += ka;
     node = c;
   }
+  if (pins && old_p > pos) t_pin_walk(D, L, W, a, node, static_cast<u32>(pos),
+                                      static_cast<u64>(old_p) * L.ps, -1);
   return inserted;
-}
-
-// pin / unpin, cache_tree.cpp:370-402: every node covering [0, len).
-__device__ __noinline__ void t_pin(const SimDev& D, Lead& L, u32 a, u64 len, int delta) {
-  const TWc W = tw_ctx(D, L);
-  // the reference's token position pp * ps stays page aligned: pp * ps < len
-  // <=> pp < ceil(len / ps); (pp + np) * ps > len <=> pp + np > floor(len / ps)
-  const u32 nf = static_cast<u32>((len + L.ps - 1) / L.ps);
-  const u32 lf = static_cast<u32>(len / L.ps);
-  u32 node = 0, fc = tw_get(W, 0).first_child;
-  u32 pp = 0;
-  while (pp < nf) {
-    const u32 c = w_find_child(D, W, node, fc, a, pp, nf);
-    if (c == 0) {
-      fail(L, E_PIN_MISSING);
-      return;
-    }
-    const TWalk w = tw_get(W, c);
-    if (pp + w.npages > lf) {
-      fail(L, E_PIN_MISSING);
-      return;
-    }
-    const int pc = tw_pin(W, c);
-    if (delta < 0 && pc == 0) {
-      fail(L, E_UNPIN_UNDERFLOW);
-      return;
-    }
-    tw_set_pin(W, c, pc + delta);
-    pp += w.npages;
-    node = c;
-    fc = w.first_child;
-  }
 }
 
 // discard_suffix, cache_tree.cpp:404-437. Returns device slots freed; adds the
