@@ -326,7 +326,7 @@ def run_b200(args):
     h2d = sum(p.c.agents * p.c.steps * C.sizeof(abi.StepPlan) for p in pops.values()) + \
         len(specs) * 512
     d2h = 0
-    phases = {"create_ms": 0.0, "run_ms": 0.0, "results_ms": 0.0}
+    phases = {"create_ms": 0.0, "run_ms": 0.0, "results_ms": 0.0, "kernel_ms": 0.0}
     for k in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -334,6 +334,7 @@ def run_b200(args):
         t1 = time.perf_counter()
         b2.run()
         t2 = time.perf_counter()
+        kern_e2e = b2.timing()[1]  # the run's kernel span (rows stream out inside it)
         res2 = b2.results_array()
         d2h = int(res2["ticks"].sum()) * C.sizeof(abi.TraceRow) + \
             n_agents * C.sizeof(abi.AgentStats) + len(res2) * C.sizeof(abi.SimResult)
@@ -344,6 +345,7 @@ def run_b200(args):
             phases["create_ms"] += 1e3 * (t1 - t0) / args.e2e_steps
             phases["run_ms"] += 1e3 * (t2 - t1) / args.e2e_steps
             phases["results_ms"] += 1e3 * (t3 - t2) / args.e2e_steps
+            phases["kernel_ms"] += kern_e2e / args.e2e_steps
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
     if dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)

@@ -285,8 +285,13 @@ KVG_API kvg_status kvg_batch_log(kvg_batch* b, size_t i, kvg_log_record* out,
                                  size_t cap, size_t* n_records);
 /* Every simulation's result of the last run, one call (cap >= n). */
 KVG_API kvg_status kvg_batch_results(kvg_batch* b, kvg_sim_result* out, size_t cap);
+/* Zero-copy view of simulation i's trace rows in the host block (valid until
+ * the next run or free). */
+KVG_API kvg_status kvg_batch_trace_view(kvg_batch* b, size_t i,
+                                        const kvg_trace_row** rows, size_t* n_rows);
 /* Host pointers to the run's output arrays (valid until the next run or
- * free). Zero-copy when the batch was created with host_outputs. */
+ * free). Zero-copy when the batch was created with host_outputs. The trace
+ * array holds every simulation's rows; kvg_batch_trace_view locates them. */
 KVG_API kvg_status kvg_batch_outputs(kvg_batch* b, const kvg_sim_result** results,
                                      const kvg_trace_row** trace_base,
                                      const kvg_agent_stats** stats_base);

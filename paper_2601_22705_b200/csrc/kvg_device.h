@@ -175,7 +175,12 @@ struct SimDev {
   kvg_log_record* log;
   u64 log_cap;
   kvg_sim_result* result;
-  u64* counts;        // [0] = trace rows produced, [1] = log records produced
+  u64* counts;        // [0] = trace rows produced, [1] = log records produced, [2] = error
+  // host delivery (host_outputs): the simulation streams its trace rows into
+  // its slice of a mapped pinned host array while it runs (in chunks after
+  // control-tick rounds, the rest at its end), so the PCIe transfer overlaps
+  // the run instead of following it (nullptr: rows stay in HBM)
+  kvg_trace_row* trace_out;
 };
 
 // Cache-op (CacheTree seam) executor descriptor.

@@ -99,6 +99,7 @@ struct Lead {
   int offload, o_full, o_then, pad3;
   u32 t_alloc, t_free_n, x_head, x_size, o_node, o_c;
   u64 t_next_ord, offloaded, reloaded;
+  u64 n_flushed;     // trace rows already streamed to D.trace_out (flush_rows)
   u32 tw_off, tw_n;  // walk mirror of node ids [0, tw_n) at this dynamic-smem offset (tree.cuh)
   double pcie_busy, link_busy;
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
@@ -612,6 +613,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.finished = 0;
   L.n_ready = 0;
   L.used = L.cclock = L.discarded = L.lookups = 0;
+  L.n_flushed = 0;
   L.agent_steps = L.events = L.evict_calls = L.evicted = 0;
   L.pin_max = L.pin_priv = 0;
   L.L0 = L.lazy_sh = 0;
@@ -1678,6 +1680,26 @@ __device__ __forceinline__ size_t smem_bytes_for(u32 n) {
          (nwords + (nwords + 31) / 32) * sizeof(u32);
 }
 
+// Streamed host delivery: copies the trace rows produced since the last flush
+// into this simulation's slice of the mapped pinned host array, 8 B words on
+// consecutive lanes (full PCIe write bursts). Rows are append-only, so a
+// flushed row never changes. Called by warp 0 after a control-tick round
+// (when at least `min_rows` are pending) and by the whole CTA at the end.
+constexpr u64 kFlushRows = 64;
+__device__ __forceinline__ void flush_rows(const SimDev& D, Lead& L, int t, int nt, u64 min_rows) {
+  const u64 n = L.n_trace < D.trace_cap ? L.n_trace : D.trace_cap;
+  const u64 f = L.n_flushed;
+  if (n < f + min_rows || n == f) return;
+  constexpr u64 kW = sizeof(kvg_trace_row) / sizeof(u64);
+  const u64* src = reinterpret_cast<const u64*>(D.trace) + f * kW;
+  u64* dst = reinterpret_cast<u64*>(D.trace_out) + f * kW;
+  const u64 words = (n - f) * kW;
+  for (u64 i = t; i < words; i += nt) dst[i] = src[i];
+  if (nt == 32) __syncwarp();
+  else __syncthreads();
+  if (t == 0) L.n_flushed = n;
+}
+
 template <int kDepth, bool kOff>
 __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   __shared__ Lead L;
@@ -1754,7 +1776,13 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     if (op.kind == OP_EXIT) break;
     if (tid == 0) PROF_MARK(L, 32 + op.kind);
     if (op.kind == OP_TICKS) {
-      if (warp == 0) coop_ticks(D, L, lane);
+      if (warp == 0) {
+        coop_ticks(D, L, lane);
+        if (D.trace_out != nullptr) {
+          __syncwarp();
+          flush_rows(D, L, lane, 32, kFlushRows);
+        }
+      }
     } else if (op.kind == OP_PHASES) {
       if (warp == 0) coop_phases(D, L, lane);
     } else {
@@ -1763,6 +1791,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     __syncthreads();
     if (tid == 0) PROF_MARK(L, 46);
   }
+  if (D.trace_out != nullptr) flush_rows(D, L, tid, blockDim.x, 0);  // the rest
 #ifdef KVG_PROFILE
   if (tid == 0) {
     PROF_MARK(L, 47);

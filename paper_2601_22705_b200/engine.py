@@ -68,6 +68,8 @@ def lib():
     L.kvg_batch_results.argtypes = [C.c_void_p, P(abi.SimResult), C.c_size_t]
     L.kvg_batch_outputs.argtypes = [C.c_void_p, P(P(abi.SimResult)), P(P(abi.TraceRow)),
                                     P(P(abi.AgentStats))]
+    L.kvg_batch_trace_view.argtypes = [C.c_void_p, C.c_size_t, P(P(abi.TraceRow)),
+                                       P(C.c_size_t)]
     L.kvg_batch_free.argtypes = [C.c_void_p]
     L.kvg_batch_free.restype = None
     L.kvg_run_batch.argtypes = [C.c_int, P(abi.SimDesc), C.c_size_t, P(abi.SimResult)]
@@ -165,6 +167,15 @@ class SimSpec:
             self.__dict__["_desc"] = d
         return d
 
+    @property
+    def desc_bytes(self) -> bytes:
+        """The descriptor's bytes (cached): batches pack them with one join."""
+        b = self.__dict__.get("_desc_bytes")
+        if b is None:
+            b = bytes(self.desc)
+            self.__dict__["_desc_bytes"] = b
+        return b
+
     @staticmethod
     def from_scenario(s: Scenario, policy_text: str | None = None,
                       population: Population | None = None) -> "SimSpec":
@@ -186,7 +197,10 @@ class Batch:
             verify = os.environ.get("KVG_VERIFY", "0") == "1"
         self.specs = specs
         if specs:
-            self.descs = (abi.SimDesc * len(specs))(*[sp.desc for sp in specs])
+            # the descriptors hold pointers into the specs' populations, which
+            # self.specs keeps alive
+            self.descs = (abi.SimDesc * len(specs)).from_buffer_copy(
+                b"".join([sp.desc_bytes for sp in specs]))
         else:
             self.descs = (abi.SimDesc * 1)()
         opt = abi.BatchOptions(warps_per_sim=warps_per_sim, log_capacity=log_capacity,
@@ -240,11 +254,12 @@ class Batch:
         return [abi.struct_to_dict(rows[k]) for k in range(n.value)]
 
     def trace_array(self, i: int) -> np.ndarray:
-        n = C.c_size_t()
-        _check(lib().kvg_batch_trace(self.h, i, None, 0, C.byref(n)))
-        rows = (abi.TraceRow * max(1, n.value))()
-        _check(lib().kvg_batch_trace(self.h, i, rows, n.value, C.byref(n)))
-        return np.ctypeslib.as_array(rows)[: n.value]
+        """Simulation i's trace rows (one copy out of the host block)."""
+        p, n = C.POINTER(abi.TraceRow)(), C.c_size_t()
+        _check(lib().kvg_batch_trace_view(self.h, i, C.byref(p), C.byref(n)))
+        if n.value == 0:
+            return np.ctypeslib.as_array((abi.TraceRow * 1)())[:0]
+        return np.ctypeslib.as_array(p, shape=(n.value,)).copy()
 
     def agent_stats(self, i: int) -> list[dict]:
         na = self.specs[i].population.c.agents

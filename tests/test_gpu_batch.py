@@ -61,6 +61,28 @@ def test_host_delivery_equals_device_outputs():
         assert a.agent_stats(i) == h.agent_stats(i)
 
 
+def test_streamed_host_delivery_mixed_batch_with_regrow():
+    # rows stream into the pinned host array at cursor-allocated offsets (in
+    # finish order); a tiny trace capacity forces the regrow + re-run path
+    specs = []
+    for pol, seed in [("uncontrolled", 1), ("aimd", 2), ("aimd", 3), ("uncontrolled", 4)]:
+        s = config.c1_toy(pol)
+        s.seed = seed
+        specs.append(engine.SimSpec.from_scenario(s))
+    a = engine.Batch(specs)
+    a.run()
+    h = engine.Batch(specs, host_outputs=True, trace_capacity=8)
+    h.run()
+    for i in range(len(specs)):
+        assert _det(a.result(i)) == _det(h.result(i))
+        assert a.trace(i) == h.trace(i) and len(h.trace(i)) > 8
+        assert a.agent_stats(i) == h.agent_stats(i)
+    h.run()  # rerun reuses the host block
+    for i in range(len(specs)):
+        assert a.trace(i) == h.trace(i)
+        assert (a.trace_array(i) == h.trace_array(i)).all()
+
+
 def test_trace_overflow_regrows_and_reruns():
     s = config.c1_toy("aimd")
     spec = engine.SimSpec.from_scenario(s)
