@@ -1770,6 +1770,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     L.prof_ph = 47;
   }
 #endif
+  const bool stream = D.trace_out != nullptr;  // streamed host delivery
   for (;;) {
     if (tid == 0) leader_step<kOff>(D, L, op);
     __syncthreads();
@@ -1778,7 +1779,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     if (op.kind == OP_TICKS) {
       if (warp == 0) {
         coop_ticks(D, L, lane);
-        if (D.trace_out != nullptr) {
+        if (stream) {
           __syncwarp();
           flush_rows(D, L, lane, 32, kFlushRows);
         }
@@ -1791,7 +1792,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     __syncthreads();
     if (tid == 0) PROF_MARK(L, 46);
   }
-  if (D.trace_out != nullptr) flush_rows(D, L, tid, blockDim.x, 0);  // the rest
+  if (stream) flush_rows(D, L, tid, blockDim.x, 0);  // the rest
 #ifdef KVG_PROFILE
   if (tid == 0) {
     PROF_MARK(L, 47);
