@@ -6,6 +6,7 @@
 #include <mutex>
 #include <unordered_map>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>

@@ -83,6 +83,20 @@ def test_streamed_host_delivery_mixed_batch_with_regrow():
         assert (a.trace_array(i) == h.trace_array(i)).all()
 
 
+def test_host_delivery_packed_fallback(monkeypatch):
+    # a host block over the streaming limit falls back to pack + one DMA
+    monkeypatch.setenv("KVG_STREAM_MAX", "1024")
+    s = config.c1_toy("aimd")
+    spec = engine.SimSpec.from_scenario(s)
+    a = engine.Batch([spec, spec])
+    a.run()
+    h = engine.Batch([spec, spec], host_outputs=True)
+    h.run()
+    for i in range(2):
+        assert a.trace(i) == h.trace(i)
+        assert (a.trace_array(i) == h.trace_array(i)).all()
+
+
 def test_trace_overflow_regrows_and_reruns():
     s = config.c1_toy("aimd")
     spec = engine.SimSpec.from_scenario(s)
