@@ -1686,7 +1686,7 @@ __device__ __forceinline__ size_t smem_bytes_for(u32 n) {
 // flushed row never changes. Called by warp 0 after a control-tick round
 // (when at least `min_rows` are pending) and by the whole CTA at the end.
 constexpr u64 kFlushRows = 64;
-__device__ __forceinline__ void flush_rows(const SimDev& D, Lead& L, int t, int nt, u64 min_rows) {
+__device__ __noinline__ void flush_rows(const SimDev& D, Lead& L, int t, int nt, u64 min_rows) {
   const u64 n = L.n_trace < D.trace_cap ? L.n_trace : D.trace_cap;
   const u64 f = L.n_flushed;
   if (n < f + min_rows || n == f) return;
