@@ -1685,16 +1685,27 @@ __device__ __forceinline__ size_t smem_bytes_for(u32 n) {
 // consecutive lanes (full PCIe write bursts). Rows are append-only, so a
 // flushed row never changes. Called by warp 0 after a control-tick round
 // (when at least `min_rows` are pending) and by the whole CTA at the end.
-constexpr u64 kFlushRows = 64;
+constexpr u64 kFlushRows = 128;
 __device__ __noinline__ void flush_rows(const SimDev& D, Lead& L, int t, int nt, u64 min_rows) {
   const u64 n = L.n_trace < D.trace_cap ? L.n_trace : D.trace_cap;
   const u64 f = L.n_flushed;
   if (n < f + min_rows || n == f) return;
   constexpr u64 kW = sizeof(kvg_trace_row) / sizeof(u64);
-  const u64* src = reinterpret_cast<const u64*>(D.trace) + f * kW;
-  u64* dst = reinterpret_cast<u64*>(D.trace_out) + f * kW;
-  const u64 words = (n - f) * kW;
-  for (u64 i = t; i < words; i += nt) dst[i] = src[i];
+  // 16 B stores: the HBM and host slices share their 16 B alignment (both are
+  // 256 B aligned per simulation), so only a leading / trailing word is single
+  const u64* src = reinterpret_cast<const u64*>(D.trace);
+  u64* dst = reinterpret_cast<u64*>(D.trace_out);
+  u64 w0 = f * kW;
+  const u64 w1 = n * kW;
+  if (w0 & 1) {
+    if (t == 0) dst[w0] = src[w0];
+    ++w0;
+  }
+  const u64 pairs = (w1 - w0) >> 1;
+  const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(src + w0);
+  ulonglong2* d2 = reinterpret_cast<ulonglong2*>(dst + w0);
+  for (u64 i = t; i < pairs; i += nt) d2[i] = s2[i];
+  if (((w1 - w0) & 1) && t == nt - 1) dst[w1 - 1] = src[w1 - 1];
   if (nt == 32) __syncwarp();
   else __syncthreads();
   if (t == 0) L.n_flushed = n;
