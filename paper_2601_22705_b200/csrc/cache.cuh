@@ -298,10 +298,10 @@ __device__ u64 tc_reload(const SimDev& D, Lead& L, u32 a, u64 len, u64 from, u64
     }
     N[c].host = 0;
     tw_host(tw_ctx(D, L), c, 0);
-    N[c].device_slots = static_cast<u32>(ka);
+    tm_slots(tw_ctx(D, L), c, static_cast<u32>(ka));
     N[c].last_access = now;
     L.used += ka;
-    t_gain(D, c);
+    t_gain(D, L, c);
     promoted += ka * L.ps;
     pos += ka * L.ps;
     node = c;

@@ -155,6 +155,7 @@ struct Op {
   FrEnt* fr;
   u32 t_n;
   unsigned int fr_n;
+  u32 tw_off, tw_n;  // the shared-memory mirror (tree.cuh): ids [0, tw_n)
 };
 
 constexpr int kBins = 512;

@@ -106,7 +106,15 @@ struct TWalk {
   u32 tailh;  // tail | host << 31
 };
 static_assert(sizeof(TWalk) == 16, "TWalk must stay 16 B");
-constexpr unsigned kTWalkSmemBytes = sizeof(TWalk) + sizeof(int);  // + the pin mirror
+// Shared-memory twin of the frontier fields (node ids below the mirror bound):
+// the eviction sweep decides frontier membership from shared memory alone.
+struct TMeta {
+  u32 device_slots;
+  int pin_count, cwd;
+  u32 alive;
+};
+static_assert(sizeof(TMeta) == 16, "TMeta must stay 16 B");
+constexpr unsigned kTWalkSmemBytes = sizeof(TWalk) + sizeof(TMeta);
 
 struct FrEnt {  // eviction frontier heap entry: (last_access, ordinal) order
   u64 la, ord;

@@ -1055,6 +1055,8 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
     op.kind = OP_FRONTIER;
     op.fr_n = 0;
     op.t_n = L.t_alloc;
+    op.tw_off = L.tw_off;
+    op.tw_n = L.tw_n;
     L.phase = PH_O_EVICT_POP;
   };
   auto next_member = [&]() {
@@ -1103,10 +1105,10 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
       const u32 c = L.o_c;
       N[c].host = 0;
       tw_host(tw_ctx(D, L), c, 0);
-      N[c].device_slots = static_cast<u32>(L.o_ka);
+      tm_slots(tw_ctx(D, L), c, static_cast<u32>(L.o_ka));
       N[c].last_access = L.o_now;
       L.used += L.o_ka;
-      t_gain(D, c);
+      t_gain(D, L, c);
       L.o_promoted += L.o_ka * L.ps;
       L.o_pos += L.o_ka * L.ps;
       L.o_node = c;

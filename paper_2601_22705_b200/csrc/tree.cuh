@@ -44,8 +44,8 @@ __device__ __forceinline__ TWc tw_ctx(const SimDev& D, const Lead& L) {
 __device__ __forceinline__ uint4* tw_sm(const TWc& W) {
   return reinterpret_cast<uint4*>(kvg_tw_smem + W.off);
 }
-__device__ __forceinline__ int* tw_sm_pin(const TWc& W) {
-  return reinterpret_cast<int*>(kvg_tw_smem + W.off + static_cast<size_t>(W.n) * sizeof(TWalk));
+__device__ __forceinline__ TMeta* tw_sm_meta(const TWc& W) {
+  return reinterpret_cast<TMeta*>(kvg_tw_smem + W.off + static_cast<size_t>(W.n) * sizeof(TWalk));
 }
 __device__ __forceinline__ TWalk tw_get(const TWc& W, u32 id) {
   uint4 v;
@@ -62,15 +62,28 @@ __device__ __forceinline__ TWalk* tw_ref(const TWc& W, u32 id) {  // single-fiel
   return id < W.n ? reinterpret_cast<TWalk*>(tw_sm(W)) + id : W.g + id;
 }
 __device__ __forceinline__ int tw_pin(const TWc& W, u32 id) {
-  return id < W.n ? tw_sm_pin(W)[id] : W.N[id].pin_count;
+  return id < W.n ? tw_sm_meta(W)[id].pin_count : W.N[id].pin_count;
 }
 __device__ __forceinline__ void tw_set_pin(const TWc& W, u32 id, int v) {
-  if (id < W.n) tw_sm_pin(W)[id] = v;
+  if (id < W.n) tw_sm_meta(W)[id].pin_count = v;
   W.N[id].pin_count = v;
+}
+// the frontier twins: every write of device_slots / cwd / alive goes through these
+__device__ __forceinline__ void tm_slots(const TWc& W, u32 id, u32 v) {
+  if (id < W.n) tw_sm_meta(W)[id].device_slots = v;
+  W.N[id].device_slots = v;
+}
+__device__ __forceinline__ void tm_cwd(const TWc& W, u32 id, int v) {
+  if (id < W.n) tw_sm_meta(W)[id].cwd = v;
+  W.N[id].cwd = v;
+}
+__device__ __forceinline__ void tm_alive(const TWc& W, u32 id, u32 v) {
+  if (id < W.n) tw_sm_meta(W)[id].alive = v;
+  W.N[id].alive = v;
 }
 __device__ __forceinline__ void tw_put(const TWc& W, u32 id, const TNodeDev& n) {
   tw_set(W, id, TWalk{n.first_child, n.start, n.npages, n.tail | (n.host ? 0x80000000u : 0u)});
-  if (id < W.n) tw_sm_pin(W)[id] = n.pin_count;
+  if (id < W.n) tw_sm_meta(W)[id] = TMeta{n.device_slots, n.pin_count, n.cwd, n.alive};
 }
 __device__ __forceinline__ void tw_host(const TWc& W, u32 id, u32 host) {
   TWalk* w = tw_ref(W, id);
@@ -205,17 +218,17 @@ __device__ u32 t_split(const SimDev& D, Lead& L, u32 id, u64 off) {
   s.cwd = n.cwd;
   s.alive = 1;
   s.device_slots = 0;
+  const TWc W = tw_ctx(D, L);
   if (!n.host) {
     s.device_slots = n.device_slots - static_cast<u32>(off);
-    N[id].device_slots = static_cast<u32>(off);
+    tm_slots(W, id, static_cast<u32>(off));
   }
   N[sid] = s;
-  const TWc W = tw_ctx(D, L);
   tw_put(W, sid, s);
   for (u32 c = s.first_child; c != 0; c = N[c].next_sib) N[c].parent = sid;
   N[id].npages = static_cast<u32>(off);
   N[id].first_child = 0;
-  N[id].cwd = t_subdev(s) ? 1 : 0;
+  tm_cwd(W, id, t_subdev(s) ? 1 : 0);
   TWalk* w = tw_ref(W, id);
   w->npages = static_cast<u32>(off);
   w->first_child = 0;
@@ -224,21 +237,23 @@ __device__ u32 t_split(const SimDev& D, Lead& L, u32 id, u64 off) {
   return sid;
 }
 
-__device__ void t_gain(const SimDev& D, u32 id) {  // propagate_gain, cache_tree.cpp:94-102
+__device__ void t_gain(const SimDev& D, const Lead& L, u32 id) {  // propagate_gain, cache_tree.cpp:94-102
   TNodeDev* N = D.tnodes;
+  const TWc W = tw_ctx(D, L);
   u32 p = N[id].parent;
   for (;;) {
     const bool had = t_subdev(N[p]);
-    N[p].cwd += 1;
+    tm_cwd(W, p, N[p].cwd + 1);
     if (had || p == 0) break;
     p = N[p].parent;
   }
 }
-__device__ void t_loss(const SimDev& D, u32 id) {  // propagate_loss, cache_tree.cpp:104-112
+__device__ void t_loss(const SimDev& D, const Lead& L, u32 id) {  // propagate_loss, cache_tree.cpp:104-112
   TNodeDev* N = D.tnodes;
+  const TWc W = tw_ctx(D, L);
   u32 p = N[id].parent;
   for (;;) {
-    N[p].cwd -= 1;
+    tm_cwd(W, p, N[p].cwd - 1);
     if (t_subdev(N[p]) || p == 0) break;
     p = N[p].parent;
   }
@@ -248,11 +263,21 @@ __device__ __forceinline__ bool t_frontier(const TNodeDev& n) {  // cache_tree.c
   return n.alive && !n.host && n.device_slots > 0 && n.pin_count == 0 && n.cwd == 0;
 }
 
-// OP_FRONTIER: every warp sweeps the node pool, one lane per 64 B record
-// (coalesced 16 B loads), kFrU records per lane in flight so a sweep costs a
-// few L2 round trips instead of one per record, and compacts the frontier
-// nodes into op.fr with one atomic per warp (ballot + rank).
+// OP_FRONTIER: the CTA sweeps the node pool and compacts the frontier nodes
+// into op.fr with one atomic per warp (ballot + rank). Node ids below the
+// shared-memory mirror bound are decided from the mirror (TWalk host bit +
+// TMeta) and only the frontier ids then fetch (last_access, ordinal) from HBM,
+// all at once after a barrier; ids above it read their 64 B records from HBM,
+// one lane per record, kFrU records per lane in flight.
 constexpr int kFrU = 4;
+__device__ __forceinline__ void fr_emit(Op& op, int lane, bool f, const FrEnt& e) {
+  const unsigned m = __ballot_sync(FULL, f);
+  if (m == 0) return;
+  u32 b0 = 0;
+  if (lane == 0) b0 = atomicAdd(&op.fr_n, static_cast<unsigned>(__popc(m)));
+  b0 = __shfl_sync(FULL, b0, 0);
+  if (f) op.fr[b0 + __popc(m & ((1u << lane) - 1u))] = e;
+}
 __device__ __noinline__ void coop_frontier(Op& op, int warp, int lane, int nw) {
   static_assert(offsetof(TNodeDev, last_access) == 0 && offsetof(TNodeDev, ordinal) == 8 &&
                     offsetof(TNodeDev, device_slots) == 44 && offsetof(TNodeDev, pin_count) == 48 &&
@@ -261,12 +286,36 @@ __device__ __noinline__ void coop_frontier(Op& op, int warp, int lane, int nw) {
                 "coop_frontier reads TNodeDev as four 16 B quads");
   const uint4* N = reinterpret_cast<const uint4*>(op.tnodes);
   const u32 n = op.t_n;
-  const u32 stride = static_cast<u32>(nw) * 32u;
-  for (u32 base = static_cast<u32>(warp) * 32u; base < n; base += kFrU * stride) {
+  const u32 ns = n < op.tw_n ? n : op.tw_n;
+  const int tid = warp * 32 + lane, nt = nw * 32;
+  // 1) mirrored ids: frontier test from shared memory, ids only
+  const TWalk* tws = reinterpret_cast<const TWalk*>(kvg_tw_smem + op.tw_off);
+  const TMeta* tms = reinterpret_cast<const TMeta*>(kvg_tw_smem + op.tw_off +
+                                                    static_cast<size_t>(op.tw_n) * sizeof(TWalk));
+  for (u32 base = static_cast<u32>(warp) * 32u; base < ns; base += static_cast<u32>(nt)) {
+    const u32 i = base + lane;
+    bool f = false;
+    if (i < ns) {
+      const TMeta m = tms[i];
+      f = m.alive != 0 && (tws[i].tailh >> 31) == 0 && m.device_slots != 0 && m.pin_count == 0 &&
+          m.cwd == 0;
+    }
+    fr_emit(op, lane, f, FrEnt{0, 0, i, 0});
+  }
+  __syncthreads();
+  const u32 n1 = op.fr_n;
+  // 2a) their (last_access, ordinal), every load independent
+  for (u32 k = tid; k < n1; k += nt) {
+    const uint4 q0 = N[4 * static_cast<size_t>(op.fr[k].id)];
+    op.fr[k].la = static_cast<u64>(q0.x) | static_cast<u64>(q0.y) << 32;
+    op.fr[k].ord = static_cast<u64>(q0.z) | static_cast<u64>(q0.w) << 32;
+  }
+  // 2b) ids past the mirror: whole records from HBM
+  for (u32 base = ns + static_cast<u32>(warp) * 32u; base < n; base += kFrU * static_cast<u32>(nt)) {
     uint4 q0[kFrU], q2[kFrU], q3[kFrU];
 #pragma unroll
     for (int u = 0; u < kFrU; ++u) {
-      const u32 i = base + u * stride + lane;
+      const u32 i = base + u * nt + lane;
       q0[u] = q2[u] = q3[u] = make_uint4(0, 0, 0, 0);
       if (i < n) {
         q0[u] = N[4 * static_cast<size_t>(i)];
@@ -278,16 +327,10 @@ __device__ __noinline__ void coop_frontier(Op& op, int warp, int lane, int nw) {
     for (int u = 0; u < kFrU; ++u) {
       // t_frontier: alive && !host && device_slots > 0 && pin_count == 0 && cwd == 0
       const bool f = q3[u].w != 0 && q3[u].z == 0 && q2[u].w != 0 && q3[u].x == 0 && q3[u].y == 0;
-      const unsigned m = __ballot_sync(FULL, f);
-      if (m == 0) continue;
-      u32 b0 = 0;
-      if (lane == 0) b0 = atomicAdd(&op.fr_n, static_cast<unsigned>(__popc(m)));
-      b0 = __shfl_sync(FULL, b0, 0);
-      if (f)
-        op.fr[b0 + __popc(m & ((1u << lane) - 1u))] =
-            FrEnt{static_cast<u64>(q0[u].x) | static_cast<u64>(q0[u].y) << 32,
-                  static_cast<u64>(q0[u].z) | static_cast<u64>(q0[u].w) << 32,
-                  base + u * stride + lane, 0};
+      fr_emit(op, lane, f,
+              FrEnt{static_cast<u64>(q0[u].x) | static_cast<u64>(q0[u].y) << 32,
+                    static_cast<u64>(q0[u].z) | static_cast<u64>(q0[u].w) << 32,
+                    base + u * nt + lane, 0});
     }
   }
 }
@@ -501,7 +544,7 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
       inserted += n - pos;
       t_add_child(D, L, node, l);
       h_insert(D, t_key(L, a, pos), l);
-      t_gain(D, l);
+      t_gain(D, L, l);
       if (pins) pin_move(D, L, W, l, static_cast<u32>(pos), static_cast<u32>(n), old_p);
       pos = n;
       node = l;
@@ -517,10 +560,10 @@ __device__ __noinline__ u64 t_insert_commit(const SimDev& D, Lead& L, u32 a, u64
       const u32 pages = tw_get(W, c).npages;
       N[c].host = 0;
       tw_host(W, c, 0);
-      N[c].device_slots = pages;
+      tm_slots(W, c, pages);
       L.used += pages;
       inserted += pages;
-      t_gain(D, c);
+      t_gain(D, L, c);
     }
     N[c].last_access = now;
     if (pins && !pin_move(D, L, W, c, static_cast<u32>(pos), static_cast<u32>(pos + ka), old_p))
@@ -572,7 +615,7 @@ __device__ __noinline__ u64 t_discard(const SimDev& D, Lead& L, u32 a, u64 len, 
     fail(L, E_DISCARD_PINNED);
     return 0;
   }
-  if (t_subdev(N[b])) t_loss(D, b);
+  if (t_subdev(N[b])) t_loss(D, L, b);
   L.used -= slots;
   L.discarded += toks;
   t_remove_child(D, L, node, b);
@@ -583,7 +626,7 @@ __device__ __noinline__ u64 t_discard(const SimDev& D, Lead& L, u32 a, u64 len, 
     const u32 x = D.tstack[--sp];
     for (u32 c = N[x].first_child; c != 0; c = N[c].next_sib) D.tstack[sp++] = c;
     h_erase(D, t_nkey(L, N[x], N[x].start));
-    N[x].alive = 0;
+    tm_alive(tw_ctx(D, L), x, 0);
     D.tfree[L.t_free_n++] = x;
   }
   return slots;
@@ -647,10 +690,10 @@ __device__ __noinline__ u64 t_evict_pop(const SimDev& D, Lead& L, u32 nf, u64 ne
     const u64 toks = static_cast<u64>(vn.npages) * L.ps;
     L.offloaded += toks;
     *offl += toks;
-    N[v].device_slots = 0;
+    tm_slots(tw_ctx(D, L), v, 0);
     N[v].host = 1;
     tw_host(tw_ctx(D, L), v, 1);
-    t_loss(D, v);
+    t_loss(D, L, v);
     const u32 parent = vn.parent;
     if (parent != 0 && t_frontier(N[parent]))
       fr_push(h, nf, FrEnt{N[parent].last_access, N[parent].ordinal, parent, 0});
