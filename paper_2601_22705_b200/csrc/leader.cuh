@@ -1819,7 +1819,10 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
 // all in flight in one wave (measured: 24/SM leaves a 544-sim second wave).
 
 #ifndef KVG_SMALL_DEPTH
-#define KVG_SMALL_DEPTH 4
+#define KVG_SMALL_DEPTH 2
+#endif
+#ifndef KVG_BIG_DEPTH
+#define KVG_BIG_DEPTH 4
 #endif
 #ifndef KVG_SMALL_MINB
 #define KVG_SMALL_MINB 28
@@ -1835,7 +1838,7 @@ __global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small_off(co
 
 // Latency variant: up to 32 warps cooperate on one big simulation.
 __global__ void __launch_bounds__(1024, 1) engine_kernel_big(const SimDev* __restrict__ sims) {
-  engine_body<8, true>(sims);
+  engine_body<KVG_BIG_DEPTH, true>(sims);
 }
 
 }  // namespace kvg
