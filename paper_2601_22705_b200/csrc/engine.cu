@@ -466,8 +466,19 @@ __device__ __forceinline__ void scan_summ(const Op& op, int warp, int lane, int 
       e[g] = Summ{0, 0, 0, 0, 0, 0};
       if (bk[g] != NIL32) e[g] = ld_summ(&op.summ[bk[g]]);
     }
+    // one copy of f's body: the loads above stay in flight, the calls rotate
+    // through registers (f is large: the radix-select histogram step)
+#pragma unroll 1
+    for (int g = 0; g < kSumDepth; ++g) {
+      const u32 b0 = bk[0];
+      const Summ e0 = e[0];
 #pragma unroll
-    for (int g = 0; g < kSumDepth; ++g) f(bk[g] != NIL32, bk[g], e[g]);
+      for (int j = 0; j + 1 < kSumDepth; ++j) {
+        bk[j] = bk[j + 1];
+        e[j] = e[j + 1];
+      }
+      f(b0 != NIL32, b0, e0);
+    }
   }
 }
 
