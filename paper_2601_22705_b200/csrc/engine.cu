@@ -858,6 +858,7 @@ cudaError_t init(void* d_state, const kvg::SimDev& sim, unsigned long long capac
   h.lead.ps = page_size;
   h.lead.S = shared_pages;
   h.lead.offload = 1;
+  h.lead.log_on = sim.log != nullptr;  // victims are reported through the log
   cudaError_t e = cudaMemcpy(d_state, &h, sizeof h, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return e;
   kvg::cache_tree_init<<<1, 1>>>(static_cast<kvg::TreeCacheDev*>(d_state));

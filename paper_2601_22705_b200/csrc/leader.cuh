@@ -100,6 +100,7 @@ struct Lead {
   u32 t_alloc, t_free_n, x_head, x_size, o_node, o_c;
   u64 t_next_ord, offloaded, reloaded;
   u64 n_flushed;     // trace rows already streamed to D.trace_out (flush_rows)
+  u32 log_on, log_pad;  // D.log != nullptr
   u32 tw_off, tw_n;  // walk mirror of node ids [0, tw_n) at this dynamic-smem offset (tree.cuh)
   double pcie_busy, link_busy;
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
@@ -127,11 +128,16 @@ __device__ __forceinline__ void prof_mark(Lead& L, int next_slot) {
 
 // ------------------------------------------------------------------ helpers
 
-__device__ __forceinline__ void log_rec(const SimDev& D, Lead& L, u32 kind, u32 agent, u64 a,
-                                        u64 b) {
-  if (D.log == nullptr) return;
+// event log (tests / tracing): the on/off flag lives in the Lead (shared
+// memory), the store path out of line, so the 13 call sites cost a branch
+__device__ __noinline__ void log_store(const SimDev& D, Lead& L, u32 kind, u32 agent, u64 a,
+                                       u64 b) {
   unsigned long long i = L.n_log++;
   if (i < D.log_cap) D.log[i] = kvg_log_record{kind, agent, L.cclock, a, b};
+}
+__device__ __forceinline__ void log_rec(const SimDev& D, Lead& L, u32 kind, u32 agent, u64 a,
+                                        u64 b) {
+  if (L.log_on) log_store(D, L, kind, agent, a, b);
 }
 
 // lifecycle_edge (workload.cpp:110-128)
@@ -614,6 +620,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.n_ready = 0;
   L.used = L.cclock = L.discarded = L.lookups = 0;
   L.n_flushed = 0;
+  L.log_on = D.log != nullptr;
   L.agent_steps = L.events = L.evict_calls = L.evicted = 0;
   L.pin_max = L.pin_priv = 0;
   L.L0 = L.lazy_sh = 0;
