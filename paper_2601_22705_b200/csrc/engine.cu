@@ -408,7 +408,10 @@ __device__ __noinline__ void coop_range(Op& op, int warp, int lane, int nw) {
 // Visits every claimed bucket, one WARP per bucket (lane l holds slot l):
 // the whole-bucket passes (suffix discard, rehash). kScanDepth buckets in
 // flight per warp, rotated through registers.
-constexpr int kScanDepth = 4;
+#ifndef KVG_SCAN_DEPTH
+#define KVG_SCAN_DEPTH 4
+#endif
+constexpr int kScanDepth = KVG_SCAN_DEPTH;
 
 template <typename F>
 __device__ __forceinline__ void scan_buckets(const Op& op, int warp, int lane, int nw, F&& f) {
@@ -447,7 +450,10 @@ __device__ __forceinline__ void scan_buckets(const Op& op, int warp, int lane, i
 // select's input. kSumDepth summaries in flight per lane; f(valid, bucket,
 // summary) is called by every lane of the warp together (warp-convergent, so
 // f may use warp collectives).
-constexpr int kSumDepth = 4;
+#ifndef KVG_SUM_DEPTH
+#define KVG_SUM_DEPTH 4
+#endif
+constexpr int kSumDepth = KVG_SUM_DEPTH;
 
 template <typename F>
 __device__ __forceinline__ void scan_summ(const Op& op, int warp, int lane, int nw, F&& f) {

@@ -25,6 +25,9 @@ constexpr u32 NIL = 0xffffffffu;
 // Leader helpers called from many phases. Inlined: measured on C4, calls
 // (register save/restore through local memory) cost more than the smaller
 // code saves in instruction fetch (59.9 ms out of line vs 47.0 ms inlined).
+#ifndef KVG_MID_FN  // helpers with many call sites: one out-of-line copy
+#define KVG_MID_FN __forceinline__
+#endif
 #ifndef KVG_LEADER_FN
 #define KVG_LEADER_FN __forceinline__
 #endif
@@ -194,7 +197,7 @@ __device__ KVG_LEADER_FN u32 ready_next(const SimDev& D, const Lead& L, u32 from
 }
 
 // AgentRecord::set_state (workload.cpp:130-137)
-__device__ KVG_LEADER_FN void set_state(const SimDev& D, Lead& L, u32 id, uint8_t s) {
+__device__ KVG_MID_FN void set_state(const SimDev& D, Lead& L, u32 id, uint8_t s) {
   AgentDev& a = L.ag[id];
   if (!legal_edge(a.state, s)) {
     fail(L, E_ILLEGAL_TRANSITION);
@@ -299,7 +302,7 @@ __device__ __forceinline__ bool heap_less(const HeapEnt& x, const HeapEnt& y) {
 }
 
 // Engine::schedule for agent events (engine.cpp:143-145)
-__device__ KVG_LEADER_FN void sched_agent(const SimDev& D, Lead& L, u32 id, double t,
+__device__ KVG_MID_FN void sched_agent(const SimDev& D, Lead& L, u32 id, double t,
                                             uint8_t kind) {
   AgentDev& a = L.ag[id];
   if (a.ev_kind != EV_NONE) {
