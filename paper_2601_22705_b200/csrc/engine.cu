@@ -409,7 +409,7 @@ __device__ __noinline__ void coop_range(Op& op, int warp, int lane, int nw) {
 // the whole-bucket passes (suffix discard, rehash). kScanDepth buckets in
 // flight per warp, rotated through registers.
 #ifndef KVG_SCAN_DEPTH
-#define KVG_SCAN_DEPTH 4
+#define KVG_SCAN_DEPTH 2
 #endif
 constexpr int kScanDepth = KVG_SCAN_DEPTH;
 
@@ -451,7 +451,7 @@ __device__ __forceinline__ void scan_buckets(const Op& op, int warp, int lane, i
 // summary) is called by every lane of the warp together (warp-convergent, so
 // f may use warp collectives).
 #ifndef KVG_SUM_DEPTH
-#define KVG_SUM_DEPTH 4
+#define KVG_SUM_DEPTH 2
 #endif
 constexpr int kSumDepth = KVG_SUM_DEPTH;
 
