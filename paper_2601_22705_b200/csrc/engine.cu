@@ -862,6 +862,7 @@ cudaError_t init(void* d_state, const kvg::SimDev& sim, unsigned long long capac
   h.lead.capacity = capacity;
   h.lead.capacity_d = static_cast<double>(capacity);
   h.lead.ps = page_size;
+  h.lead.ps_shift = (page_size & (page_size - 1)) == 0 ? __builtin_ctzll(page_size) : -1;
   h.lead.S = shared_pages;
   h.lead.offload = 1;
   h.lead.log_on = sim.log != nullptr;  // victims are reported through the log

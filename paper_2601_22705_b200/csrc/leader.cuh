@@ -103,7 +103,8 @@ struct Lead {
   u32 t_alloc, t_free_n, x_head, x_size, o_node, o_c;
   u64 t_next_ord, offloaded, reloaded;
   u64 n_flushed;     // trace rows already streamed to D.trace_out (flush_rows)
-  u32 log_on, log_pad;  // D.log != nullptr
+  u32 log_on;        // D.log != nullptr
+  int ps_shift;      // log2(ps) when ps is a power of two, else -1 (pdiv / pmod)
   u32 tw_off, tw_n;  // walk mirror of node ids [0, tw_n) at this dynamic-smem offset (tree.cuh)
   double pcie_busy, link_busy;
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
@@ -153,6 +154,16 @@ __device__ __forceinline__ bool legal_edge(uint8_t from, uint8_t to) {
     case S_PAUSED: return to == S_AWAIT;
     default: return false;
   }
+}
+
+// token <-> page conversions: a shift for the power-of-two page sizes every
+// config uses, one out-of-line 64-bit divide otherwise
+__device__ __noinline__ u64 pdiv_slow(u64 x, u64 ps) { return x / ps; }
+__device__ __forceinline__ u64 pdiv(const Lead& L, u64 x) {
+  return L.ps_shift >= 0 ? x >> L.ps_shift : pdiv_slow(x, L.ps);
+}
+__device__ __forceinline__ u64 pmod(const Lead& L, u64 x) {
+  return L.ps_shift >= 0 ? x & (L.ps - 1) : x - pdiv_slow(x, L.ps) * L.ps;
 }
 
 __device__ __forceinline__ void fail(Lead& L, int code) {
@@ -276,7 +287,7 @@ __device__ __forceinline__ u32 paus_pop(const SimDev& D, Lead& L) {
 // Implicit pins: agent `id` now pins its path prefix [0, tokens).
 __device__ KVG_LEADER_FN void set_pinned(const SimDev& D, Lead& L, u32 id, u64 tokens) {
   AgentDev& a = L.ag[id];
-  const u64 old_pg = a.pinned_pg, new_pg = tokens / L.ps;
+  const u64 old_pg = a.pinned_pg, new_pg = pdiv(L, tokens);
   a.pinned_pg = static_cast<u32>(new_pg);
   if (old_pg == new_pg) return;
   const u64 S = L.S;
@@ -661,6 +672,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.capacity = D.engine.capacity;
   L.capacity_d = static_cast<double>(D.engine.capacity);
   L.ps = D.engine.page_size;
+  L.ps_shift = (L.ps & (L.ps - 1)) == 0 ? 63 - __clzll(static_cast<long long>(L.ps)) : -1;
   L.shared_len = D.shared_len;
   L.S = D.shared_pages;
   // Engine::run: admission check at t=0 (ordinal 0), first tick (ordinal 1)
@@ -1027,7 +1039,7 @@ __device__ __noinline__ void coop_phases(const SimDev& D, Lead& L, int lane) {
 __device__ __forceinline__ void member_success(const SimDev& D, Lead& L, u32 id, u64 ctx0,
                                             u64 matched) {
   AgentDev& a = L.ag[id];
-  const u64 stored = a.ctx - a.ctx % L.ps;
+  const u64 stored = a.ctx - pmod(L, a.ctx);
   const u64 missing = ctx0 - matched;
   const u64 rec = a.high_water > matched ? a.high_water - matched : 0;
   const u64 fresh = missing - rec;
@@ -1076,22 +1088,22 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
   switch (L.phase) {
     case PH_O_RELOAD_CHUNK:
     case PH_O_RELOAD_EVICTED: {  // reload's chunk loop, cache_tree.cpp:337-366
-      const u64 len = L.m_ctx0, n = len / L.ps;
+      const u64 len = L.m_ctx0, n = pdiv(L, len);
       if (L.phase == PH_O_RELOAD_CHUNK) {
         if (!(L.o_pos < len && L.o_promoted < L.o_hm)) {
           L.phase = PH_O_RELOAD_END;
           return false;
         }
-        const u32 c = t_find_child(D, L, L.o_node, id, L.o_pos / L.ps, n);
+        const u32 c = t_find_child(D, L, L.o_node, id, pdiv(L, L.o_pos), n);
         const TWc W = tw_ctx(D, L);
         if (c == 0 || !tw_is_host(tw_get(W, c))) {
           L.phase = PH_O_RELOAD_END;
           return false;
         }
-        u64 ka = t_common(D, L, c, id, L.o_pos / L.ps, n);
+        u64 ka = t_common(D, L, c, id, pdiv(L, L.o_pos), n);
         const u32 np = tw_get(W, c).npages;
         bool full = ka == np;
-        const u64 want = (L.o_hm - L.o_promoted) / L.ps;
+        const u64 want = pdiv(L, L.o_hm - L.o_promoted);
         if (ka > want) {
           ka = want;
           full = false;
@@ -1131,7 +1143,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
       if (L.o_promoted > 0) {
         const u64 m = L.o_matched;
         t_pin_move(D, L, id, m + L.o_promoted, m);
-        a.pinned_pg = static_cast<u32>((m + L.o_promoted) / L.ps);
+        a.pinned_pg = static_cast<u32>(pdiv(L, m + L.o_promoted));
         L.reloaded += L.o_promoted;
         const double end =
             x_enqueue(D, L, static_cast<double>(L.o_promoted) * D.cost.bytes_per_token);
@@ -1147,7 +1159,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
     case PH_O_INSERT_START: {
       const kvg_step_plan& plan = D.plans[static_cast<size_t>(id) * L.steps + a.step];
       a.ctx += plan.gen_tokens;  // append_tokens
-      L.m_nafter = a.ctx / L.ps;
+      L.m_nafter = pdiv(L, a.ctx);
       L.o_offl = 0;
       L.phase = PH_O_INSERT_COUNT;
       return false;
@@ -1159,7 +1171,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
         return false;
       }
       u64 created = 0;
-      const u64 stored = a.ctx - a.ctx % L.ps;
+      const u64 stored = a.ctx - pmod(L, a.ctx);
       if (L.m_nafter > 0) {
         const u64 need = t_missing(D, L, id, L.m_nafter);
         const u64 free_slots = L.capacity - L.used;
@@ -1168,14 +1180,14 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
           return true;
         }
         // insert, pin(+1, stored), unpin(-1, matched): one walk (tree.cuh)
-        created = t_insert_commit(D, L, id, L.m_nafter, static_cast<u32>(L.o_matched / L.ps), true);
+        created = t_insert_commit(D, L, id, L.m_nafter, static_cast<u32>(pdiv(L, L.o_matched)), true);
       }
       x_account(D, L, L.o_offl);
       log_rec(D, L, KVG_LOG_INSERT, id, 1, stored);
       if (L.m_nafter == 0) t_pin_move(D, L, id, stored, L.o_matched);
-      a.pinned_pg = static_cast<u32>(stored / L.ps);
+      a.pinned_pg = static_cast<u32>(pdiv(L, stored));
       L.created_pages += created;
-      if (L.m_nafter > 0) L.refreshed_pages += L.o_matched / L.ps;
+      if (L.m_nafter > 0) L.refreshed_pages += pdiv(L, L.o_matched);
       member_success(D, L, id, L.m_ctx0, L.o_matched);
       next_member();
       return false;
@@ -1206,16 +1218,16 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
       AgentDev& b = L.ag[nid];
       L.m_id = nid;
       L.m_ctx0 = b.ctx;
-      L.m_nctx = b.ctx / L.ps;
+      L.m_nctx = pdiv(L, b.ctx);
       u64 hm = 0;
       // match, pin(+1, matched), unpin(-1, pinned_len): one walk (tree.cuh)
       const u64 matched =
           t_match_pin(D, L, nid, b.ctx, static_cast<u64>(b.pinned_pg) * L.ps, &hm);
-      const u64 r = (matched + hm) / L.ps;
+      const u64 r = pdiv(L, matched + hm);
       L.lookups += r + (r < L.m_nctx ? 1 : 0);
-      L.hit_pages += matched / L.ps;
+      L.hit_pages += pdiv(L, matched);
       log_rec(D, L, KVG_LOG_MATCH, nid, matched, hm);
-      b.pinned_pg = static_cast<u32>(matched / L.ps);
+      b.pinned_pg = static_cast<u32>(pdiv(L, matched));
       L.o_matched = matched;
       L.o_hm = hm;
       L.o_offl = 0;
@@ -1230,7 +1242,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
         return false;
       }
       const TWc W = tw_ctx(D, L);
-      const u64 mp = matched / L.ps;  // matched is whole pages
+      const u64 mp = pdiv(L, matched);  // matched is whole pages
       u32 node = 0, fc = tw_get(W, 0).first_child;
       u64 pp = 0;
       while (pp < mp) {
@@ -1364,7 +1376,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
             // left in the table beyond a chain's held length are absent to
             // every reader (eviction candidates, rehash).
             {
-              const u64 fp = (L.shared_len + L.ps - 1) / L.ps;
+              const u64 fp = pdiv(L, L.shared_len + L.ps - 1);
               const u64 keep = fp > L.S ? fp - L.S : 0;
               op.freed = a.priv > keep ? static_cast<unsigned int>(a.priv - keep) : 0u;
             }
@@ -1432,7 +1444,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           continue;
         }
         L.m_ctx0 = a.ctx;
-        L.m_nctx = a.ctx / L.ps;
+        L.m_nctx = pdiv(L, a.ctx);
         L.m_now = ++L.cclock;  // match_prefix clock bump (cache_tree.cpp:115)
         // match_prefix (cache_tree.cpp:114-142). Residency is prefix-closed
         // along a path and chains only gain pages at their ends (insert) and
@@ -1473,7 +1485,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         AgentDev& a = L.ag[L.m_id];
         const kvg_step_plan& plan = D.plans[static_cast<size_t>(L.m_id) * L.steps + a.step];
         a.ctx += plan.gen_tokens;  // append_tokens
-        L.m_nafter = a.ctx / L.ps;
+        L.m_nafter = pdiv(L, a.ctx);
         L.m_f = f;
         L.rebuilt = 0;
         L.phase = PH_M_INSERT;
@@ -1564,7 +1576,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           if (sh > L.L0) L.L0 = sh;
           a.priv = static_cast<u32>(L.m_nafter > L.S ? L.m_nafter - L.S : 0);
         }
-        const u64 stored = a.ctx - a.ctx % L.ps;
+        const u64 stored = a.ctx - pmod(L, a.ctx);
         const u64 matched = L.m_f * L.ps;
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 1, stored);
         set_pinned(D, L, L.m_id, stored);  // pin(stored), unpin(matched)
@@ -1622,7 +1634,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.used -= op.freed;
           L.discarded += static_cast<u64>(op.freed) * L.ps;
           // pages from page_ceil(shared_len) on are gone (a straddling page stays, Q2)
-          const u64 fp = (L.shared_len + L.ps - 1) / L.ps;
+          const u64 fp = pdiv(L, L.shared_len + L.ps - 1);
           const u64 keep = fp > L.S ? fp - L.S : 0;
           AgentDev& a = L.ag[id];
           if (a.priv > keep) a.priv = static_cast<u32>(keep);
