@@ -1709,7 +1709,10 @@ __device__ __forceinline__ size_t smem_bytes_for(u32 n) {
 // consecutive lanes (full PCIe write bursts). Rows are append-only, so a
 // flushed row never changes. Called by warp 0 after a control-tick round
 // (when at least `min_rows` are pending) and by the whole CTA at the end.
-constexpr u64 kFlushRows = 128;
+#ifndef KVG_FLUSH_ROWS
+#define KVG_FLUSH_ROWS 128
+#endif
+constexpr u64 kFlushRows = KVG_FLUSH_ROWS;
 __device__ __noinline__ void flush_rows(const SimDev& D, Lead& L, int t, int nt, u64 min_rows) {
   const u64 n = L.n_trace < D.trace_cap ? L.n_trace : D.trace_cap;
   const u64 f = L.n_flushed;
