@@ -1858,6 +1858,9 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
 #ifndef KVG_SMALL_DEPTH
 #define KVG_SMALL_DEPTH 2
 #endif
+#ifndef KVG_BIG_SMEM_DESC
+#define KVG_BIG_SMEM_DESC false
+#endif
 #ifndef KVG_BIG_DEPTH
 #define KVG_BIG_DEPTH 4
 #endif
@@ -1875,7 +1878,7 @@ __global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small_off(co
 
 // Latency variant: up to 32 warps cooperate on one big simulation.
 __global__ void __launch_bounds__(1024, 1) engine_kernel_big(const SimDev* __restrict__ sims) {
-  engine_body<KVG_BIG_DEPTH, true, false>(sims);
+  engine_body<KVG_BIG_DEPTH, true, KVG_BIG_SMEM_DESC>(sims);
 }
 
 }  // namespace kvg
