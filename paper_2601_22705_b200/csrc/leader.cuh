@@ -104,6 +104,7 @@ struct Lead {
   u64 t_next_ord, offloaded, reloaded;
   u64 n_flushed;     // trace rows already streamed to D.trace_out (flush_rows)
   u32 log_on;        // D.log != nullptr
+  double b_wall, b_total;  // dispatch batch: max and sum of member times so far
   int ps_shift;      // log2(ps) when ps is a power of two, else -1 (pdiv / pmod)
   u32 tw_off, tw_n;  // walk mirror of node ids [0, tw_n) at this dynamic-smem offset (tree.cuh)
   double pcie_busy, link_busy;
@@ -1053,6 +1054,10 @@ __device__ __forceinline__ void member_success(const SimDev& D, Lead& L, u32 id,
   m.d = decode_t(D.cost, plan.gen_tokens, ctx0);
   m.t = m.f + m.r + m.d;
   D.batch[L.batch_n++] = m;
+  // the batch wall (max) and total (sum, member order) of engine.cpp:317-324,
+  // accumulated as members commit: same operations in the same order
+  L.b_wall = L.b_wall < m.t ? m.t : L.b_wall;
+  L.b_total += m.t;
   a.f_gen = static_cast<u32>(plan.gen_tokens);
   a.f_rec = static_cast<u32>(rec);
   a.f_has_tool = plan.has_tool != 0;
@@ -1339,6 +1344,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
             continue;
           }
           L.batch_n = 0;
+          L.b_wall = L.b_total = 0.0;
           L.m_next = ready_next(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
           L.phase = PH_MEMBER;
           continue;
@@ -1605,12 +1611,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       case PH_BATCH_END: {  // engine.cpp:317-332
         const u32 nb = L.batch_n;
         if (nb > 0) {
-          double wall = 0.0, total = 0.0;
-          for (u32 i = 0; i < nb; ++i) {
-            const double t = D.batch[i].t;
-            wall = wall < t ? t : wall;
-            total += t;
-          }
+          const double wall = L.b_wall, total = L.b_total;
           const double start = L.clock < L.gpu_busy ? L.gpu_busy : L.clock;
           L.gpu_busy = start + wall;
           L.device_busy += wall;
