@@ -157,6 +157,23 @@ __device__ __forceinline__ bool legal_edge(uint8_t from, uint8_t to) {
   }
 }
 
+// Per-agent statistics accumulate in HBM. KVG_STATS_RED=1 issues the
+// accumulations as fire-and-forget reductions (same order, same IEEE adds);
+// measured on C4 it is 7% SLOWER than the plain read-modify-write, so off.
+#ifndef KVG_STATS_RED
+#define KVG_STATS_RED 0
+#endif
+__device__ __forceinline__ void st_add(uint64_t& f, u64 v) {
+  if (KVG_STATS_RED)
+    atomicAdd(reinterpret_cast<unsigned long long*>(&f), static_cast<unsigned long long>(v));
+  else
+    f += v;
+}
+__device__ __forceinline__ void st_add(double& f, double v) {
+  if (KVG_STATS_RED) atomicAdd(&f, v);
+  else f += v;
+}
+
 // token <-> page conversions: a shift for the power-of-two page sizes every
 // config uses, one out-of-line 64-bit divide otherwise
 __device__ __noinline__ u64 pdiv_slow(u64 x, u64 ps) { return x / ps; }
@@ -483,7 +500,7 @@ __device__ __forceinline__ void pause_one(const SimDev& D, Lead& L, u32 id) {
   act_erase(D, L, id);
   paus_push(D, L, id);
   set_state(D, L, id, S_PAUSED);
-  ++D.stats[id].pause_events;
+  st_add(D.stats[id].pause_events, 1);
 }
 
 // Pauses the K ready agents with the largest admission sequence numbers, in
@@ -591,9 +608,11 @@ __device__ __noinline__ void finalize(const SimDev& D, Lead& L) {
   u64 rec_ev = 0, stalls = 0;
   double wait = 0.0;
   for (u32 i = 0; i < L.n; ++i) {  // engine.cpp:407-412, agent order
-    rec_ev += D.stats[i].recompute_events;
-    stalls += D.stats[i].stall_events;
-    wait += D.stats[i].wait_time;
+    // L2 reads (with KVG_STATS_RED the counters were accumulated at L2)
+    const kvg_agent_stats& st = D.stats[i];
+    rec_ev += __ldcg(reinterpret_cast<const unsigned long long*>(&st.recompute_events));
+    stalls += __ldcg(reinterpret_cast<const unsigned long long*>(&st.stall_events));
+    wait += __ldcg(&st.wait_time);
   }
   r->recompute_events = rec_ev;
   r->stall_events = stalls;
@@ -1063,7 +1082,7 @@ __device__ __forceinline__ void member_success(const SimDev& D, Lead& L, u32 id,
   a.f_has_tool = plan.has_tool != 0;
   a.f_obs = static_cast<u32>(plan.obs_tokens);
   a.f_tool = plan.tool_latency;
-  D.stats[id].wait_time += L.clock - a.ready_since;
+  st_add(D.stats[id].wait_time, L.clock - a.ready_since);
   set_state(D, L, id, S_GEN);
   a.stalled = 0;  // (stall bookkeeping, informational)
   ++L.agent_steps;
@@ -1152,7 +1171,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
         L.reloaded += L.o_promoted;
         const double end =
             x_enqueue(D, L, static_cast<double>(L.o_promoted) * D.cost.bytes_per_token);
-        D.stats[id].wait_time += L.clock - a.ready_since;
+        st_add(D.stats[id].wait_time, L.clock - a.ready_since);
         set_state(D, L, id, S_GEN);
         sched_agent(D, L, id, end, EV_XFER);
         next_member();
@@ -1203,7 +1222,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
       a.ctx = L.m_ctx0;
       t_pin(D, L, id, L.o_matched, -1);
       a.pinned_pg = 0;
-      ++D.stats[id].stall_events;
+      st_add(D.stats[id].stall_events, 1);
       next_member();
       return false;
     }
@@ -1363,9 +1382,9 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           kvg_agent_stats& st = D.stats[agent];
           L.decoded_cum += a.f_gen;
           L.rec_cum += a.f_rec;
-          st.generated_tokens += a.f_gen;
-          st.recompute_tokens += a.f_rec;
-          if (a.f_rec > 0) ++st.recompute_events;
+          st_add(st.generated_tokens, a.f_gen);
+          st_add(st.recompute_tokens, a.f_rec);
+          if (a.f_rec > 0) st_add(st.recompute_events, 1);
           ++a.step;
           if (a.step >= L.steps) {
             set_state(D, L, agent, S_DONE);
@@ -1602,7 +1621,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       case PH_M_RESTORED: {
         if (op.err) fail(L, op.err);
         set_pinned(D, L, L.m_id, 0);  // unpin(matched); pinned_len = 0
-        ++D.stats[L.m_id].stall_events;
+        st_add(D.stats[L.m_id].stall_events, 1);
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 0, 0);
         L.m_next = ready_next(D, L, L.m_id + 1);
         L.phase = PH_MEMBER;
