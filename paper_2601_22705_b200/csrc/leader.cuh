@@ -25,6 +25,9 @@ constexpr u32 NIL = 0xffffffffu;
 // Leader helpers called from many phases. Inlined: measured on C4, calls
 // (register save/restore through local memory) cost more than the smaller
 // code saves in instruction fetch (59.9 ms out of line vs 47.0 ms inlined).
+#ifndef KVG_TICK_AHEAD  // pipelined ticks when at least KVG_TICK_AHEAD + 1 are due
+#define KVG_TICK_AHEAD 3.0
+#endif
 #ifndef KVG_MID_FN  // helpers with many call sites: one out-of-line copy
 #define KVG_MID_FN __forceinline__
 #endif
@@ -870,7 +873,7 @@ __device__ __forceinline__ bool ticks_apply(const Lead& L) {
   if (L.kind == KVG_POLICY_AIMD && L.cfg.signal_smoothing > 0) return false;
   const double t_agent = L.hsize > 0 ? L.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
   return L.tick_t < t_agent && !(L.tick_t > L.horizon) &&
-         L.tick_t + 3.0 * L.interval < t_agent;  // >= 4 ticks: cheaper than the scalar loop
+         L.tick_t + KVG_TICK_AHEAD * L.interval < t_agent;  // >= 4 ticks: cheaper than the scalar loop
 }
 
 // OP_TICKS (warp 0): the same event sequence as fast_housekeeping — control
