@@ -2,24 +2,37 @@
 """Benchmark of the B200 engine for the kvadmit simulator hot path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--workload c4|c2|c1]
+                    [--workload c4|c5|c2|c3|c3off|c1|kernels] [--split weak|strong]
 
 Default workload (BASELINE.json metric "simulated agent-steps/s & prefix-block
 lookups/s at 1/2/4/8 B200 vs CPU ref"): C4, the 4096-simulation controller
 sweep over the C1 toy trace (64 agents x 10 steps, Qwen3-32B KV sizing; grid
 u_low x u_high x alpha x beta x h_thresh). One STEP = every
-simulation of the sweep run to completion. Weak scaling: every rank runs its
-own full 4096-sim sweep (workload seed 42 + rank); no data-path collective, one
-NCCL gather of per-sim summary records at the end.
+simulation of the sweep run to completion.
+
+Multi-GPU: simulations never exchange data, so ranks shard
+them with no data-path collective and ONE NCCL all_gather of per-simulation
+summary records at the end. `--gpus N` without torchrun re-executes itself
+under torch.distributed.run with N ranks (one per GPU).
+  --split weak   (default) every rank runs its own full 4096-sim sweep
+                 (workload seed 42 + rank; rank 0 = the BASELINE config);
+  --split strong the seed-42 sweep's 4096 sims split [g*N/G, (g+1)*N/G).
+C5 (`--workload c5`) is one 65,536-agent simulation per GPU: rank r runs
+replica r of {aimd, agent_cap:256, agent_cap:1024, agent_cap:4096} x seeds
+{5, 6} (a single simulation's LRU order is global: replicas only).
+
+`--workload kernels` measures the page-table kernels in isolation (batched
+prefix lookup and eviction select on C2- and C5-size tables, bench_kernels.py).
 
 --impl reference runs the UNMODIFIED reference run_simulation (oracle/_ref,
-compiled from /root/reference sources) on all host cores, rank 0 only.
+compiled from /root/reference sources) on the host cores, rank 0 only.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,19 +46,24 @@ PEAKS_PATH = os.path.join(REPO, "MEASURED_PEAKS.json")
 PROFILE_SUMMARY = os.path.join(REPO, "profiles", "ncu_summary.json")
 METRIC = "simulated agent-steps/s & prefix-block lookups/s at 1/2/4/8 B200 vs CPU ref"
 HBM_FALLBACK_GBS = 6650.0
+C5_REPLICAS = [("aimd", 5), ("agent_cap:256", 5), ("agent_cap:1024", 5), ("agent_cap:4096", 5),
+               ("aimd", 6), ("agent_cap:256", 6), ("agent_cap:1024", 6), ("agent_cap:4096", 6)]
 
 
-def parse_args():
+def parse_args(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--workload", default="c4", choices=["c4", "c2", "c3", "c3off", "c1"])
+    p.add_argument("--workload", default="c4",
+                   choices=["c4", "c5", "c2", "c3", "c3off", "c1", "kernels"])
+    p.add_argument("--split", default="weak", choices=["weak", "strong"])
     p.add_argument("--sims", type=int, default=4096)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-probe-mode", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
-    return p.parse_args()
+    return p.parse_args(argv)
 
 
 def env_rank():
@@ -53,25 +71,80 @@ def env_rank():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_respawn(args, argv) -> bool:
+    """`bench.py --gpus N` outside torchrun: re-execute under
+    torch.distributed.run with N ranks. Returns False when already a rank (or
+    N == 1); otherwise runs the N-rank job and exits with its status."""
+    _, world, _ = env_rank()
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        if "WORLD_SIZE" in os.environ and world != args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return False
+    if args.impl == "b200":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+    sys.exit(subprocess.call(cmd))
+
+
 # --------------------------------------------------------------------------- workloads
 
-def build_scenarios(workload: str, rank: int, sims: int):
-    from paper_2601_22705_b200 import sweep
-    scen = sweep.weak_shard(workload, rank, sims)
-    if workload == "c4":
-        desc = (f"C4 controller sweep: {sims} sims of C1 (64 agents x 10 steps, private 1024-token "
-                f"prompts, 12,629-page cache, Qwen3-32B KV sizing), workload seed {42 + rank}")
-    elif workload == "c2":
-        desc = "C2: 1024 agents x 16 steps, 4K->55.7K contexts, 2,038,926-page cache, aimd"
-    elif workload == "c3":
-        desc = ("C3: DeepSeek-V3 MLA sizing, 2048 agents x 10 steps, 613,697-page cache, "
-                "aimd h_thresh=0.3")
-    elif workload == "c3off":
-        desc = ("C3 shape, offload tier: 32 agents x 10 steps, scaled cache (peak/1.5), "
-                "uncontrolled admission + offload eviction (PCIe 25 GB/s link model)")
-    else:
-        desc = "C1 toy: 64 agents x 10 steps, aimd"
-    return scen, desc
+def build_scenarios(args, rank: int, world: int):
+    from paper_2601_22705_b200 import config, sweep
+    w = args.workload
+    if w == "c4":
+        if args.split == "strong":
+            scen = sweep.strong_shard(config.c4_sweep(args.sims, seed=42), rank, world)
+            desc = (f"C4 controller sweep: {args.sims} sims of C1 (64 agents x 10 steps, private "
+                    f"1024-token prompts, 12,629-page cache, Qwen3-32B KV sizing), workload seed "
+                    f"42, split over {world} GPU(s): this rank sims "
+                    f"[{rank * args.sims // world}, {(rank + 1) * args.sims // world})")
+        else:
+            scen = sweep.weak_shard("c4", rank, args.sims)
+            desc = (f"C4 controller sweep: {args.sims} sims of C1 (64 agents x 10 steps, private "
+                    f"1024-token prompts, 12,629-page cache, Qwen3-32B KV sizing), workload seed "
+                    f"42 + rank ({42 + rank} here)")
+        return scen, desc
+    if w == "c5":
+        pol, seed = C5_REPLICAS[rank % len(C5_REPLICAS)]
+        s = config.c5_stress(pol, seed=seed)
+        return [s], (f"C5 stress replica {rank}: 65,536 agents x 16 steps, shared 8,192-token "
+                     f"prompt, contexts to 107K tokens, 16,777,216-page cache, {pol}, seed {seed}, "
+                     f"horizon 1e6 s simulated")
+    scen = sweep.weak_shard(w, rank, args.sims)
+    desc = {
+        "c2": "C2: 1024 agents x 16 steps, 4K->55.7K contexts, 2,038,926-page cache, aimd",
+        "c3": "C3: DeepSeek-V3 MLA sizing, 2048 agents x 10 steps, 613,697-page cache, "
+              "aimd h_thresh=0.3",
+        "c3off": "C3 shape, offload tier: 32 agents x 10 steps, scaled cache (peak/1.5), "
+                 "uncontrolled admission + offload eviction (PCIe 25 GB/s link model)",
+        "c1": "C1 toy: 64 agents x 10 steps, aimd",
+    }[w]
+    return scen, desc + (f", workload seed + rank" if world > 1 else "")
+
+
+def cpu_scenarios(args, scen):
+    """What the CPU reference runs for this workload: the same simulations
+    (all of them), except C5, whose full size the CPU reference cannot hold
+    (contexts materialised at 8 B per token: ~48 GB):
+    there the 1,024-agent C5 shape (same distributions, capacity = peak/1.5)."""
+    if args.workload != "c5":
+        return scen, None
+    from paper_2601_22705_b200 import config, engine
+    s = config.c5_stress(scen[0].policy, seed=scen[0].seed, agents=1024, capacity=1)
+    s.engine.capacity = config.scaled_capacity(
+        engine.Population(s.workload, s.seed).peak_aggregate_tokens)
+    return [s], "C5 shape scaled to 1,024 agents (the full size does not fit the CPU reference)"
 
 
 def make_specs(scen):
@@ -149,11 +222,21 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- helpers
 
-def algorithmic_bytes(results, tree: bool = False) -> dict:
-    """SURVEY.md §8(d) / BASELINE.md §2 per-unit byte counts. Offload mode
-    (tree=True): an eviction select reads one 64 B node record per pool entry."""
-    look = sum(16 * r.lookups + 8 * r.hit_pages for r in results)
-    ins = sum(16 * r.created_pages + 8 * r.refreshed_pages for r in results)
+def algorithmic_bytes(results, tree: bool = False, probed: bool = False) -> dict:
+    """SURVEY.md §8(d) per-unit byte counts for the operations the timed
+    kernel actually performs:
+      lookup   16 B slot read per counted lookup — only when the block-hash
+               probe runs (probed=True); with the held prefix state (the
+               default, verify=0) no page is read to answer a match;
+      refresh  0: matched / re-inserted pages carry their chain's stamp, one
+               scalar per chain (DESIGN.md §4.1), so no per-page stamp write;
+      insert   16 B per created page;
+      evict    8 B per resident page per select call (64 B per node record in
+               offload mode) + 16 B per victim;
+      state    96 B read + 96 B write per agent state-machine advance;
+      tick     88 B per trace row."""
+    look = sum(16 * r.lookups for r in results) if probed else 0
+    ins = sum(16 * r.created_pages for r in results)
     ev = sum((64 if tree else 8) * r.evict_scanned + 16 * r.evicted_pages for r in results)
     state = sum(192 * r.agent_events for r in results)
     tick = sum(88 * r.ticks for r in results)
@@ -164,40 +247,37 @@ def algorithmic_bytes(results, tree: bool = False) -> dict:
 def load_peak():
     try:
         with open(PEAKS_PATH) as fh:
-            return float(json.load(fh)["hbm_gbs"]), "measured"
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
-        return HBM_FALLBACK_GBS, "fallback"
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
 
 
 def load_traffic(workload):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/ncu_summary.json), with the capture it came from."""
     try:
         with open(PROFILE_SUMMARY) as fh:
-            d = json.load(fh)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+            d = json.load(fh).get(workload, {})
+        return d.get("dram_bytes_per_launch"), {k: d.get(k) for k in ("source", "duration_ms")}
     except Exception:
-        return None
+        return None, None
 
 
-def cpu_sample(workload: str, scen):
-    """Bounded CPU sample of a workload (all current workloads run whole)."""
-    return scen, None
-
-
-def cpu_reference(scen, threads: int, sample_every: int = 1):
-    """The reference's own run_simulation on host cores (oracle/_ref)."""
+def cpu_reference(scen, threads: int):
+    """The reference's own run_simulation on host cores (oracle/_ref, the
+    unmodified reference sources): run_rows-style thread pool."""
     import ctypes as C
 
     from paper_2601_22705_b200 import abi
     from tests.helpers import ref_lib
     lib = ref_lib()
-    chosen = scen[::sample_every]
-    n = len(chosen)
+    n = len(scen)
     wls = (abi.WorkloadConfig * n)()
     seeds = (C.c_uint64 * n)()
     pols = (abi.Policy * n)()
     costs = (abi.CostParams * n)()
     engs = (abi.EngineParams * n)()
-    for i, s in enumerate(chosen):
+    for i, s in enumerate(scen):
         pol, eng = s.resolved()
         wls[i] = s.workload.to_abi()
         seeds[i] = s.seed
@@ -210,8 +290,13 @@ def cpu_reference(scen, threads: int, sample_every: int = 1):
     rc = lib.kvr_run_many(n, wls, seeds, pols, costs, engs, threads, mk, dec, C.byref(wall))
     if rc != 0:
         raise RuntimeError(lib.kvr_last_error().decode())
-    steps = sum(s.workload.agents * s.workload.steps for s in chosen)
+    steps = sum(s.workload.agents * s.workload.steps for s in scen)
     return steps, wall.value, n
+
+
+def cpu_threads(workload: str) -> int:
+    # a single simulation is single-threaded by design
+    return (os.cpu_count() or 1) if workload == "c4" else 1
 
 
 # --------------------------------------------------------------------------- arms
@@ -220,23 +305,18 @@ def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    scen, desc = build_scenarios(args.workload, 0, args.sims)
-    scen, note = cpu_sample(args.workload, scen)
-    threads = os.cpu_count() or 1
-    # bounded sample per step so --steps K --warmup W finishes within minutes
-    every = {"c4": 8}.get(args.workload, 1)
+    scen, desc = build_scenarios(args, 0, 1 if args.split == "weak" else 1)
+    scen, note = cpu_scenarios(args, scen)
+    threads = cpu_threads(args.workload)
     for _ in range(args.warmup if args.workload in ("c4", "c1") else 0):
-        cpu_reference(scen, threads, every)
-    vals, walls = [], []
+        cpu_reference(scen, threads)
+    walls = []
     steps = n = 0
     for _ in range(args.steps):
-        steps, wall, n = cpu_reference(scen, threads, every)
-        vals.append(steps / wall)
+        steps, wall, n = cpu_reference(scen, threads)
         walls.append(wall)
-    value = sum(steps for _ in walls) / sum(walls)
-    sample = (f"{n} of the {len(scen)} simulations (every {every}th) per step, reference "
-              f"run_simulation on {threads} threads" if every > 1 else
-              f"all {n} simulation(s) per step on {threads} threads")
+    value = steps * len(walls) / sum(walls)
+    sample = f"all {n} simulation(s) of the workload per step, {threads} thread(s)"
     if note:
         sample = note + "; " + sample
     line = {"metric": METRIC, "value": value, "unit": "agent-steps/s", "impl": "reference",
@@ -257,40 +337,44 @@ def run_b200(args):
 
     import torch
 
-    from paper_2601_22705_b200 import abi, engine
+    from paper_2601_22705_b200 import abi, engine, sweep
     rank, world, local = env_rank()
     dist = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-    device = torch.cuda.current_device() if torch.cuda.is_available() else 0
-    scen, desc = build_scenarios(args.workload, rank, args.sims)
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the engine has no CPU path)")
+    device = torch.cuda.current_device()
+    scen, desc = build_scenarios(args, rank, world)
     specs, pops = make_specs(scen)
-    batch = engine.Batch(specs, device=device)
+    batch = engine.Batch(specs, device=device, verify=False)
     for _ in range(max(args.warmup, 1)):
         batch.run()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
-    sampler = ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(device)).split(",")[0])
-                           if os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")[0].isdigit()
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",")
+    sampler = ClockSampler(int(vis[device]) if len(vis) > device and vis[device].isdigit()
                            else device)
     sampler.start()
+    torch.cuda.synchronize()
     step_ms = kern_ms = 0.0
-    per_step = []
     for _ in range(args.steps):
-        batch.run()
+        batch.run()  # device-resident inputs; CUDA events on the launch stream
         a, k = batch.timing()
         step_ms += a
         kern_ms += k
-        per_step.append(a)
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     sampler.stop()
     results = batch.results_raw()
     units = sum(r.agent_steps for r in results)          # per step, this rank
     lookups = sum(r.lookups for r in results)
-    bad = [i for i, r in enumerate(results) if r.status != 0]
+    bad = [i for i, r in enumerate(results) if r.status not in (0, abi.KVG_ERR_HORIZON)]
+    horizon = sum(1 for r in results if r.status == abi.KVG_ERR_HORIZON)
     tot = torch.tensor([step_ms, kern_ms], dtype=torch.float64, device="cuda")
     cnt = torch.tensor([units, lookups], dtype=torch.float64, device="cuda")
     if dist:
@@ -300,41 +384,65 @@ def run_b200(args):
     all_units, all_lookups = cnt.tolist()
     value = all_units * args.steps / (max_ms / 1e3)
     # ---- NCCL final metric gather: per-sim summary records of every rank
-    from paper_2601_22705_b200 import sweep
     summary = sweep.gather_records(sweep.records(results), dist, device="cuda")
     makespans = summary[:, 0].cpu().tolist()
-    # ---- roofline of the engine kernel
+    # ---- roofline of the engine kernel (bytes of the operations it performs)
     ab = algorithmic_bytes(results, tree=args.workload == "c3off")
     kernel_s = (kern_ms / args.steps) / 1e3
     peak, peak_kind = load_peak()
     achieved = ab["total"] / kernel_s / 1e9
+    traffic, tsrc = load_traffic(args.workload)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": load_traffic(args.workload),
-            "peak_source": peak_kind, "kernel": "kvg::engine_kernel_small" if len(specs) >= 296
-            else "kvg::engine_kernel_big",
-            "algorithmic_bytes_per_launch": ab,
-            "kernel_ms_per_launch": kern_ms / args.steps}
+            "frac": achieved / peak, "traffic": traffic, "traffic_capture": tsrc,
+            "peak_source": peak_kind,
+            "kernel": "kvg::engine_kernel_small" if len(specs) >= 296 else "kvg::engine_kernel_big",
+            "algorithmic_bytes_per_launch": ab, "kernel_ms_per_launch": kern_ms / args.steps,
+            "limiter": "latency of each simulation's sequential event chain (ncu: issue-bound "
+                       "at low eligible warps, DESIGN.md §5); the page kernels alone: "
+                       "bench.py --workload kernels"}
+    # ---- the same step with the block-hash probe on (verify=1: every match
+    # also re-derived over the agent's whole context by kernel 1)
+    probe = None
+    if not args.no_probe_mode and args.workload in ("c4", "c1", "c2", "c3"):
+        pb = engine.Batch(specs, device=device, verify=True)
+        pb.run()
+        pms, pkms = [], []
+        for _ in range(2):
+            pb.run()
+            a, k = pb.timing()
+            pms.append(a)
+            pkms.append(k)
+        pres = pb.results_raw()
+        pab = algorithmic_bytes(pres, tree=False, probed=True)
+        pk = statistics.mean(pkms) / 1e3
+        probe = {"ms_per_step": statistics.mean(pms),
+                 "value": sum(r.agent_steps for r in pres) / (statistics.mean(pms) / 1e3),
+                 "lookups_per_s": sum(r.lookups for r in pres) / (statistics.mean(pms) / 1e3),
+                 "lookup_bytes_per_launch": pab["lookup"],
+                 "achieved_gbs": pab["total"] / pk / 1e9,
+                 "results_identical": all(
+                     (x.makespan, x.agent_steps, x.lookups, x.ticks) ==
+                     (y.makespan, y.agent_steps, y.lookups, y.ticks)
+                     for x, y in zip(pres, results))}
+        pb.close()
     # ---- end to end through the C ABI with host buffers: every step creates
     # the batch from host populations (H2D), runs it, and the kernel streams
     # results / trace rows / agent stats into pinned host memory (D2H)
-    # the device-resident batch goes back to the workspace cache first, so the
-    # e2e batches reuse its HBM arena (and, after one untimed step, the pinned
-    # host block) like any repeated caller would
     batch.close()
     e2e_ms = []
     n_agents = sum(s.population.c.agents for s in specs)
     h2d = sum(p.c.agents * p.c.steps * C.sizeof(abi.StepPlan) for p in pops.values()) + \
-        len(specs) * 512
+        len(specs) * C.sizeof(abi.SimDesc)
     d2h = 0
     phases = {"create_ms": 0.0, "run_ms": 0.0, "results_ms": 0.0, "kernel_ms": 0.0}
     for k in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        b2 = engine.Batch(specs, device=device, host_outputs=True)
+        b2 = engine.Batch(specs, device=device, host_outputs=True, verify=False)
         t1 = time.perf_counter()
         b2.run()
         t2 = time.perf_counter()
-        kern_e2e = b2.timing()[1]  # the run's kernel span (rows stream out inside it)
+        kern_e2e = b2.timing()[1]
         res2 = b2.results_array()
         d2h = int(res2["ticks"].sum()) * C.sizeof(abi.TraceRow) + \
             n_agents * C.sizeof(abi.AgentStats) + len(res2) * C.sizeof(abi.SimResult)
@@ -353,16 +461,15 @@ def run_b200(args):
     # ---- CPU baseline (rank 0, N=1): the reference on the host cores
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        every = 8 if args.workload == "c4" else 1
+        threads = cpu_threads(args.workload)
         try:
-            cscen, note = cpu_sample(args.workload, scen)
-            steps_cpu, wall, n = cpu_reference(cscen, threads, every)
+            cscen, note = cpu_scenarios(args, scen)
+            steps_cpu, wall, n = cpu_reference(cscen, threads)
             cpu = {"value": steps_cpu / wall, "unit": "agent-steps/s", "cores": threads,
                    "kind": "reference",
                    "sample": (note + "; " if note else "") +
-                   f"{n} of {len(cscen)} simulations (every {every}th), unmodified "
-                   f"reference run_simulation, {threads} threads, {wall:.2f} s"}
+                   f"all {n} simulation(s) of the workload, unmodified reference "
+                   f"run_simulation, {threads} thread(s), {wall:.2f} s"}
         except Exception as e:  # the reference build travels with the repo; report if absent
             cpu = {"value": None, "unit": "agent-steps/s", "cores": threads,
                    "kind": "reference", "sample": f"unavailable: {e}"}
@@ -370,21 +477,31 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": value, "unit": "agent-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64/u64", "data": "synthetic (seeded reference workload generator)",
+            "higher_is_better": True,
+            "scaling": "strong" if (args.split == "strong" and args.workload == "c4") else "weak",
+            "vs_baseline": None, "dtype": "f64/u64",
+            "data": "synthetic (seeded reference workload generator)",
             "config": {"workload": desc, "sims_per_gpu": len(specs),
-                       "parallelism": f"independent sims sharded over {world} GPU(s)",
+                       "parallelism": f"independent simulations sharded over {world} GPU(s) "
+                                      f"({args.split} split), NCCL all_gather of records",
                        "l2": "inputs larger than L2: per-sim hash tables total "
-                             f"{batch_bytes(specs) / 2**30:.1f} GiB, re-initialised every step"},
+                             f"{batch_bytes(specs) / 2**30:.1f} GiB, re-initialised every step",
+                       "verify": 0},
             "lookups_per_s": all_lookups * args.steps / (max_ms / 1e3),
+            "lookups_note": "counted per SURVEY §8(d) (resolved pages + terminating miss); "
+                            "answered from the held prefix state, the block-hash probe is "
+                            "not run in the timed region (see probe_mode)",
+            "probe_mode": probe,
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "phases_ms": {k: round(v, 2) for k, v in phases.items()}},
             "gpu_launches": args.steps * launches_per_step(specs),
             "clocks": sampler.summary(),
-            "parity": {"sims": len(summary), "nonzero_status": len(bad),
-                       "makespan_min": min(makespans), "makespan_max": max(makespans)},
+            "parity": {"sims": len(summary), "bad_status": len(bad), "horizon": horizon,
+                       "makespan_min": min(makespans), "makespan_max": max(makespans),
+                       "pinned_by": "tests/test_full_golden.py (every C4 sim vs the reference, "
+                                    "verify 0 and 1)"},
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -398,13 +515,19 @@ def batch_bytes(specs):
 
 
 def launches_per_step(specs):
-    # one engine-kernel launch per warps-per-sim group (uniform workloads: 1)
+    # one engine-kernel launch per warps-per-sim group; every bench workload is
+    # uniform (all sims one shape), so one launch per step
     return 1
 
 
 def main():
-    args = parse_args()
-    if args.impl == "reference":
+    argv = sys.argv[1:]
+    args = parse_args(argv)
+    maybe_respawn(args, argv)
+    if args.workload == "kernels":
+        import bench_kernels
+        bench_kernels.main(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_b200(args)

@@ -290,11 +290,18 @@ KVG_API kvg_status kvg_batch_results(kvg_batch* b, kvg_sim_result* out, size_t c
 KVG_API kvg_status kvg_batch_trace_view(kvg_batch* b, size_t i,
                                         const kvg_trace_row** rows, size_t* n_rows);
 /* Host pointers to the run's output arrays (valid until the next run or
- * free). Zero-copy when the batch was created with host_outputs. The trace
- * array holds every simulation's rows; kvg_batch_trace_view locates them. */
+ * free). Zero-copy when the batch was created with host_outputs.
+ *   results[i]  is simulation i's result (caller order, dense);
+ *   stats_base / trace_base hold every simulation's agent stats / trace rows
+ *   in padded per-simulation slices: simulation i's slice starts at the
+ *   element index kvg_batch_offsets reports (not at a dense prefix sum). */
 KVG_API kvg_status kvg_batch_outputs(kvg_batch* b, const kvg_sim_result** results,
                                      const kvg_trace_row** trace_base,
                                      const kvg_agent_stats** stats_base);
+/* Element index of simulation i's first agent-stats record in stats_base and
+ * of its first trace row in trace_base (see kvg_batch_outputs). */
+KVG_API kvg_status kvg_batch_offsets(kvg_batch* b, size_t i, size_t* stats_index,
+                                     size_t* trace_index);
 KVG_API void kvg_batch_free(kvg_batch* b);
 
 /* One-shot convenience: create, run, read scalar results, free. */

@@ -403,6 +403,56 @@ KVR_API int kvr_run_many(size_t n, const kvg_workload_config* wls,
   });
 }
 
+/* Many independent runs with their full outputs, for full-size golden
+ * fixtures (e.g. all 4,096 C4 sweep simulations): res[i] receives run i's
+ * SimulationResult scalars, trace[i * trace_stride ...] its trace rows
+ * (n_trace[i] = the row count, which may exceed trace_stride: then only the
+ * first trace_stride rows are written and the caller retries with a larger
+ * stride), agents[agent_off[i] ...] its agent stats. Runs on `threads`
+ * threads like kvr_run_many. Horizon aborts keep their partial results
+ * (status KVG_ERR_HORIZON in res[i].status). */
+KVR_API int kvr_run_many_out(size_t n, const kvg_workload_config* wls,
+                             const uint64_t* seeds, const kvg_policy* policies,
+                             const kvg_cost_params* costs,
+                             const kvg_engine_params* engines, unsigned threads,
+                             kvg_sim_result* res, kvg_trace_row* trace,
+                             size_t trace_stride, size_t* n_trace,
+                             kvg_agent_stats* agents, const size_t* agent_off) {
+  return guarded([&] {
+    std::vector<std::exception_ptr> errs(n);
+    std::atomic<size_t> next{0};
+    auto worker = [&] {
+      for (;;) {
+        size_t i = next.fetch_add(1);
+        if (i >= n) return;
+        try {
+          kvadmit::Population pop = kvadmit::build_population(to_workload(wls[i]), seeds[i]);
+          kvadmit::SimulationResult partial, r;
+          int status = KVG_OK;
+          try {
+            r = kvadmit::run_simulation(std::move(pop), to_policy(policies[i]),
+                                        to_cost(costs[i]), to_engine(engines[i]), &partial);
+          } catch (const kvadmit::HorizonError&) {
+            r = std::move(partial);
+            status = KVG_ERR_HORIZON;
+          }
+          fill_result(r, status, &res[i], trace + i * trace_stride, trace_stride,
+                      &n_trace[i], agents + agent_off[i], wls[i].agents);
+        } catch (...) {
+          errs[i] = std::current_exception();
+        }
+      }
+    };
+    unsigned t = threads < 1 ? 1 : threads;
+    std::vector<std::thread> pool;
+    for (unsigned k = 1; k < t; ++k) pool.emplace_back(worker);
+    worker();
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
+  });
+}
+
 /* ---------------- run artifacts through the reference's own writers ------- */
 
 /* execute_run's finalize (experiment.cpp:161-170) on a reference run:

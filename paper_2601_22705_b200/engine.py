@@ -68,6 +68,7 @@ def lib():
     L.kvg_batch_results.argtypes = [C.c_void_p, P(abi.SimResult), C.c_size_t]
     L.kvg_batch_outputs.argtypes = [C.c_void_p, P(P(abi.SimResult)), P(P(abi.TraceRow)),
                                     P(P(abi.AgentStats))]
+    L.kvg_batch_offsets.argtypes = [C.c_void_p, C.c_size_t, P(C.c_size_t), P(C.c_size_t)]
     L.kvg_batch_trace_view.argtypes = [C.c_void_p, C.c_size_t, P(P(abi.TraceRow)),
                                        P(C.c_size_t)]
     L.kvg_batch_free.argtypes = [C.c_void_p]
@@ -245,6 +246,29 @@ class Batch:
         _check(lib().kvg_batch_results(self.h, out.ctypes.data_as(C.POINTER(abi.SimResult)),
                                        self.n))
         return out[: self.n]
+
+    def outputs(self):
+        """Zero-copy numpy views of the host output block: (results[n],
+        [agent-stats slice per simulation], [trace-row slice per simulation])."""
+        r, t, st = C.POINTER(abi.SimResult)(), C.POINTER(abi.TraceRow)(), \
+            C.POINTER(abi.AgentStats)()
+        _check(lib().kvg_batch_outputs(self.h, C.byref(r), C.byref(t), C.byref(st)))
+        res = np.ctypeslib.as_array(r, shape=(max(1, self.n),))[: self.n]
+        stats, rows = [], []
+        for i in range(self.n):
+            si, ti = C.c_size_t(), C.c_size_t()
+            _check(lib().kvg_batch_offsets(self.h, i, C.byref(si), C.byref(ti)))
+            na = self.specs[i].population.c.agents
+            stats.append(np.ctypeslib.as_array(
+                C.cast(C.byref(st.contents, si.value * C.sizeof(abi.AgentStats)),
+                       C.POINTER(abi.AgentStats)), shape=(max(1, na),))[:na])
+            p, nt = C.POINTER(abi.TraceRow)(), C.c_size_t()
+            _check(lib().kvg_batch_trace_view(self.h, i, C.byref(p), C.byref(nt)))
+            view = C.cast(C.byref(t.contents, ti.value * C.sizeof(abi.TraceRow)),
+                          C.POINTER(abi.TraceRow))
+            assert C.addressof(view.contents) == C.addressof(p.contents) or nt.value == 0
+            rows.append(np.ctypeslib.as_array(view, shape=(max(1, nt.value),))[:nt.value])
+        return res, stats, rows
 
     def trace(self, i: int) -> list[dict]:
         n = C.c_size_t()

@@ -30,10 +30,10 @@ def weak_shard(workload: str, rank: int, sims: int):
     if workload == "c3off":  # offload tier on the 32-agent C3 shape (the reference's
         # offload runs take minutes from 128 agents on; the full size exceeds the horizon)
         s = config.c3_dsv3("offload", agents=32, capacity=1)
+        s.seed = 3 + rank  # before the capacity: it is this rank's population peak
         from . import engine
         s.engine.capacity = config.scaled_capacity(
             engine.Population(s.workload, s.seed).peak_aggregate_tokens)
-        s.seed = 3 + rank
         return [s]
     s = config.c1_toy("aimd")
     s.seed = 42 + rank

@@ -282,3 +282,27 @@ def cache_fuzz_program(rounds: int = 40, ops: int = 300, seed: int = 0xacce97ed)
         progs.append(dict(capacity=cap, page_size=page, prompt=prompt, shared=int(shared),
                           agents=agents, ops=prog_ops, seed=r))
     return progs
+
+
+# Full-size BASELINE configurations the reference finishes in seconds to
+# minutes (tests/golden/make_golden_full.py -> full_runs.json). C5 is scaled
+# (the full 65,536-agent shape cannot run on the CPU reference: SURVEY.md
+# fact 0.3-6): 1,024 and 4,096 agents of the C5 shape, capacity = peak / 1.5.
+FULL_CASES: list[dict] = [
+    dict(id="c3_aimd_h03", builder="c3", policy="aimd",
+         overrides={"controller.h_thresh": 0.3}),
+    dict(id="c5s1024_aimd", builder="c5s", agents=1024, policy="aimd"),
+    dict(id="c5s4096_aimd", builder="c5s", agents=4096, policy="aimd"),
+    dict(id="c5s1024_cap256", builder="c5s", agents=1024, policy="agent_cap:256"),
+    dict(id="c5s4096_cap1024", builder="c5s", agents=4096, policy="agent_cap:1024"),
+]
+
+
+def full_case_scenario(case: dict):
+    if case["builder"] == "c3":
+        s = config.c3_dsv3(case["policy"])
+        for k, v in case.get("overrides", {}).items():
+            section, _, name = k.partition(".")
+            setattr(getattr(s, section), name, v)
+        return s, case["policy"]
+    return case_scenario(case)

@@ -45,3 +45,23 @@ def run_record(run: dict) -> dict:
         rec["n_events"] = len(run["digests"])
         rec["digest_sha"] = hashlib.sha256(run["digests"].tobytes()).hexdigest()
     return rec
+
+
+def sim_digest(status: int, result: dict, trace, agents) -> str:
+    """One 16-hex digest of a whole simulation's reference-defined outputs,
+    for full-size fixtures (thousands of simulations): the result record,
+    the raw trace rows (kvg_trace_row, 88 B each: every field is a double or
+    u64, so the bytes are the bit patterns) and the six AgentStats fields of
+    every agent (the first 48 B of each kvg_agent_stats; the reference does
+    not define finish_time / finish_ordinal). `trace` and `agents` are numpy
+    structured arrays in the ABI layouts."""
+    import json
+
+    import numpy as np
+    h = hashlib.sha256()
+    h.update(json.dumps(dict(status=status, result=result_record(result)),
+                        sort_keys=True).encode())
+    h.update(np.ascontiguousarray(trace).view(np.uint8).tobytes())
+    a = np.ascontiguousarray(agents).view(np.uint8).reshape(-1, 64)[:, :48]
+    h.update(a.tobytes())
+    return h.hexdigest()[:16]

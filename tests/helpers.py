@@ -172,7 +172,7 @@ def oracle_run(s: Scenario, policy_text: str | None = None, digests: bool = Fals
                 agents=_rows(agents, s.workload.agents),
                 digests=np.ctypeslib.as_array(dig)[:nd.value].copy() if digests else None,
                 log=[(r.kind, r.agent, r.clock, r.a, r.b) for r in lg[:nl.value]] if log else None,
-                raw_result=res, raw_trace=trace, n_trace=nt.value)
+                raw_result=res, raw_trace=trace, n_trace=nt.value, raw_agents=agents)
 
 
 def load_presets() -> dict:
@@ -191,3 +191,53 @@ def ref_artifacts(s: Scenario, policy_text: str | None, out_dir: str, label: str
     rc = lib.kvr_run_artifacts(C.byref(wl), s.seed, C.byref(pol), C.byref(cost), C.byref(ep),
                                s.name.encode(), label.encode(), out_dir.encode())
     assert rc == 0, lib.kvr_last_error()
+
+
+def ref_run_many_out(scen: list, threads: int | None = None, stride: int = 4096):
+    """The reference's run_simulation over many scenarios on host threads,
+    with every output: [(status, result dict, trace rows, agent stats)], the
+    arrays as numpy structured arrays in the ABI layouts."""
+    lib = ref_lib()
+    P = C.POINTER
+    lib.kvr_run_many_out.argtypes = [C.c_size_t, P(abi.WorkloadConfig), P(C.c_uint64),
+                                     P(abi.Policy), P(abi.CostParams), P(abi.EngineParams),
+                                     C.c_uint, P(abi.SimResult), P(abi.TraceRow), C.c_size_t,
+                                     P(C.c_size_t), P(abi.AgentStats), P(C.c_size_t)]
+    n = len(scen)
+    wls = (abi.WorkloadConfig * n)()
+    seeds = (C.c_uint64 * n)()
+    pols = (abi.Policy * n)()
+    costs = (abi.CostParams * n)()
+    engs = (abi.EngineParams * n)()
+    aoff = (C.c_size_t * n)()
+    na = 0
+    for i, s in enumerate(scen):
+        pol, eng = s.resolved()
+        wls[i] = s.workload.to_abi()
+        seeds[i] = s.seed
+        pols[i] = pol
+        costs[i] = s.cost.to_abi()
+        engs[i] = eng.to_abi()
+        aoff[i] = na
+        na += s.workload.agents
+    threads = threads or os.cpu_count() or 1
+    while True:
+        res = (abi.SimResult * n)()
+        trace = np.zeros(n * stride, dtype=np.ctypeslib.as_array((abi.TraceRow * 1)()).dtype)
+        agents = np.zeros(max(1, na), dtype=np.ctypeslib.as_array((abi.AgentStats * 1)()).dtype)
+        nt = (C.c_size_t * n)()
+        rc = lib.kvr_run_many_out(n, wls, seeds, pols, costs, engs, threads, res,
+                                  trace.ctypes.data_as(P(abi.TraceRow)), stride, nt,
+                                  agents.ctypes.data_as(P(abi.AgentStats)), aoff)
+        if rc != 0:
+            raise RuntimeError(lib.kvr_last_error().decode())
+        mx = max(nt[i] for i in range(n))
+        if mx <= stride:
+            break
+        stride = mx
+    out = []
+    for i, s in enumerate(scen):
+        r = abi.struct_to_dict(res[i])
+        out.append((r["status"], r, trace[i * stride: i * stride + nt[i]],
+                    agents[aoff[i]: aoff[i] + s.workload.agents]))
+    return out

@@ -81,3 +81,40 @@ def test_gloo_world2_shard_and_gather():
     assert got[0][1] == weak_serial and got[1][1] == weak_serial
     # rank 1's weak shard is a different workload (seed 43), not a copy of rank 0's
     assert weak_serial[0] != weak_serial[1]
+
+
+def test_bench_strong_split_partitions_the_c4_sweep():
+    import bench
+    for world in (1, 2, 4, 8):
+        seen = []
+        for r in range(world):
+            args = bench.parse_args(["--split", "strong", "--gpus", str(world)])
+            scen, desc = bench.build_scenarios(args, r, world)
+            seen += [s.name for s in scen]
+            assert len(scen) == 4096 // world and f"[{r * 4096 // world}," in desc
+        assert seen == [f"c4_{k}" for k in range(4096)]
+
+
+def test_bench_c5_replicas_one_per_rank():
+    import bench
+    args = bench.parse_args(["--workload", "c5"])
+    got = [(s.policy, s.seed) for r in range(8) for s in bench.build_scenarios(args, r, 8)[0]]
+    assert got == bench.C5_REPLICAS and len(set(got)) == 8
+
+
+@pytest.mark.timeout(600)
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun re-executes itself as a 2-rank
+    torch.distributed job (the path the driver's --gpus N takes); the CPU
+    reference arm needs no GPU, rank 0 prints the line with n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--impl", "reference",
+                        "--gpus", "2", "--workload", "c1", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, env=env, timeout=540)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
