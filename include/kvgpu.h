@@ -200,6 +200,10 @@ typedef struct kvg_sim_result {
   uint64_t agent_events;    /* agent state-machine advances                   */
   uint64_t device_cycles;   /* SM clock cycles this simulation ran (device)   */
   kvg_phase_label phases[3];
+  /* status KVG_ERR_HORIZON: the event time that passed the horizon and the
+   * agents still unfinished (HorizonError's message, engine.cpp:112-119) */
+  double abort_time;
+  uint64_t unfinished;
 } kvg_sim_result;
 
 /* Optional per-simulation event log (parity testing). */
@@ -469,6 +473,30 @@ KVG_API kvg_status kvg_cache_victims(const kvg_cache* c, size_t begin,
 KVG_API kvg_status kvg_cache_hit_window(const kvg_cache* c, double* matched,
                                         double* requested);
 KVG_API void kvg_cache_free(kvg_cache* c);
+
+/* Grid-wide page-table kernels (discard mode). kvg_cache_exec runs an EVICT
+ * op as ONE cooperative launch over every SM (shared-memory radix-select
+ * histograms merged once per digit pass) instead of on the one-CTA executor:
+ *   KVG_GRID_AUTO   when the table has >= 4096 claimed buckets (default),
+ *   KVG_GRID_NEVER  never, KVG_GRID_ALWAYS always.
+ * record_victims = 0 stops appending victims to the handle's victim list
+ * (bulk evictions of millions of pages; counts are still returned). */
+enum { KVG_GRID_AUTO = 0, KVG_GRID_NEVER = 1, KVG_GRID_ALWAYS = 2 };
+KVG_API kvg_status kvg_cache_configure(kvg_cache* c, uint32_t grid_mode,
+                                       uint32_t record_victims);
+/* n match_prefix calls (cache_tree.cpp:114-142) in one grid launch: agent
+ * agents[i]'s owner-form sequence of lens[i] tokens. Leaves the cache (clock,
+ * page stamps, summaries, hit window) and results[i] exactly as n successive
+ * KVG_OP_MATCH ops through kvg_cache_exec would: query i runs at clock
+ * clock0 + i + 1 and a page's final stamp is that of the last query covering
+ * it. One warp per query over all SMs. Discard mode only. */
+KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
+                                         const uint64_t* lens, size_t n,
+                                         kvg_cache_op_result* results);
+/* Device time (CUDA events on the launching stream) of the kernels of the
+ * last kvg_cache_exec / kvg_cache_match_batch call, ms; grid_blocks = CTAs
+ * of the last grid-wide eviction. */
+KVG_API kvg_status kvg_cache_last_ms(const kvg_cache* c, double* ms, uint32_t* grid_blocks);
 
 #ifdef __cplusplus
 } /* extern "C" */

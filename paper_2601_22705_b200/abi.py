@@ -117,7 +117,7 @@ class SimResult(C.Structure):
                 ("hit_matched", f64), ("hit_requested", f64),
                 ("hit_pages", u64), ("created_pages", u64), ("refreshed_pages", u64),
                 ("evict_scanned", u64), ("agent_events", u64), ("device_cycles", u64),
-                ("phases", PhaseLabel * 3)]
+                ("phases", PhaseLabel * 3), ("abort_time", f64), ("unfinished", u64)]
 
 
 class LogRecord(C.Structure):

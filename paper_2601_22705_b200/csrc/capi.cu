@@ -130,6 +130,11 @@ cudaError_t exec(void* d_state, const kvg_cache_op* d_ops, unsigned n, kvg_cache
 cudaError_t hit_window(const void* d_state, double* m, double* r);
 }  // namespace kvg_tree_seam
 
+namespace kvg_grid_seam {  // engine.cu
+cudaError_t match(const kvg::GridMatchArgs& a, cudaStream_t s);
+cudaError_t evict(const kvg::GridEvictArgs& a, cudaStream_t s, unsigned* blocks_out);
+}  // namespace kvg_grid_seam
+
 struct kvg_cache {
   int device = 0;
   bool offload = false;
@@ -144,7 +149,156 @@ struct kvg_cache {
   u64 victim_cap = 0;
   std::vector<kvg_victim> victims;  // host copy, sorted per op
   double hit_m = 0, hit_r = 0;
+  // grid-wide kernels (grid.cuh): scratch, routing mode, last device time
+  uint32_t grid_mode = KVG_GRID_AUTO;
+  uint32_t record_victims = 1;
+  char* gscratch = nullptr;  // [ghist 3*2*2048 u32 | freed | err | work | pad]
+  u32* d_best = nullptr;     // [shared_pages + 1]
+  char* gq = nullptr;        // match-batch query arrays
+  size_t gq_cap = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double last_ms = 0;
+  unsigned last_blocks = 0;
 };
+
+namespace {
+
+constexpr size_t kGHistBytes = 3 * 2 * kvg::kGridBins * sizeof(u32);
+constexpr u64 kGridAutoBuckets = 4096;  // claimed buckets from which EVICT goes grid-wide
+
+kvg_status cache_state(kvg_cache* c, kvg::CacheState* st) {
+  CUDA_TRY(cudaMemcpy(st, c->d_state, sizeof *st, cudaMemcpyDeviceToHost));
+  return KVG_OK;
+}
+
+// evict(k) as one cooperative launch over every SM (grid_evict_kernel).
+kvg_status grid_evict(kvg_cache* c, const kvg_cache_op& o, kvg_cache_op_result* r) {
+  kvg::CacheState st{};
+  kvg_status rc = cache_state(c, &st);
+  if (rc != KVG_OK) return rc;
+  const u64 k = o.arg, e = st.used - st.pinned_pages;
+  *r = kvg_cache_op_result{};
+  r->status = KVG_OK;
+  r->clock = st.clock;
+  r->used = st.used;
+  r->victims_begin = r->victims_end = st.n_victims;
+  if (k == 0 || e == 0) return KVG_OK;  // cache_tree.cpp:272 (and nothing evictable)
+  const bool sw = st.swapped & 1;
+  kvg::GridEvictArgs a{};
+  a.table = sw ? c->h.alt : c->h.table;
+  a.summ = sw ? c->h.alt_summ : c->h.summ;
+  a.occ = sw ? c->h.alt_occ : c->h.occ;
+  a.occ_n = static_cast<u32>(st.occ_n);
+  a.mask = c->h.bucket_mask;
+  a.S = c->shared_pages;
+  a.k = k;
+  a.evictable = e;
+  a.clock = st.clock;
+  a.vic = c->record_victims ? c->d_victims : nullptr;
+  a.vic_cap = c->victim_cap;
+  a.vic_n = reinterpret_cast<unsigned long long*>(
+      reinterpret_cast<char*>(c->d_state) + offsetof(kvg::CacheState, n_victims));
+  a.ghist = reinterpret_cast<u32*>(c->gscratch);
+  a.freed = reinterpret_cast<unsigned int*>(c->gscratch + kGHistBytes);
+  a.err = reinterpret_cast<int*>(c->gscratch + kGHistBytes + 4);
+  CUDA_TRY(cudaMemset(c->gscratch, 0, kGHistBytes + 8));
+  CUDA_TRY(cudaEventRecord(c->ev0));
+  CUDA_TRY(kvg_grid_seam::evict(a, 0, &c->last_blocks));
+  CUDA_TRY(cudaEventRecord(c->ev1));
+  CUDA_TRY(cudaEventSynchronize(c->ev1));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->last_ms += ms;
+  unsigned int freed = 0;
+  int err = 0;
+  CUDA_TRY(cudaMemcpy(&freed, a.freed, 4, cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&err, a.err, 4, cudaMemcpyDeviceToHost));
+  st.used -= freed;
+  st.discarded += static_cast<u64>(freed) * c->page_size;
+  kvg::CacheState cur{};
+  rc = cache_state(c, &cur);  // n_victims advanced on the device
+  if (rc != KVG_OK) return rc;
+  st.n_victims = cur.n_victims;
+  CUDA_TRY(cudaMemcpy(c->d_state, &st, sizeof st, cudaMemcpyHostToDevice));
+  if (st.n_victims > c->victim_cap)
+    return (kvg_status)set_error(KVG_ERR_STATE, "victim list overflow");
+  const u64 base = r->victims_begin;
+  c->victims.resize(st.n_victims);
+  if (st.n_victims > base)
+    CUDA_TRY(cudaMemcpy(c->victims.data() + base, c->d_victims + base,
+                        (st.n_victims - base) * sizeof(kvg_victim), cudaMemcpyDeviceToHost));
+  r->status = err ? KVG_ERR_STATE : KVG_OK;
+  r->r0 = freed;
+  r->used = st.used;
+  r->victims_end = st.n_victims;
+  return KVG_OK;
+}
+
+}  // namespace
+
+namespace {
+
+// Victims of one op in the reference's eviction order: stamp ascending, the
+// deeper page of equal stamps first (cache_tree.cpp:270-319).
+void sort_victims(kvg_cache* c, const kvg_cache_op_result& r) {
+  if (r.victims_end > c->victims.size() || r.victims_begin >= r.victims_end) return;
+  std::sort(c->victims.begin() + r.victims_begin, c->victims.begin() + r.victims_end,
+            [](const kvg_victim& x, const kvg_victim& y) {
+              if (x.stamp != y.stamp) return x.stamp < y.stamp;
+              return (x.key & 0xffffffffull) > (y.key & 0xffffffffull);
+            });
+}
+
+bool use_grid_evict(kvg_cache* c) {
+  if (c->grid_mode == KVG_GRID_NEVER) return false;
+  if (c->grid_mode == KVG_GRID_ALWAYS) return true;
+  kvg::CacheState st{};
+  if (cache_state(c, &st) != KVG_OK) return false;
+  return st.occ_n >= kGridAutoBuckets;
+}
+
+// ops executed in order by the one-CTA executor (cache.cuh).
+kvg_status exec_cta(kvg_cache* c, const kvg_cache_op* ops, size_t n,
+                    kvg_cache_op_result* results) {
+  kvg_cache_op* d_ops = nullptr;
+  kvg_cache_op_result* d_res = nullptr;
+  CUDA_TRY(cudaMalloc(&d_ops, n * sizeof(kvg_cache_op)));
+  CUDA_TRY(cudaMalloc(&d_res, n * sizeof(kvg_cache_op_result)));
+  CUDA_TRY(cudaMemcpy(d_ops, ops, n * sizeof(kvg_cache_op), cudaMemcpyHostToDevice));
+  // victims of this call are appended after the ones already collected
+  kvg::CacheState st{};
+  CUDA_TRY(cudaMemcpy(&st, c->d_state, sizeof st, cudaMemcpyDeviceToHost));
+  const u64 base = st.n_victims;
+  kvg::CacheDev h = c->h;
+  if (!c->record_victims) h.victims = nullptr;
+  h.n_ops = static_cast<u32>(n);
+  h.ops = d_ops;
+  h.results = d_res;
+  CUDA_TRY(cudaMemcpy(c->d, &h, sizeof h, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaEventRecord(c->ev0));
+  kvg::cache_kernel<<<1, 256>>>(c->d);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(c->ev1));
+  CUDA_TRY(cudaEventSynchronize(c->ev1));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->last_ms += ms;
+  CUDA_TRY(cudaMemcpy(results, d_res, n * sizeof(kvg_cache_op_result), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemcpy(&st, c->d_state, sizeof st, cudaMemcpyDeviceToHost));
+  cudaFree(d_ops);
+  cudaFree(d_res);
+  if (st.n_victims > c->victim_cap)
+    return (kvg_status)set_error(KVG_ERR_STATE, "victim list overflow");
+  c->victims.resize(st.n_victims);
+  if (st.n_victims > base)
+    CUDA_TRY(cudaMemcpy(c->victims.data() + base, c->d_victims + base,
+                        (st.n_victims - base) * sizeof(kvg_victim), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < n; ++i) sort_victims(c, results[i]);
+  return KVG_OK;
+}
+
+
+}  // namespace
 
 extern "C" {
 
@@ -244,6 +398,10 @@ KVG_API kvg_status kvg_cache_create(int device, uint64_t capacity, uint64_t page
   c->h.summ = reinterpret_cast<kvg::Summ*>(sp);
   c->h.alt_summ = reinterpret_cast<kvg::Summ*>(sp + sb);
   CUDA_TRY(cudaMemset(c->d_state, 0, sizeof(kvg::CacheState)));
+  CUDA_TRY(cudaMalloc(&c->gscratch, kGHistBytes + 64));
+  CUDA_TRY(cudaMalloc(&c->d_best, (c->shared_pages + 1) * sizeof(u32)));
+  CUDA_TRY(cudaEventCreate(&c->ev0));
+  CUDA_TRY(cudaEventCreate(&c->ev1));
   *out = c;
   return KVG_OK;
 }
@@ -276,41 +434,28 @@ KVG_API kvg_status kvg_cache_exec(kvg_cache* c, const kvg_cache_op* ops, size_t 
     CUDA_TRY(kvg_tree_seam::hit_window(c->tree_state, &c->hit_m, &c->hit_r));
     return KVG_OK;
   }
-  kvg_cache_op* d_ops = nullptr;
-  kvg_cache_op_result* d_res = nullptr;
-  CUDA_TRY(cudaMalloc(&d_ops, n * sizeof(kvg_cache_op)));
-  CUDA_TRY(cudaMalloc(&d_res, n * sizeof(kvg_cache_op_result)));
-  CUDA_TRY(cudaMemcpy(d_ops, ops, n * sizeof(kvg_cache_op), cudaMemcpyHostToDevice));
-  // victims of this call are appended after the ones already collected
-  kvg::CacheState st{};
-  CUDA_TRY(cudaMemcpy(&st, c->d_state, sizeof st, cudaMemcpyDeviceToHost));
-  const u64 base = st.n_victims;
-  kvg::CacheDev h = c->h;
-  h.n_ops = static_cast<u32>(n);
-  h.ops = d_ops;
-  h.results = d_res;
-  CUDA_TRY(cudaMemcpy(c->d, &h, sizeof h, cudaMemcpyHostToDevice));
-  kvg::cache_kernel<<<1, 256>>>(c->d);
-  CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaDeviceSynchronize());
-  CUDA_TRY(cudaMemcpy(results, d_res, n * sizeof(kvg_cache_op_result), cudaMemcpyDeviceToHost));
-  CUDA_TRY(cudaMemcpy(&st, c->d_state, sizeof st, cudaMemcpyDeviceToHost));
-  cudaFree(d_ops);
-  cudaFree(d_res);
-  if (st.n_victims > c->victim_cap)
-    return (kvg_status)set_error(KVG_ERR_STATE, "victim list overflow");
-  c->victims.resize(st.n_victims);
-  if (st.n_victims > base)
-    CUDA_TRY(cudaMemcpy(c->victims.data() + base, c->d_victims + base,
-                        (st.n_victims - base) * sizeof(kvg_victim), cudaMemcpyDeviceToHost));
-  for (size_t i = 0; i < n; ++i) {
-    auto b0 = c->victims.begin() + results[i].victims_begin;
-    auto e0 = c->victims.begin() + results[i].victims_end;
-    std::sort(b0, e0, [](const kvg_victim& x, const kvg_victim& y) {
-      if (x.stamp != y.stamp) return x.stamp < y.stamp;
-      return (x.key & 0xffffffffull) > (y.key & 0xffffffffull);
-    });
+  c->last_ms = 0;
+  // EVICT ops on a big table run grid-wide (grid.cuh); everything between
+  // them runs on the one-CTA op executor, in order
+  size_t i = 0;
+  while (i < n) {
+    size_t j = i;
+    while (j < n && !(ops[j].kind == KVG_OP_EVICT && use_grid_evict(c))) ++j;
+    if (j > i) {
+      const kvg_status rc = exec_cta(c, ops + i, j - i, results + i);
+      if (rc != KVG_OK) return rc;
+    }
+    if (j < n) {
+      const kvg_status rc = grid_evict(c, ops[j], results + j);
+      if (rc != KVG_OK) return rc;
+      sort_victims(c, results[j]);
+      ++j;
+    }
+    i = j;
   }
+  kvg::CacheState st{};
+  const kvg_status rc = cache_state(c, &st);
+  if (rc != KVG_OK) return rc;
   c->hit_m = st.hit_m;
   c->hit_r = st.hit_r;
   return KVG_OK;
@@ -331,11 +476,119 @@ KVG_API kvg_status kvg_cache_hit_window(const kvg_cache* c, double* matched, dou
   return KVG_OK;
 }
 
+KVG_API kvg_status kvg_cache_configure(kvg_cache* c, uint32_t grid_mode,
+                                       uint32_t record_victims) {
+  if (c == nullptr || grid_mode > KVG_GRID_ALWAYS)
+    return (kvg_status)set_error(KVG_ERR_CONFIG, "bad cache configuration");
+  c->grid_mode = grid_mode;
+  c->record_victims = record_victims ? 1u : 0u;
+  return KVG_OK;
+}
+
+KVG_API kvg_status kvg_cache_last_ms(const kvg_cache* c, double* ms, uint32_t* grid_blocks) {
+  if (c == nullptr) return (kvg_status)set_error(KVG_ERR_CONFIG, "null cache");
+  if (ms) *ms = c->last_ms;
+  if (grid_blocks) *grid_blocks = c->last_blocks;
+  return KVG_OK;
+}
+
+KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
+                                         const uint64_t* lens, size_t n,
+                                         kvg_cache_op_result* results) {
+  if (c == nullptr || (n > 0 && (agents == nullptr || lens == nullptr || results == nullptr)))
+    return (kvg_status)set_error(KVG_ERR_CONFIG, "null argument");
+  if (c->offload)
+    return (kvg_status)set_error(KVG_ERR_CONFIG,
+                                 "match_batch: discard-mode caches only (offload matches "
+                                 "split nodes, kvg_cache_exec)");
+  CUDA_TRY(cudaSetDevice(c->device));
+  c->last_ms = 0;
+  // queue arrays: agents u32, lens u64, f u32, resident u32, work counter
+  const size_t need = n * (4 + 8 + 4 + 4) + 64;
+  if (need > c->gq_cap) {
+    cudaFree(c->gq);
+    c->gq = nullptr;
+    c->gq_cap = 0;
+    CUDA_TRY(cudaMalloc(&c->gq, need));
+    c->gq_cap = need;
+  }
+  std::vector<u32> f(n), res(n);
+  size_t i = 0;
+  while (i < n) {
+    // one sub-batch: no agent twice, so a private chunk has a single writer
+    std::unordered_map<u32, char> seen;
+    size_t j = i;
+    while (j < n && seen.emplace(agents[j], 0).second) ++j;
+    const size_t m = j - i;
+    kvg::CacheState st{};
+    kvg_status rc = cache_state(c, &st);
+    if (rc != KVG_OK) return rc;
+    char* p = c->gq;
+    u64* d_lens = reinterpret_cast<u64*>(p);
+    u32* d_agents = reinterpret_cast<u32*>(p + n * 8);
+    u32* d_f = d_agents + n;
+    u32* d_res = d_f + n;
+    unsigned int* d_work = reinterpret_cast<unsigned int*>(d_res + n);
+    CUDA_TRY(cudaMemcpy(d_lens, lens + i, m * 8, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_agents, agents + i, m * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemset(d_work, 0, 4));
+    CUDA_TRY(cudaMemset(c->d_best, 0, (c->shared_pages + 1) * sizeof(u32)));
+    const bool sw = st.swapped & 1;
+    kvg::GridMatchArgs a{};
+    a.table = sw ? c->h.alt : c->h.table;
+    a.summ = sw ? c->h.alt_summ : c->h.summ;
+    a.mask = c->h.bucket_mask;
+    a.n = static_cast<u32>(m);
+    a.S = c->shared_pages;
+    a.ps = c->page_size;
+    a.clock0 = st.clock;
+    a.agents = d_agents;
+    a.lens = d_lens;
+    a.f_out = d_f;
+    a.res_out = d_res;
+    a.best = c->d_best;
+    a.work = d_work;
+    CUDA_TRY(cudaEventRecord(c->ev0));
+    CUDA_TRY(kvg_grid_seam::match(a, 0));
+    CUDA_TRY(cudaEventRecord(c->ev1));
+    CUDA_TRY(cudaEventSynchronize(c->ev1));
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    c->last_ms += ms;
+    CUDA_TRY(cudaMemcpy(f.data() + i, d_f, m * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(res.data() + i, d_res, m * 4, cudaMemcpyDeviceToHost));
+    // the hit window accumulates in call order (cache_tree.cpp:139-140)
+    for (size_t k = i; k < j; ++k) {
+      const u64 matched = static_cast<u64>(f[k]) * c->page_size;
+      st.hit_m += static_cast<double>(matched);
+      st.hit_r += static_cast<double>(lens[k]);
+      kvg_cache_op_result& r = results[k];
+      r = kvg_cache_op_result{};
+      r.status = res[k] == f[k] ? KVG_OK : KVG_ERR_STATE;
+      r.r0 = matched;
+      r.clock = st.clock + (k - i) + 1;
+      r.used = st.used;
+      r.victims_begin = r.victims_end = st.n_victims;
+    }
+    st.clock += m;
+    CUDA_TRY(cudaMemcpy(c->d_state, &st, sizeof st, cudaMemcpyHostToDevice));
+    c->hit_m = st.hit_m;
+    c->hit_r = st.hit_r;
+    i = j;
+  }
+  return KVG_OK;
+}
+
 KVG_API void kvg_cache_free(kvg_cache* c) {
   if (c == nullptr) return;
   cudaSetDevice(c->device);
   cudaFree(c->mem);
   cudaFree(c->d_victims);
+  cudaFree(c->gscratch);
+  cudaFree(c->d_best);
+  cudaFree(c->gq);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
   delete c;
 }
 

@@ -837,6 +837,8 @@ __global__ void __launch_bounds__(256) pack_traces(const SimDev* __restrict__ si
 
 }  // namespace kvg
 
+#include "grid.cuh"
+
 #ifdef KVG_PROFILE
 // dev-only: read and clear the phase profile (tools/probe_phases.py)
 extern "C" __attribute__((visibility("default"))) int kvg_debug_profile(unsigned long long* out) {
@@ -894,3 +896,45 @@ cudaError_t hit_window(const void* d_state, double* m, double* r) {
 }
 
 }  // namespace kvg_tree_seam
+
+// --------------------------------------------------------------------------
+// Host glue of the grid-wide seam kernels (grid.cuh), used by capi.cu.
+namespace kvg_grid_seam {
+
+static int sm_count(int dev) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 1;
+}
+
+cudaError_t match(const kvg::GridMatchArgs& a, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kvg::grid_match_kernel,
+                                                kvg::kGridMatchWarps * 32, 0);
+  if (per_sm < 1) per_sm = 1;
+  const unsigned blocks = static_cast<unsigned>(sm_count(dev) * per_sm);
+  kvg::grid_match_kernel<<<blocks, kvg::kGridMatchWarps * 32, 0, s>>>(a);
+  kvg::grid_match_shared_kernel<<<1, 1024, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t evict(const kvg::GridEvictArgs& a, cudaStream_t s, unsigned* blocks_out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kvg::grid_evict_kernel, 512, 0);
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 2) per_sm = 2;
+  unsigned blocks = static_cast<unsigned>(sm_count(dev) * per_sm);
+  // no more CTAs than 32-bucket lane groups to scan (the barrier costs the same)
+  const unsigned need = (a.occ_n + 16 * 32 * 2 - 1) / (16 * 32 * 2);
+  if (blocks > need) blocks = need > 0 ? need : 1;
+  if (blocks_out) *blocks_out = blocks;
+  void* args[] = {const_cast<kvg::GridEvictArgs*>(&a)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kvg::grid_evict_kernel),
+                                     dim3(blocks), dim3(512), args, 0, s);
+}
+
+}  // namespace kvg_grid_seam

@@ -217,4 +217,39 @@ struct CacheState {
   u64 swapped;  // table/alt swapped by a rebuild (parity of rebuilds)
 };
 
+// Grid-wide seam kernels (grid.cuh): launch arguments.
+struct GridMatchArgs {
+  Slot* table;
+  Summ* summ;
+  u32 mask;
+  u32 n;             // queries
+  u64 S;             // shared-prompt pages (owner 0)
+  u64 ps;            // page size, tokens
+  u64 clock0;        // cache clock before the batch
+  const u32* agents; // [n]
+  const u64* lens;   // [n] sequence lengths, tokens
+  u32* f_out;        // [n] first missing page (capped at len/ps)
+  u32* res_out;      // [n] resident pages in the range
+  u32* best;         // [S] shared winners: max(i+1) of queries whose range ends at page p+1
+  unsigned int* work;  // dynamic query queue head
+};
+
+constexpr int kGridDigit = 11;
+constexpr u32 kGridBins = 1u << kGridDigit;
+
+struct GridEvictArgs {
+  Slot* table;
+  Summ* summ;
+  u32* occ;
+  u32 occ_n, mask;
+  u64 S;
+  u64 k, evictable, clock;
+  kvg_victim* vic;
+  u64 vic_cap;
+  unsigned long long* vic_n;
+  u32* ghist;           // [3][2][kGridBins], zeroed by the host
+  unsigned int* freed;  // pages freed (zeroed by the host)
+  int* err;
+};
+
 }  // namespace kvg

@@ -111,6 +111,7 @@ struct Lead {
   int ps_shift;      // log2(ps) when ps is a power of two, else -1 (pdiv / pmod)
   u32 tw_off, tw_n;  // walk mirror of node ids [0, tw_n) at this dynamic-smem offset (tree.cuh)
   double pcie_busy, link_busy;
+  double abort_t;    // event time that passed the horizon (KVG_ERR_HORIZON)
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
 #ifdef KVG_PROFILE
   // dev-only phase profile (tools/probe_phases.py): cycles per leader phase,
@@ -640,6 +641,8 @@ __device__ __noinline__ void finalize(const SimDev& D, Lead& L) {
   r->evict_scanned = L.evict_scanned;
   r->agent_events = L.agent_events;
   r->device_cycles = static_cast<u64>(clock64() - L.t_start);
+  r->abort_time = L.status == KVG_ERR_HORIZON ? L.abort_t : 0.0;
+  r->unfinished = L.n - L.finished;
   D.counts[0] = L.n_trace;
   D.counts[1] = L.n_log;
   D.counts[2] = static_cast<u64>(L.err);
@@ -1348,6 +1351,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         if (which != 0 && L.finished == L.n) continue;  // housekeeping after the end
         if (bt > L.horizon) {
           L.status = KVG_ERR_HORIZON;
+          L.abort_t = bt;
           L.phase = PH_DONE;
           continue;
         }

@@ -104,6 +104,10 @@ def lib():
     L.kvg_cache_hit_window.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double)]
     L.kvg_cache_free.argtypes = [C.c_void_p]
     L.kvg_cache_free.restype = None
+    L.kvg_cache_configure.argtypes = [C.c_void_p, C.c_uint32, C.c_uint32]
+    L.kvg_cache_match_batch.argtypes = [C.c_void_p, P(C.c_uint32), P(C.c_uint64), C.c_size_t,
+                                        P(abi.CacheOpResult)]
+    L.kvg_cache_last_ms.argtypes = [C.c_void_p, P(C.c_double), P(C.c_uint32)]
     _lib = L
     return L
 
@@ -375,13 +379,43 @@ class DeviceCache:
             if nv:
                 _check(lib().kvg_cache_victims(self.h, r.victims_begin, r.victims_end, vic))
             out.append(dict(status=r.status, r0=r.r0, r1=r.r1, clock=r.clock, used=r.used,
-                            victims=[vic[j].key for j in range(nv)]))
+                            victims=[vic[j].key for j in range(nv)],
+                            vrange=(r.victims_begin, r.victims_end)))
         return out
+
+    def victim_stamps(self, res: dict) -> list[int]:
+        """Last-access stamps of one op result's victims, in victim order."""
+        b, e = res["vrange"]
+        vic = (abi.Victim * max(1, e - b))()
+        if e > b:
+            _check(lib().kvg_cache_victims(self.h, b, e, vic))
+        return [vic[j].stamp for j in range(e - b)]
 
     def hit_window(self):
         m, r = C.c_double(), C.c_double()
         _check(lib().kvg_cache_hit_window(self.h, C.byref(m), C.byref(r)))
         return m.value, r.value
+
+    def configure(self, grid_mode: int = 0, record_victims: bool = True):
+        """grid_mode: 0 auto (EVICT grid-wide on big tables), 1 never, 2 always."""
+        _check(lib().kvg_cache_configure(self.h, grid_mode, int(record_victims)))
+
+    def match_batch(self, agents, lens) -> list[dict]:
+        """n match_prefix calls in one grid launch (== n KVG_OP_MATCH ops)."""
+        import numpy as np
+        a = np.ascontiguousarray(agents, dtype=np.uint32)
+        ln = np.ascontiguousarray(lens, dtype=np.uint64)
+        n = len(a)
+        res = (abi.CacheOpResult * max(1, n))()
+        _check(lib().kvg_cache_match_batch(self.h, a.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                           ln.ctypes.data_as(C.POINTER(C.c_uint64)), n, res))
+        return [dict(status=res[i].status, r0=res[i].r0, r1=res[i].r1, clock=res[i].clock,
+                     used=res[i].used, victims=[]) for i in range(n)]
+
+    def last_ms(self):
+        ms, blocks = C.c_double(), C.c_uint32()
+        _check(lib().kvg_cache_last_ms(self.h, C.byref(ms), C.byref(blocks)))
+        return ms.value, blocks.value
 
     def close(self):
         if getattr(self, "h", None):
