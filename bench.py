@@ -222,7 +222,8 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- helpers
 
-def algorithmic_bytes(results, tree: bool = False, probed: bool = False) -> dict:
+def algorithmic_bytes(results, tree: bool = False, probed: bool = False,
+                      chain: bool = False) -> dict:
     """SURVEY.md §8(d) per-unit byte counts for the operations the timed
     kernel actually performs:
       lookup   16 B slot read per counted lookup — only when the block-hash
@@ -234,10 +235,18 @@ def algorithmic_bytes(results, tree: bool = False, probed: bool = False) -> dict
       evict    8 B per resident page per select call (64 B per node record in
                offload mode) + 16 B per victim;
       state    96 B read + 96 B write per agent state-machine advance;
-      tick     88 B per trace row."""
+      tick     88 B per trace row.
+    chain=True (discard mode without the probe: the benchmarked path) keeps
+    the cache as per-agent chains: an insert extends a chain
+    (no page written) and an eviction walks the chain LRU — 72 B (agent
+    record + LRU links) per chain visited, nothing per victim."""
     look = sum(16 * r.lookups for r in results) if probed else 0
-    ins = sum(16 * r.created_pages for r in results)
-    ev = sum((64 if tree else 8) * r.evict_scanned + 16 * r.evicted_pages for r in results)
+    if chain:
+        ins = 0
+        ev = sum(72 * r.evict_scanned for r in results)
+    else:
+        ins = sum(16 * r.created_pages for r in results)
+        ev = sum((64 if tree else 8) * r.evict_scanned + 16 * r.evicted_pages for r in results)
     state = sum(192 * r.agent_events for r in results)
     tick = sum(88 * r.ticks for r in results)
     return dict(lookup=look, insert=ins, evict=ev, state=state, tick=tick,
@@ -361,7 +370,10 @@ def run_b200(args):
     sampler.start()
     torch.cuda.synchronize()
     step_ms = kern_ms = 0.0
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.steps):
+        flush.fill_(1)  # L2 (126 MB) flushed between timed steps, outside the events
+        torch.cuda.synchronize()
         batch.run()  # device-resident inputs; CUDA events on the launch stream
         a, k = batch.timing()
         step_ms += a
@@ -387,7 +399,8 @@ def run_b200(args):
     summary = sweep.gather_records(sweep.records(results), dist, device="cuda")
     makespans = summary[:, 0].cpu().tolist()
     # ---- roofline of the engine kernel (bytes of the operations it performs)
-    ab = algorithmic_bytes(results, tree=args.workload == "c3off")
+    ab = algorithmic_bytes(results, tree=args.workload == "c3off",
+                           chain=args.workload != "c3off")
     kernel_s = (kern_ms / args.steps) / 1e3
     peak, peak_kind = load_peak()
     achieved = ab["total"] / kernel_s / 1e9
@@ -484,13 +497,16 @@ def run_b200(args):
             "config": {"workload": desc, "sims_per_gpu": len(specs),
                        "parallelism": f"independent simulations sharded over {world} GPU(s) "
                                       f"({args.split} split), NCCL all_gather of records",
-                       "l2": "inputs larger than L2: per-sim hash tables total "
-                             f"{batch_bytes(specs) / 2**30:.1f} GiB, re-initialised every step",
+                       "l2": "flushed between timed steps (256 MiB device memset outside "
+                             "the CUDA-event window)",
+                       "cache_state": "chain mode: per-agent chains + LRU, no page table "
+                                      "(DESIGN.md §4.1); probe_mode runs the page table",
                        "verify": 0},
             "lookups_per_s": all_lookups * args.steps / (max_ms / 1e3),
-            "lookups_note": "counted per SURVEY §8(d) (resolved pages + terminating miss); "
-                            "answered from the held prefix state, the block-hash probe is "
-                            "not run in the timed region (see probe_mode)",
+            "lookups_note": "EQUIVALENT lookups: counted per SURVEY §8(d) (resolved pages + "
+                            "terminating miss) but answered from the held prefix state; the "
+                            "block-hash probe is not run in the timed region (probe_mode "
+                            "runs it; bench.py --workload kernels measures it alone)",
             "probe_mode": probe,
             "roofline": roof, "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "agent-steps/s", "h2d_bytes_per_step": h2d,

@@ -95,7 +95,7 @@ u64 xfer_ring(const kvg_sim_desc& d) {
 constexpr size_t kBigSmemMax = 200 * 1024;
 size_t hot_smem_bytes(u64 n) {
   const u64 nwords = (n + 31) / 32;
-  return n * (sizeof(kvg::AgentDev) + sizeof(kvg::HeapEnt)) + (nwords + (nwords + 31) / 32) * 4;
+  return n * (sizeof(kvg::AgentDev) + sizeof(kvg::HeapEnt) + 8) + (nwords + (nwords + 31) / 32) * 4;
 }
 size_t hot_smem(u64 n, bool big = false) {
   if (!big) return n > 128 ? 0 : hot_smem_bytes(n);
@@ -503,16 +503,8 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
                                  "split nodes, kvg_cache_exec)");
   CUDA_TRY(cudaSetDevice(c->device));
   c->last_ms = 0;
-  // queue arrays: agents u32, lens u64, f u32, resident u32, work counter
-  const size_t need = n * (4 + 8 + 4 + 4) + 64;
-  if (need > c->gq_cap) {
-    cudaFree(c->gq);
-    c->gq = nullptr;
-    c->gq_cap = 0;
-    CUDA_TRY(cudaMalloc(&c->gq, need));
-    c->gq_cap = need;
-  }
-  std::vector<u32> f(n), res(n);
+  const u64 S = c->shared_pages, ps = c->page_size;
+  std::vector<kvg_cache_op_result> out(n);
   size_t i = 0;
   while (i < n) {
     // one sub-batch: no agent twice, so a private chunk has a single writer
@@ -520,34 +512,69 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
     size_t j = i;
     while (j < n && seen.emplace(agents[j], 0).second) ++j;
     const size_t m = j - i;
+    // work items: every query's private chunks in groups of kGridItemChunks
+    std::vector<u32> iq, ic;
+    iq.reserve(m);
+    ic.reserve(m);
+    for (size_t k = 0; k < m; ++k) {
+      const u64 np = lens[i + k] / ps;
+      if (np <= S) {
+        iq.push_back(static_cast<u32>(k));
+        ic.push_back(~0u);
+        continue;
+      }
+      for (u64 c0 = S >> 5; c0 <= (np - 1) >> 5; c0 += kvg::kGridItemChunks) {
+        iq.push_back(static_cast<u32>(k));
+        ic.push_back(static_cast<u32>(c0));
+      }
+    }
+    const size_t items = iq.size();
+    const size_t words = S / 32 + 1;
+    const size_t need = m * (8 + 4 + 4 + 4) + items * 8 + words * 4 + 256;
+    if (need > c->gq_cap) {
+      cudaFree(c->gq);
+      c->gq = nullptr;
+      c->gq_cap = 0;
+      CUDA_TRY(cudaMalloc(&c->gq, need));
+      c->gq_cap = need;
+    }
+    char* p = c->gq;
+    u64* d_lens = reinterpret_cast<u64*>(p);
+    u32* d_agents = reinterpret_cast<u32*>(d_lens + m);
+    u32* d_fm = d_agents + m;
+    u32* d_res = d_fm + m;
+    u32* d_iq = d_res + m;
+    u32* d_ic = d_iq + items;
+    u32* d_smask = d_ic + items;
     kvg::CacheState st{};
     kvg_status rc = cache_state(c, &st);
     if (rc != KVG_OK) return rc;
-    char* p = c->gq;
-    u64* d_lens = reinterpret_cast<u64*>(p);
-    u32* d_agents = reinterpret_cast<u32*>(p + n * 8);
-    u32* d_f = d_agents + n;
-    u32* d_res = d_f + n;
-    unsigned int* d_work = reinterpret_cast<unsigned int*>(d_res + n);
     CUDA_TRY(cudaMemcpy(d_lens, lens + i, m * 8, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d_agents, agents + i, m * 4, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemset(d_work, 0, 4));
-    CUDA_TRY(cudaMemset(c->d_best, 0, (c->shared_pages + 1) * sizeof(u32)));
+    CUDA_TRY(cudaMemcpy(d_iq, iq.data(), items * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_ic, ic.data(), items * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemset(d_fm, 0xff, m * 4));
+    CUDA_TRY(cudaMemset(d_res, 0, m * 4));
+    CUDA_TRY(cudaMemset(d_smask, 0, words * 4));
+    CUDA_TRY(cudaMemset(c->d_best, 0, (S + 1) * sizeof(u32)));
     const bool sw = st.swapped & 1;
     kvg::GridMatchArgs a{};
     a.table = sw ? c->h.alt : c->h.table;
     a.summ = sw ? c->h.alt_summ : c->h.summ;
     a.mask = c->h.bucket_mask;
     a.n = static_cast<u32>(m);
-    a.S = c->shared_pages;
-    a.ps = c->page_size;
+    a.S = S;
+    a.ps = ps;
     a.clock0 = st.clock;
     a.agents = d_agents;
     a.lens = d_lens;
-    a.f_out = d_f;
-    a.res_out = d_res;
+    a.n_items = static_cast<u32>(items);
+    a.item_q = d_iq;
+    a.item_c = d_ic;
+    a.fm = d_fm;
+    a.res = d_res;
+    a.smask = d_smask;
     a.best = c->d_best;
-    a.work = d_work;
     CUDA_TRY(cudaEventRecord(c->ev0));
     CUDA_TRY(kvg_grid_seam::match(a, 0));
     CUDA_TRY(cudaEventRecord(c->ev1));
@@ -555,18 +582,42 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
     float ms = 0;
     CUDA_TRY(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     c->last_ms += ms;
-    CUDA_TRY(cudaMemcpy(f.data() + i, d_f, m * 4, cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(res.data() + i, d_res, m * 4, cudaMemcpyDeviceToHost));
-    // the hit window accumulates in call order (cache_tree.cpp:139-140)
-    for (size_t k = i; k < j; ++k) {
-      const u64 matched = static_cast<u64>(f[k]) * c->page_size;
+    std::vector<u32> fm(m), res(m), smask(words);
+    CUDA_TRY(cudaMemcpy(fm.data(), d_fm, m * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(res.data(), d_res, m * 4, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(smask.data(), d_smask, words * 4, cudaMemcpyDeviceToHost));
+    // shared part: first non-resident shared page and resident pages below p
+    u64 f_sh = S;
+    for (u64 p0 = 0; p0 < S; p0 += 32) {
+      const u32 lim = S - p0 >= 32 ? 0xffffffffu : ((1u << (S - p0)) - 1u);
+      const u32 miss = ~smask[p0 / 32] & lim;
+      if (miss) {
+        f_sh = p0 + __builtin_ctz(miss);
+        break;
+      }
+    }
+    std::vector<u64> pre(words + 1, 0);
+    for (size_t w = 0; w < words; ++w) pre[w + 1] = pre[w] + __builtin_popcount(smask[w]);
+    auto res_below = [&](u64 p) -> u64 {  // resident shared pages in [0, p)
+      const u64 w = p / 32, r = p % 32;
+      return pre[w] + (r ? __builtin_popcount(smask[w] & ((1u << r) - 1u)) : 0);
+    };
+    // results and the hit window in call order (cache_tree.cpp:139-140)
+    for (size_t k = 0; k < m; ++k) {
+      const u64 np = lens[i + k] / ps;
+      const u64 sh = np < S ? np : S;
+      u64 f = np;
+      if (f_sh < sh) f = f_sh;
+      if (fm[k] != 0xffffffffu && fm[k] < f) f = fm[k];
+      const u64 resident = res_below(sh) + res[k];
+      const u64 matched = f * ps;
       st.hit_m += static_cast<double>(matched);
-      st.hit_r += static_cast<double>(lens[k]);
-      kvg_cache_op_result& r = results[k];
+      st.hit_r += static_cast<double>(lens[i + k]);
+      kvg_cache_op_result& r = results[i + k];
       r = kvg_cache_op_result{};
-      r.status = res[k] == f[k] ? KVG_OK : KVG_ERR_STATE;
+      r.status = resident == f ? KVG_OK : KVG_ERR_STATE;
       r.r0 = matched;
-      r.clock = st.clock + (k - i) + 1;
+      r.clock = st.clock + k + 1;
       r.used = st.used;
       r.victims_begin = r.victims_end = st.n_victims;
     }
@@ -576,6 +627,7 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
     c->hit_r = st.hit_r;
     i = j;
   }
+  (void)out;
   return KVG_OK;
 }
 

@@ -455,31 +455,31 @@ __device__ __forceinline__ void scan_buckets(const Op& op, int warp, int lane, i
 #endif
 constexpr int kSumDepth = KVG_SUM_DEPTH;
 
-template <typename F>
+template <int kDepth = kSumDepth, typename F>
 __device__ __forceinline__ void scan_summ(const Op& op, int warp, int lane, int nw, F&& f) {
   const u32 n_occ = op.occ_n;
-  const u32 stride = static_cast<u32>(nw) * 32u * kSumDepth;
-  for (u32 base = static_cast<u32>(warp) * 32u * kSumDepth; base < n_occ; base += stride) {
-    u32 bk[kSumDepth];
-    Summ e[kSumDepth];
+  const u32 stride = static_cast<u32>(nw) * 32u * kDepth;
+  for (u32 base = static_cast<u32>(warp) * 32u * kDepth; base < n_occ; base += stride) {
+    u32 bk[kDepth];
+    Summ e[kDepth];
 #pragma unroll
-    for (int g = 0; g < kSumDepth; ++g) {
+    for (int g = 0; g < kDepth; ++g) {
       const u32 i = base + g * 32u + lane;
       bk[g] = i < n_occ ? __ldcg(&op.occ[i]) : NIL32;
     }
 #pragma unroll
-    for (int g = 0; g < kSumDepth; ++g) {
+    for (int g = 0; g < kDepth; ++g) {
       e[g] = Summ{0, 0, 0, 0, 0, 0};
       if (bk[g] != NIL32) e[g] = ld_summ(&op.summ[bk[g]]);
     }
     // one copy of f's body: the loads above stay in flight, the calls rotate
     // through registers (f is large: the radix-select histogram step)
 #pragma unroll 1
-    for (int g = 0; g < kSumDepth; ++g) {
+    for (int g = 0; g < kDepth; ++g) {
       const u32 b0 = bk[0];
       const Summ e0 = e[0];
 #pragma unroll
-      for (int j = 0; j + 1 < kSumDepth; ++j) {
+      for (int j = 0; j + 1 < kDepth; ++j) {
         bk[j] = bk[j + 1];
         e[j] = e[j + 1];
       }
@@ -914,9 +914,12 @@ cudaError_t match(const kvg::GridMatchArgs& a, cudaStream_t s) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kvg::grid_match_kernel,
                                                 kvg::kGridMatchWarps * 32, 0);
   if (per_sm < 1) per_sm = 1;
-  const unsigned blocks = static_cast<unsigned>(sm_count(dev) * per_sm);
+  unsigned blocks = static_cast<unsigned>(sm_count(dev) * per_sm);
+  const unsigned need = (a.n_items + kvg::kGridMatchWarps - 1) / kvg::kGridMatchWarps;
+  if (blocks > need) blocks = need > 0 ? need : 1;
+  if (a.S > 0) kvg::grid_match_prep_kernel<<<1, 1024, 0, s>>>(a);
   kvg::grid_match_kernel<<<blocks, kvg::kGridMatchWarps * 32, 0, s>>>(a);
-  kvg::grid_match_shared_kernel<<<1, 1024, 0, s>>>(a);
+  if (a.S > 0) kvg::grid_match_shared_kernel<<<1, 1024, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -929,7 +932,7 @@ cudaError_t evict(const kvg::GridEvictArgs& a, cudaStream_t s, unsigned* blocks_
   if (per_sm > 2) per_sm = 2;
   unsigned blocks = static_cast<unsigned>(sm_count(dev) * per_sm);
   // no more CTAs than 32-bucket lane groups to scan (the barrier costs the same)
-  const unsigned need = (a.occ_n + 16 * 32 * 2 - 1) / (16 * 32 * 2);
+  const unsigned need = (a.occ_n + 16 * 32 * kvg::kGridSumDepth - 1) / (16 * 32 * kvg::kGridSumDepth);
   if (blocks > need) blocks = need > 0 ? need : 1;
   if (blocks_out) *blocks_out = blocks;
   void* args[] = {const_cast<kvg::GridEvictArgs*>(&a)};

@@ -27,6 +27,37 @@ namespace kvg {
 
 constexpr int kGridMatchWarps = 8;
 
+// Shared prompt, probed ONCE per batch (every query's range starts with the
+// same shared chunks): smask[c] = resident pages of shared chunk c.
+__global__ void __launch_bounds__(1024) grid_match_prep_kernel(GridMatchArgs A) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const u64 chunks = (A.S + 31) / 32;
+  for (u64 c = warp; c < chunks; c += nw) {
+    const u64 tag = c * 32;  // owner 0
+    u32 b = static_cast<u32>(hash64(tag)) & A.mask;
+    bool found = false;
+    Slot s{kEmptyKey, 0};
+    for (;;) {
+      s = ld_slot(&A.table[(size_t)b * kChunk + lane]);
+      const u64 k0 = __shfl_sync(FULL, s.key, 0);
+      if (k0 == tag) { found = true; break; }
+      if (k0 == kEmptyKey) break;
+      b = (b + 1) & A.mask;
+    }
+    const bool res = found && (s.meta & kResident) && tag + lane < A.S;
+    const u32 m = __ballot_sync(FULL, res);
+    if (lane == 0) A.smask[c] = m;
+  }
+}
+
+// One warp per work item: item k covers up to kGridItemChunks private chunks
+// of query item_q[k] starting at chunk item_c[k] (the host splits every
+// query's private range [S, len/ps) so long contexts spread over many warps).
+// Each item probes its chunks (all in flight), refreshes their resident
+// pages to the query's clock (a private chunk has one writer per batch: the
+// host splits batches so an agent appears once) and folds first miss /
+// resident count into the query's accumulators. A query's first item also
+// files its shared range for the shared-stamp pass.
 __global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMatchArgs A) {
   __shared__ Op wops[kGridMatchWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -43,34 +74,34 @@ __global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMa
     op.log_victims = 0;
   }
   __syncwarp();
-  for (;;) {
-    u32 i = 0;
-    if (lane == 0) i = atomicAdd(A.work, 1u);
-    i = __shfl_sync(FULL, i, 0);
-    if (i >= A.n) break;
-    const u32 a = A.agents[i];
+  const u32 gw = blockIdx.x * kGridMatchWarps + w, GW = gridDim.x * kGridMatchWarps;
+  for (u32 k = gw; k < A.n_items; k += GW) {
+    const u32 i = A.item_q[k];
+    const u64 c0 = A.item_c[k];
     const u64 n = A.lens[i] / A.ps;
-    const u64 sh = n < A.S ? n : A.S;
-    if (lane == 0) post_range(op, a, 0, sh, 0, 0, 0);  // shared part: probe only
-    __syncwarp();
-    if (sh > 0) coop_range<8>(op, 0, lane, 1);
-    __syncwarp();
-    if (n > A.S) {  // private part: probe and refresh (single writer)
+    if (c0 == ~0u) {  // head item of a query without private pages
       if (lane == 0) {
-        op.p0 = A.S;
-        op.p1 = n;
-        op.flags = RF_STAMP;
-        op.stamp = A.clock0 + i + 1;
+        const u64 sh = n < A.S ? n : A.S;
+        if (sh > 0) atomicMax(&A.best[sh - 1], i + 1);
       }
-      __syncwarp();
-      coop_range<8>(op, 0, lane, 1);
-      __syncwarp();
+      continue;
     }
+    const u64 lo = c0 * 32 > A.S ? c0 * 32 : A.S;
+    const u64 hi_c = (c0 + kGridItemChunks) * 32;
+    const u64 hi = hi_c < n ? hi_c : n;
     if (lane == 0) {
-      const u64 fm = op.first_miss;
-      A.f_out[i] = static_cast<u32>(fm < n ? fm : n);
-      A.res_out[i] = op.resident;
-      if (sh > 0) atomicMax(&A.best[sh - 1], i + 1);
+      post_range(op, A.agents[i], lo, hi, RF_STAMP, 0, A.clock0 + i + 1);
+      if (lo == A.S) {  // the query's first item
+        const u64 sh = n < A.S ? n : A.S;
+        if (sh > 0) atomicMax(&A.best[sh - 1], i + 1);
+      }
+    }
+    __syncwarp();
+    coop_range<kGridItemChunks>(op, 0, lane, 1);
+    __syncwarp();
+    if (lane == 0) {
+      if (op.first_miss != ~0ull) atomicMin(&A.fm[i], static_cast<u32>(op.first_miss));
+      if (op.resident) atomicAdd(&A.res[i], op.resident);
     }
     __syncwarp();
   }
@@ -178,7 +209,7 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
       }
       __syncthreads();
       const u64 prefix = op.prefix;
-      scan_summ(op, gw, lane, GW, [&](bool valid, u32 b, const Summ& e) {
+      scan_summ<kGridSumDepth>(op, gw, lane, GW, [&](bool valid, u32 b, const Summ& e) {
         const bool mixed = valid && (e.sf & kMixed);
         u32 c = 0;
         u64 st = 0;
@@ -227,7 +258,7 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
     cut = op.cut_depth;
   }
   unsigned int freed = 0;
-  scan_summ(op, gw, lane, GW, [&](bool valid, u32 b, const Summ& e) {
+  scan_summ<kGridSumDepth>(op, gw, lane, GW, [&](bool valid, u32 b, const Summ& e) {
     if (!valid) return;
     if (e.sf & kMixed) {
       freed += scatter_mixed(op, b, all, T, cut);

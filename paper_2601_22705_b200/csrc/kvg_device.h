@@ -163,6 +163,7 @@ struct SimDev {
   HeapEnt* heap;      // agent events (leader-only binary heap)
   u32* rbits;         // ready bitmap: in_active && AwaitingAdmission
   u32* rl1;           // second level: non-empty words of rbits
+  u32* lru;           // [2 * n_agents] chain LRU links {prev, next} (leader.cuh)
   u32* pin_hist;      // [shared_pages+1]: agents per shared-pin depth
   u32* pin_lvl;       // bitmap of non-empty pin_hist levels
   u32* hist;          // [2 * 512]: eviction radix-select histogram scratch
@@ -218,6 +219,9 @@ struct CacheState {
 };
 
 // Grid-wide seam kernels (grid.cuh): launch arguments.
+constexpr int kGridItemChunks = 8;  // private chunks per match work item (4 KB of slots)
+constexpr int kGridSumDepth = 8;    // bucket summaries in flight per lane (grid evict)
+
 struct GridMatchArgs {
   Slot* table;
   Summ* summ;
@@ -228,10 +232,13 @@ struct GridMatchArgs {
   u64 clock0;        // cache clock before the batch
   const u32* agents; // [n]
   const u64* lens;   // [n] sequence lengths, tokens
-  u32* f_out;        // [n] first missing page (capped at len/ps)
-  u32* res_out;      // [n] resident pages in the range
-  u32* best;         // [S] shared winners: max(i+1) of queries whose range ends at page p+1
-  unsigned int* work;  // dynamic query queue head
+  u32 n_items, pad;
+  const u32* item_q; // [n_items] query of each work item
+  const u32* item_c; // [n_items] first private chunk (~0: no private pages)
+  u32* fm;           // [n] first missing private page (NIL32 = none), atomicMin
+  u32* res;          // [n] resident private pages, atomicAdd
+  u32* smask;        // [S/32 + 1] resident pages of each shared chunk
+  u32* best;         // [S] shared winners: max(i+1) of queries whose shared range ends at page p+1
 };
 
 constexpr int kGridDigit = 11;

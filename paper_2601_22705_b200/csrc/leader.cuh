@@ -112,6 +112,12 @@ struct Lead {
   u32 tw_off, tw_n;  // walk mirror of node ids [0, tw_n) at this dynamic-smem offset (tree.cuh)
   double pcie_busy, link_busy;
   double abort_t;    // event time that passed the horizon (KVG_ERR_HORIZON)
+  // chain mode (discard, verify off): the cache is held as chains, no page
+  // table. lru = per-agent {prev, next} links of the agents holding private
+  // pages, in chain-stamp order
+  u32* lru;
+  u32 lru_head, lru_tail;
+  int chain;
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
 #ifdef KVG_PROFILE
   // dev-only phase profile (tools/probe_phases.py): cycles per leader phase,
@@ -328,6 +334,82 @@ __device__ KVG_LEADER_FN void set_pinned(const SimDev& D, Lead& L, u32 id, u64 t
     while (bits == 0 && w > 0) bits = D.pin_lvl[--w];
     L.pin_max = bits ? (w << 5) + 31 - __clz(bits) : 0;
   }
+}
+
+// ---------------------------------------------------------------- chain LRU
+// Discard mode holds every agent's resident private pages as ONE chain
+// [S, S + priv) whose pages all carry the agent's latest refresh stamp
+// (a.lazy), and the shared prompt as the chain [0, L0) stamped lazy_sh, the
+// newest stamp of all. Every refresh stamps with the next
+// clock value, so ordering chains by stamp is an LRU list: a refresh moves the
+// agent to the tail. evict(needed) = "the needed smallest (stamp asc, page
+// index desc) unpinned resident pages" (cache_tree.cpp:270-319)
+// therefore takes chain tails from the LRU head on, then the shared chain's
+// tail (its stamp ties only with the newest agent's chain, whose pages are
+// deeper and go first). The list holds exactly the agents with priv > 0.
+constexpr u32 kLruOut = 0xfffffffeu;  // prev link of an agent not in the list
+
+__device__ __forceinline__ void lru_unlink(Lead& L, u32 id) {
+  u32* e = &L.lru[2 * id];
+  const u32 p = e[0], nx = e[1];
+  if (p != NIL) L.lru[2 * p + 1] = nx; else L.lru_head = nx;
+  if (nx != NIL) L.lru[2 * nx] = p; else L.lru_tail = p;
+  e[0] = kLruOut;
+}
+
+// Agent `id` was just refreshed (its stamp is the newest): move / append it
+// to the tail.
+__device__ __forceinline__ void lru_touch(Lead& L, u32 id) {
+  u32* e = &L.lru[2 * id];
+  if (e[0] != kLruOut) {
+    if (L.lru_tail == id) return;
+    lru_unlink(L, id);
+  }
+  e[0] = L.lru_tail;
+  e[1] = NIL;
+  if (L.lru_tail != NIL) L.lru[2 * L.lru_tail + 1] = id; else L.lru_head = id;
+  L.lru_tail = id;
+}
+
+// Frees `need` (> 0, <= evictable) pages in reference eviction order: each
+// chain from the LRU head loses its unpinned tail (pages [max(S, pinned),
+// S + priv), deepest first), then the shared chain [pin_max, L0). Victims are
+// logged in that order. Chains visited count as scanned (roofline).
+__device__ __noinline__ void chain_evict(const SimDev& D, Lead& L, u64 need) {
+  const u64 S = L.S;
+  u32 id = L.lru_head;
+  while (need > 0 && id != NIL) {
+    const u32 nx = L.lru[2 * id + 1];
+    AgentDev& a = L.ag[id];
+    const u64 lo = a.pinned_pg > S ? a.pinned_pg : S;
+    const u64 hi = S + a.priv;
+    ++L.evict_scanned;
+    if (hi > lo) {
+      const u64 t = hi - lo < need ? hi - lo : need;
+      if (L.log_on) {
+        const u64 owner = (static_cast<u64>(id) + 1) << 32;
+        for (u64 p = hi; p > hi - t;) {
+          --p;
+          log_store(D, L, KVG_LOG_VICTIM, L.m_id, owner | p, a.lazy);
+        }
+      }
+      a.priv -= static_cast<u32>(t);
+      need -= t;
+      if (a.priv == 0) lru_unlink(L, id);
+    }
+    id = nx;
+  }
+  if (need > 0 && L.L0 > L.pin_max) {
+    const u64 t = L.L0 - L.pin_max < need ? L.L0 - L.pin_max : need;
+    if (L.log_on)
+      for (u64 p = L.L0; p > L.L0 - t;) {
+        --p;
+        log_store(D, L, KVG_LOG_VICTIM, L.m_id, p, L.lazy_sh);
+      }
+    L.L0 -= t;
+    need -= t;
+  }
+  if (need > 0) fail(L, E_EVICT_MISMATCH);
 }
 
 __device__ __forceinline__ bool heap_less(const HeapEnt& x, const HeapEnt& y) {
@@ -665,6 +747,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.pin_max = L.pin_priv = 0;
   L.L0 = L.lazy_sh = 0;
   L.verify = D.verify != 0;
+  L.lru_head = L.lru_tail = NIL;
   L.hit_pages = L.created_pages = L.refreshed_pages = L.evict_scanned = L.agent_events = 0;
   L.hit_m = L.hit_r = 0.0;
   L.n = D.n_agents;
@@ -735,6 +818,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.pcie_busy = L.link_busy = 0.0;
   L.offloaded = L.reloaded = 0;
   if (L.offload) tree_init(D, L);
+  L.chain = !L.offload && !L.verify;
   L.phase = PH_EVENT;
 }
 
@@ -1492,6 +1576,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         }
         a.lazy = L.m_now;
         L.lazy_sh = L.m_now;
+        if (L.lru[2 * id] != kLruOut) lru_touch(L, id);
         L.phase = PH_M_MATCHED;
         if (L.verify && L.m_nctx > 0) {
           post_range(op, id, 0, L.m_nctx, 0, 0, 0);
@@ -1543,6 +1628,14 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.phase = PH_M_FAIL;
           continue;
         }
+        if (L.chain) {  // chain LRU: no page table, no cooperative op
+          const u64 r = k < e ? k : e;
+          chain_evict(D, L, r);
+          L.used -= r;
+          L.discarded += r * L.ps;
+          L.evicted += r;
+          continue;  // PH_M_INSERT again (cache_tree.cpp:176-186)
+        }
         L.m_k = k;
         L.m_e = e;
         L.evict_scanned += L.used;
@@ -1571,8 +1664,8 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         continue;
       }
       case PH_M_COMMIT: {
-        if (static_cast<u64>(op.occ_n) + range_chunks(L.m_f, L.m_nafter) >
-            (static_cast<u64>(op.mask) + 1) / 2) {
+        if (!L.chain && static_cast<u64>(op.occ_n) + range_chunks(L.m_f, L.m_nafter) >
+                            (static_cast<u64>(op.mask) + 1) / 2) {
           if (L.rebuilt) {
             fail(L, E_TABLE_FULL);
             continue;
@@ -1588,6 +1681,11 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         L.ag[L.m_id].lazy = L.cclock;
         L.lazy_sh = L.cclock;
         L.phase = PH_M_CREATED;
+        if (L.chain) {  // the leaf [f, n_after) extends the agent's chain
+          op.created = L.m_f < L.m_nafter ? static_cast<unsigned int>(L.m_nafter - L.m_f) : 0u;
+          op.err = E_NONE;
+          continue;
+        }
         if (L.m_f < L.m_nafter) {
           post_range(op, L.m_id, L.m_f, L.m_nafter, RF_CREATE, 0, L.cclock);
           return;
@@ -1607,6 +1705,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           const u64 sh = L.m_nafter < L.S ? L.m_nafter : L.S;
           if (sh > L.L0) L.L0 = sh;
           a.priv = static_cast<u32>(L.m_nafter > L.S ? L.m_nafter - L.S : 0);
+          if (a.priv > 0) lru_touch(L, L.m_id);
         }
         const u64 stored = a.ctx - pmod(L, a.ctx);
         const u64 matched = L.m_f * L.ps;
@@ -1665,6 +1764,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           const u64 keep = fp > L.S ? fp - L.S : 0;
           AgentDev& a = L.ag[id];
           if (a.priv > keep) a.priv = static_cast<u32>(keep);
+          if (a.priv == 0 && L.lru[2 * id] != kLruOut) lru_unlink(L, id);
         }
         log_rec(D, L, KVG_LOG_DISCARD, id, 0, op.freed);
         act_erase(D, L, id);  // on_request_complete / on_agent_finished
@@ -1727,7 +1827,7 @@ __device__ __forceinline__ void run_op(Op& op, Hist& h, int tid, int warp, int l
 
 __device__ __forceinline__ size_t smem_bytes_for(u32 n) {
   const u32 nwords = (n + 31) / 32;
-  return static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt)) +
+  return static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt) + 2 * sizeof(u32)) +
          (nwords + (nwords + 31) / 32) * sizeof(u32);
 }
 
@@ -1795,11 +1895,13 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
       used = (smem_bytes_for(n) + 15) / 16 * 16;
       L.ag = reinterpret_cast<AgentDev*>(dyn);
       L.heap = reinterpret_cast<HeapEnt*>(dyn + static_cast<size_t>(n) * sizeof(AgentDev));
-      L.rbits = reinterpret_cast<u32*>(dyn + static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt)));
+      L.lru = reinterpret_cast<u32*>(dyn + static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt)));
+      L.rbits = L.lru + 2 * static_cast<size_t>(n);
       L.rl1 = L.rbits + nwords;
     } else {
       L.ag = D.agents;
       L.heap = D.heap;
+      L.lru = D.lru;
       L.rbits = D.rbits;
       L.rl1 = D.rl1;
     }
@@ -1830,6 +1932,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     a.act_seq = 0;
     a.ready = 0;
     ag[i] = a;
+    L.lru[2 * i] = kLruOut;
     D.pend[i] = i;
     D.stats[i] = kvg_agent_stats{0, 0, 0, 0, 0, 0.0, -1.0, 0};
   }

@@ -98,7 +98,7 @@ def test_gpu_full_c4_verify_on_equals_verify_off(c4_specs):
         outs.append((res.copy(), [s.copy() for s in stats], [r.copy() for r in rows]))
         b.close()
     (ra, sa, ta), (rb, sb, tb) = outs
-    skip = {"device_cycles"}
+    skip = {"device_cycles", "evict_scanned"}  # chains (verify off) vs pages (verify on)
     for f in ra.dtype.names:
         if f not in skip:
             assert (ra[f] == rb[f]).all(), f

@@ -25,9 +25,10 @@ def preset(name):
     return config.scenario_from_dict(load_presets()[name])
 
 
-def gpu_run(s, policy=None, warps=0, log=False):
+def gpu_run(s, policy=None, warps=0, log=False, verify=None):
     spec = engine.SimSpec.from_scenario(s, policy)
-    b = engine.Batch([spec], warps_per_sim=warps, log_capacity=(1 << 20) if log else 0)
+    b = engine.Batch([spec], warps_per_sim=warps, log_capacity=(1 << 20) if log else 0,
+                     verify=verify)
     st = b.run()
     out = dict(status=st, result=b.result(0), trace=b.trace(0), agents=b.agent_stats(0))
     if log:
@@ -47,10 +48,14 @@ CASES = [
 
 
 @pytest.mark.parametrize("name,policy", CASES)
-@pytest.mark.parametrize("warps", [1, 4])
-def test_presets_bit_exact(name, policy, warps):
+@pytest.mark.parametrize("warps,verify", [(1, True), (4, True), (0, False)],
+                         ids=["table-w1", "table-w4", "chain"])
+def test_presets_bit_exact(name, policy, warps, verify):
+    """table: page table + block-hash probe on every match (verify on);
+    chain: the benchmarked path (chain LRU, no page table) — its eviction
+    victims are logged in the reference's order by construction."""
     s = preset(name)
-    g = gpu_run(s, policy, warps=warps, log=True)
+    g = gpu_run(s, policy, warps=warps, log=True, verify=verify)
     o = oracle_run(s, policy, log=True)
     assert g["status"] == o["status"]
     assert diff_all(g, o, AGENT_ALL) == []
@@ -60,9 +65,10 @@ def test_presets_bit_exact(name, policy, warps):
 
 
 @pytest.mark.parametrize("policy", ["uncontrolled", "aimd"])
-def test_c1_toy_bit_exact(policy):
+@pytest.mark.parametrize("verify", [True, False], ids=["table", "chain"])
+def test_c1_toy_bit_exact(policy, verify):
     s = config.c1_toy(policy)
-    g = gpu_run(s, policy, log=True)
+    g = gpu_run(s, policy, log=True, verify=verify)
     o = oracle_run(s, policy, log=True)
     assert diff_all(g, o, AGENT_ALL) == []
     assert g["log"] == o["log"]
