@@ -93,13 +93,17 @@ u64 xfer_ring(const kvg_sim_desc& d) {
 // big-sim kernel runs one CTA per SM and keeps up to ~200 KB of them (2,048
 // agents = 160 KB), so a lone C2 / C3 leader never leaves shared memory.
 constexpr size_t kBigSmemMax = 200 * 1024;
-size_t hot_smem_bytes(u64 n) {
+// per agent: record 64 B + heap entry 16 B + completion-ring slot 4 B, and
+// in the big kernel the chain-LRU links 8 B (leader.cuh smem_bytes_for);
+// then the two-level ready bitmap
+size_t hot_smem_bytes(u64 n, bool big) {
   const u64 nwords = (n + 31) / 32;
-  return n * (sizeof(kvg::AgentDev) + sizeof(kvg::HeapEnt) + 8) + (nwords + (nwords + 31) / 32) * 4;
+  return n * (sizeof(kvg::AgentDev) + sizeof(kvg::HeapEnt) + 4 + (big ? 8 : 0)) +
+         (nwords + (nwords + 31) / 32) * 4;
 }
 size_t hot_smem(u64 n, bool big = false) {
-  if (!big) return n > 128 ? 0 : hot_smem_bytes(n);
-  const size_t b = hot_smem_bytes(n);
+  if (!big) return n > 128 ? 0 : hot_smem_bytes(n, false);
+  const size_t b = hot_smem_bytes(n, true);
   return b <= kBigSmemMax ? b : 0;
 }
 
@@ -131,8 +135,10 @@ cudaError_t hit_window(const void* d_state, double* m, double* r);
 }  // namespace kvg_tree_seam
 
 namespace kvg_grid_seam {  // engine.cu
-cudaError_t match(const kvg::GridMatchArgs& a, cudaStream_t s);
-cudaError_t evict(const kvg::GridEvictArgs& a, cudaStream_t s, unsigned* blocks_out);
+unsigned match_blocks(int dev);
+unsigned evict_blocks(int dev, unsigned occ_n);
+cudaError_t match(const kvg::GridMatchArgs& a, unsigned blocks, cudaStream_t s);
+cudaError_t evict(const kvg::GridEvictArgs& a, unsigned blocks, cudaStream_t s);
 }  // namespace kvg_grid_seam
 
 struct kvg_cache {
@@ -202,8 +208,9 @@ kvg_status grid_evict(kvg_cache* c, const kvg_cache_op& o, kvg_cache_op_result* 
   a.freed = reinterpret_cast<unsigned int*>(c->gscratch + kGHistBytes);
   a.err = reinterpret_cast<int*>(c->gscratch + kGHistBytes + 4);
   CUDA_TRY(cudaMemset(c->gscratch, 0, kGHistBytes + 8));
+  c->last_blocks = kvg_grid_seam::evict_blocks(c->device, a.occ_n);
   CUDA_TRY(cudaEventRecord(c->ev0));
-  CUDA_TRY(kvg_grid_seam::evict(a, 0, &c->last_blocks));
+  CUDA_TRY(kvg_grid_seam::evict(a, c->last_blocks, 0));
   CUDA_TRY(cudaEventRecord(c->ev1));
   CUDA_TRY(cudaEventSynchronize(c->ev1));
   float ms = 0;
@@ -512,25 +519,15 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
     size_t j = i;
     while (j < n && seen.emplace(agents[j], 0).second) ++j;
     const size_t m = j - i;
-    // work items: every query's private chunks in groups of kGridItemChunks
-    std::vector<u32> iq, ic;
-    iq.reserve(m);
-    ic.reserve(m);
+    u64 max_groups = 0;
     for (size_t k = 0; k < m; ++k) {
       const u64 np = lens[i + k] / ps;
-      if (np <= S) {
-        iq.push_back(static_cast<u32>(k));
-        ic.push_back(~0u);
-        continue;
-      }
-      for (u64 c0 = S >> 5; c0 <= (np - 1) >> 5; c0 += kvg::kGridItemChunks) {
-        iq.push_back(static_cast<u32>(k));
-        ic.push_back(static_cast<u32>(c0));
-      }
+      if (np > S)
+        max_groups = std::max<u64>(
+            max_groups, (((np - 1) >> 5) - (S >> 5)) / kvg::kGridItemChunks + 1);
     }
-    const size_t items = iq.size();
     const size_t words = S / 32 + 1;
-    const size_t need = m * (8 + 4 + 4 + 4) + items * 8 + words * 4 + 256;
+    const size_t need = m * (8 + 4 + 4 + 4 + 4) + words * 4 + 256;
     if (need > c->gq_cap) {
       cudaFree(c->gq);
       c->gq = nullptr;
@@ -543,16 +540,15 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
     u32* d_agents = reinterpret_cast<u32*>(d_lens + m);
     u32* d_fm = d_agents + m;
     u32* d_res = d_fm + m;
-    u32* d_iq = d_res + m;
-    u32* d_ic = d_iq + items;
-    u32* d_smask = d_ic + items;
+    u32* d_cont = d_res + m;
+    u32* d_smask = d_cont + m;
+    unsigned int* d_ncont = d_smask + words;
     kvg::CacheState st{};
     kvg_status rc = cache_state(c, &st);
     if (rc != KVG_OK) return rc;
     CUDA_TRY(cudaMemcpy(d_lens, lens + i, m * 8, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d_agents, agents + i, m * 4, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_iq, iq.data(), items * 4, cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(d_ic, ic.data(), items * 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemset(d_ncont, 0, 4));
     CUDA_TRY(cudaMemset(d_fm, 0xff, m * 4));
     CUDA_TRY(cudaMemset(d_res, 0, m * 4));
     CUDA_TRY(cudaMemset(d_smask, 0, words * 4));
@@ -568,15 +564,16 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
     a.clock0 = st.clock;
     a.agents = d_agents;
     a.lens = d_lens;
-    a.n_items = static_cast<u32>(items);
-    a.item_q = d_iq;
-    a.item_c = d_ic;
+    a.max_groups = static_cast<u32>(max_groups);
+    a.cont = d_cont;
+    a.n_cont = d_ncont;
     a.fm = d_fm;
     a.res = d_res;
     a.smask = d_smask;
     a.best = c->d_best;
+    const unsigned blocks = kvg_grid_seam::match_blocks(c->device);
     CUDA_TRY(cudaEventRecord(c->ev0));
-    CUDA_TRY(kvg_grid_seam::match(a, 0));
+    CUDA_TRY(kvg_grid_seam::match(a, blocks, 0));
     CUDA_TRY(cudaEventRecord(c->ev1));
     CUDA_TRY(cudaEventSynchronize(c->ev1));
     float ms = 0;

@@ -74,6 +74,7 @@ enum OpKind : int {
   OP_FRONTIER,   // offload tree: compact eviction-frontier nodes (tree.cuh)
   OP_TICKS,      // warp 0: pipelined control ticks + no-op admission checks
   OP_PHASES,     // warp 0: phase labels over the trace rows
+  OP_GROUP,      // warp 0: a dispatch batch's completions advanced together
 };
 
 enum RangeFlags : u32 {
@@ -839,6 +840,13 @@ __global__ void __launch_bounds__(256) pack_traces(const SimDev* __restrict__ si
 
 #include "grid.cuh"
 
+#ifdef KVG_GRID_PROF
+extern "C" __attribute__((visibility("default"))) int kvg_debug_gprof(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, kvg::g_gprof, sizeof(kvg::g_gprof));
+  return 0;
+}
+#endif
+
 #ifdef KVG_PROFILE
 // dev-only: read and clear the phase profile (tools/probe_phases.py)
 extern "C" __attribute__((visibility("default"))) int kvg_debug_profile(unsigned long long* out) {
@@ -901,40 +909,57 @@ cudaError_t hit_window(const void* d_state, double* m, double* r) {
 // Host glue of the grid-wide seam kernels (grid.cuh), used by capi.cu.
 namespace kvg_grid_seam {
 
-static int sm_count(int dev) {
-  int n = 0;
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n > 0 ? n : 1;
+// Launch geometry (SM count and occupancy), computed once per device and
+// cached, so no host-side query runs inside a timed launch window.
+struct Geom {
+  int sms = 0, match_per_sm = 0, evict_per_sm = 0;
+};
+static Geom geom_of(int dev) {
+  static Geom g[64];
+  static bool have[64] = {false};
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!have[dev]) {
+    Geom x;
+    cudaDeviceGetAttribute(&x.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x.match_per_sm, kvg::grid_match_kernel,
+                                                  kvg::kGridMatchWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&x.evict_per_sm, kvg::grid_evict_kernel, 512, 0);
+    x.sms = x.sms > 0 ? x.sms : 1;
+    x.match_per_sm = x.match_per_sm > 0 ? x.match_per_sm : 1;
+    x.evict_per_sm = x.evict_per_sm > 0 ? (x.evict_per_sm < 2 ? x.evict_per_sm : 2) : 1;
+    g[dev] = x;
+    have[dev] = true;
+  }
+  return g[dev];
 }
 
-cudaError_t match(const kvg::GridMatchArgs& a, cudaStream_t s) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kvg::grid_match_kernel,
-                                                kvg::kGridMatchWarps * 32, 0);
-  if (per_sm < 1) per_sm = 1;
-  unsigned blocks = static_cast<unsigned>(sm_count(dev) * per_sm);
-  const unsigned need = (a.n_items + kvg::kGridMatchWarps - 1) / kvg::kGridMatchWarps;
+unsigned match_blocks(int dev) {
+  const Geom g = geom_of(dev);
+  return static_cast<unsigned>(g.sms * g.match_per_sm);
+}
+
+// no more CTAs than 32-bucket lane groups to scan (a grid barrier costs the
+// same either way)
+unsigned evict_blocks(int dev, unsigned occ_n) {
+  const Geom g = geom_of(dev);
+  unsigned blocks = static_cast<unsigned>(g.sms * g.evict_per_sm);
+  const unsigned need = (occ_n + 16 * 32 * kvg::kGridSumDepth - 1) / (16 * 32 * kvg::kGridSumDepth);
   if (blocks > need) blocks = need > 0 ? need : 1;
+  return blocks;
+}
+
+cudaError_t match(const kvg::GridMatchArgs& a, unsigned blocks, cudaStream_t s) {
+  const unsigned need = (a.n + kvg::kGridMatchWarps - 1) / kvg::kGridMatchWarps;
   if (a.S > 0) kvg::grid_match_prep_kernel<<<1, 1024, 0, s>>>(a);
-  kvg::grid_match_kernel<<<blocks, kvg::kGridMatchWarps * 32, 0, s>>>(a);
+  kvg::grid_match_kernel<<<need < blocks ? (need ? need : 1) : blocks, kvg::kGridMatchWarps * 32, 0,
+                           s>>>(a);
+  if (a.max_groups > 1)
+    kvg::grid_match_rest_kernel<<<blocks, kvg::kGridMatchWarps * 32, 0, s>>>(a);
   if (a.S > 0) kvg::grid_match_shared_kernel<<<1, 1024, 0, s>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t evict(const kvg::GridEvictArgs& a, cudaStream_t s, unsigned* blocks_out) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kvg::grid_evict_kernel, 512, 0);
-  if (per_sm < 1) per_sm = 1;
-  if (per_sm > 2) per_sm = 2;
-  unsigned blocks = static_cast<unsigned>(sm_count(dev) * per_sm);
-  // no more CTAs than 32-bucket lane groups to scan (the barrier costs the same)
-  const unsigned need = (a.occ_n + 16 * 32 * kvg::kGridSumDepth - 1) / (16 * 32 * kvg::kGridSumDepth);
-  if (blocks > need) blocks = need > 0 ? need : 1;
-  if (blocks_out) *blocks_out = blocks;
+cudaError_t evict(const kvg::GridEvictArgs& a, unsigned blocks, cudaStream_t s) {
   void* args[] = {const_cast<kvg::GridEvictArgs*>(&a)};
   return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kvg::grid_evict_kernel),
                                      dim3(blocks), dim3(512), args, 0, s);

@@ -27,6 +27,19 @@ namespace kvg {
 
 constexpr int kGridMatchWarps = 8;
 
+#ifdef KVG_GRID_PROF  // dev-only phase timestamps of CTA 0 (tools/probe_grid.py)
+__device__ unsigned long long g_gprof[32];
+__device__ __forceinline__ void gprof(int k) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gprof[k] = t;
+  }
+}
+#else
+__device__ __forceinline__ void gprof(int) {}
+#endif
+
 // Shared prompt, probed ONCE per batch (every query's range starts with the
 // same shared chunks): smask[c] = resident pages of shared chunk c.
 __global__ void __launch_bounds__(1024) grid_match_prep_kernel(GridMatchArgs A) {
@@ -50,18 +63,31 @@ __global__ void __launch_bounds__(1024) grid_match_prep_kernel(GridMatchArgs A) 
   }
 }
 
-// One warp per work item: item k covers up to kGridItemChunks private chunks
-// of query item_q[k] starting at chunk item_c[k] (the host splits every
-// query's private range [S, len/ps) so long contexts spread over many warps).
-// Each item probes its chunks (all in flight), refreshes their resident
-// pages to the query's clock (a private chunk has one writer per batch: the
-// host splits batches so an agent appears once) and folds first miss /
-// resident count into the query's accumulators. A query's first item also
-// files its shared range for the shared-stamp pass.
-__global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMatchArgs A) {
-  __shared__ Op wops[kGridMatchWarps];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  Op& op = wops[w];
+// Probes chunk group g (kGridItemChunks chunks, all in flight) of query i's
+// private range [S, len/ps), refreshes its resident pages to the query's
+// clock (a private chunk has one writer per batch: the host splits batches so
+// an agent appears once) and folds first miss / resident count into the
+// query's accumulators. Returns true when the group had no miss.
+__device__ __forceinline__ bool match_group(const GridMatchArgs& A, Op& op, u32 i, u64 n, u64 g,
+                                            int lane) {
+  const u64 c0 = (A.S >> 5) + g * kGridItemChunks;
+  const u64 lo = c0 * 32 > A.S ? c0 * 32 : A.S;
+  const u64 hi_c = (c0 + kGridItemChunks) * 32;
+  const u64 hi = hi_c < n ? hi_c : n;
+  if (lane == 0) post_range(op, A.agents[i], lo, hi, RF_STAMP, 0, A.clock0 + i + 1);
+  __syncwarp();
+  coop_range<kGridItemChunks>(op, 0, lane, 1);
+  __syncwarp();
+  const bool clean = op.first_miss == ~0ull;
+  if (lane == 0) {
+    if (!clean) atomicMin(&A.fm[i], static_cast<u32>(op.first_miss));
+    if (op.resident) atomicAdd(&A.res[i], op.resident);
+  }
+  __syncwarp();
+  return clean;
+}
+
+__device__ __forceinline__ void match_warp_init(const GridMatchArgs& A, Op& op, int lane) {
   if (lane == 0) {
     op.table = A.table;
     op.summ = A.summ;
@@ -74,36 +100,51 @@ __global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMa
     op.log_victims = 0;
   }
   __syncwarp();
+}
+
+__device__ __forceinline__ u64 match_groups(const GridMatchArgs& A, u64 n) {
+  if (n <= A.S) return 0;
+  return (((n - 1) >> 5) - (A.S >> 5)) / kGridItemChunks + 1;
+}
+
+// Pass 1, one warp per query: files the shared range for the shared-stamp
+// pass and probes the first private chunk group. Queries whose first group
+// is fully resident (and that have more) go on the continuation list.
+__global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMatchArgs A) {
+  __shared__ Op wops[kGridMatchWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Op& op = wops[w];
+  match_warp_init(A, op, lane);
   const u32 gw = blockIdx.x * kGridMatchWarps + w, GW = gridDim.x * kGridMatchWarps;
-  for (u32 k = gw; k < A.n_items; k += GW) {
-    const u32 i = A.item_q[k];
-    const u64 c0 = A.item_c[k];
+  for (u32 i = gw; i < A.n; i += GW) {
     const u64 n = A.lens[i] / A.ps;
-    if (c0 == ~0u) {  // head item of a query without private pages
-      if (lane == 0) {
-        const u64 sh = n < A.S ? n : A.S;
-        if (sh > 0) atomicMax(&A.best[sh - 1], i + 1);
-      }
-      continue;
-    }
-    const u64 lo = c0 * 32 > A.S ? c0 * 32 : A.S;
-    const u64 hi_c = (c0 + kGridItemChunks) * 32;
-    const u64 hi = hi_c < n ? hi_c : n;
     if (lane == 0) {
-      post_range(op, A.agents[i], lo, hi, RF_STAMP, 0, A.clock0 + i + 1);
-      if (lo == A.S) {  // the query's first item
-        const u64 sh = n < A.S ? n : A.S;
-        if (sh > 0) atomicMax(&A.best[sh - 1], i + 1);
-      }
+      const u64 sh = n < A.S ? n : A.S;
+      if (sh > 0) atomicMax(&A.best[sh - 1], i + 1);
     }
-    __syncwarp();
-    coop_range<kGridItemChunks>(op, 0, lane, 1);
-    __syncwarp();
-    if (lane == 0) {
-      if (op.first_miss != ~0ull) atomicMin(&A.fm[i], static_cast<u32>(op.first_miss));
-      if (op.resident) atomicAdd(&A.res[i], op.resident);
-    }
-    __syncwarp();
+    const u64 groups = match_groups(A, n);
+    if (groups == 0) continue;
+    if (match_group(A, op, i, n, 0, lane) && groups > 1 && lane == 0)
+      A.cont[atomicAdd(A.n_cont, 1u)] = i;
+  }
+}
+
+// Pass 2: the remaining groups of the continued queries, flattened over
+// (continued query, group) so a long resident context spreads over many warps.
+__global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_rest_kernel(GridMatchArgs A) {
+  __shared__ Op wops[kGridMatchWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  Op& op = wops[w];
+  match_warp_init(A, op, lane);
+  const u64 gw = blockIdx.x * kGridMatchWarps + w, GW = gridDim.x * kGridMatchWarps;
+  const u64 per = A.max_groups - 1;
+  const u64 total = static_cast<u64>(*A.n_cont) * per;
+  for (u64 k = gw; k < total; k += GW) {
+    const u32 i = A.cont[k / per];
+    const u64 g = 1 + k % per;
+    const u64 n = A.lens[i] / A.ps;
+    if (g >= match_groups(A, n)) continue;
+    match_group(A, op, i, n, g, lane);
   }
 }
 
@@ -160,6 +201,85 @@ __global__ void __launch_bounds__(1024) grid_match_shared_kernel(GridMatchArgs A
 
 // ------------------------------------------------------------------ evict
 
+// scan_summ for the grid: the same in-flight depth, but consecutive 32-bucket
+// groups of the occupancy list go to consecutive warps of the whole grid
+// (round robin), so a run of victims — the oldest chains sit together at the
+// front of the list — is spread over every SM instead of a few warps.
+template <int kDepth, typename F>
+__device__ __forceinline__ void grid_scan_summ(const Op& op, u32 gw, int lane, u32 GW, F&& f) {
+  const u32 n_occ = op.occ_n;
+  const u32 groups = (n_occ + 31) / 32;
+  for (u32 it = 0; it * kDepth * GW < groups; ++it) {
+    u32 bk[kDepth];
+    Summ e[kDepth];
+#pragma unroll
+    for (int g = 0; g < kDepth; ++g) {
+      const u32 i = ((it * kDepth + g) * GW + gw) * 32u + lane;
+      bk[g] = i < n_occ ? __ldcg(&op.occ[i]) : NIL32;
+    }
+#pragma unroll
+    for (int g = 0; g < kDepth; ++g) {
+      e[g] = Summ{0, 0, 0, 0, 0, 0};
+      if (bk[g] != NIL32) e[g] = ld_summ(&op.summ[bk[g]]);
+    }
+#pragma unroll 1
+    for (int g = 0; g < kDepth; ++g) {
+      const u32 b0 = bk[0];
+      const Summ e0 = e[0];
+#pragma unroll
+      for (int j = 0; j + 1 < kDepth; ++j) {
+        bk[j] = bk[j + 1];
+        e[j] = e[j + 1];
+      }
+      f(b0 != NIL32, b0, e0);
+    }
+  }
+}
+
+// select_bin over a histogram in SHARED memory (the merged grid histogram is
+// staged there first: one coalesced 8 KB load instead of ~64 dependent L2
+// reads per lane).
+__device__ __forceinline__ u32 select_bin_s(Op& op, const u32* cnt, u32 nbins, int d, int lane,
+                                            u64* rank_in_bin) {
+  const u32 per = (nbins + 31) / 32;
+  const u32 base = lane * per;
+  u32 local = 0;
+  for (u32 i = 0; i < per; ++i)
+    if (base + i < nbins) local += cnt[base + i];
+  u32 incl = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 v = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const u64 need = op.need;
+  const unsigned ballot = __ballot_sync(FULL, static_cast<u64>(incl) >= need);
+  if (ballot == 0) {
+    if (lane == 0) op.err = E_EVICT_MISMATCH;
+    *rank_in_bin = 1;
+    return 0;
+  }
+  const int L = __ffs(ballot) - 1;
+  u64 cum = __shfl_sync(FULL, incl - local, L);
+  u32 bin = 0;
+  if (lane == L) {
+    u32 i = 0;
+    for (; i + 1 < per; ++i) {
+      const u32 c = cnt[base + i];
+      if (cum + c >= need) break;
+      cum += c;
+    }
+    bin = base + i;
+  }
+  bin = __shfl_sync(FULL, bin, L);
+  cum = __shfl_sync(FULL, cum, L);
+  *rank_in_bin = need - cum;
+  if (lane == 0) {
+    op.need = need - cum;
+    op.prefix = (op.prefix << d) | bin;
+  }
+  return bin;
+}
+
 __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
@@ -192,6 +312,7 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
     op.err = E_NONE;
   }
   __syncthreads();
+  gprof(0);
   const bool all = op.all;
   u64 T = 0, cut = 0;
   if (!all) {
@@ -209,7 +330,7 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
       }
       __syncthreads();
       const u64 prefix = op.prefix;
-      scan_summ<kGridSumDepth>(op, gw, lane, GW, [&](bool valid, u32 b, const Summ& e) {
+      grid_scan_summ<kGridSumDepth>(op, gw, lane, GW, [&](bool valid, u32 b, const Summ& e) {
         const bool mixed = valid && (e.sf & kMixed);
         u32 c = 0;
         u64 st = 0;
@@ -232,6 +353,7 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
         }
         if (mixed) hist_mixed(op, hs, b, prefix, lo_bits, shift, nbins, last);
       });
+      gprof(1 + 4 * pass);
       __syncthreads();
       u32* gc = A.ghist + static_cast<size_t>(pass % 3) * 2 * kGridBins;
       u32* gd = gc + kGridBins;
@@ -239,18 +361,27 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
         if (scnt[i]) atomicAdd(&gc[i], scnt[i]);
         if (last && sdmax[i]) atomicMax(&gd[i], sdmax[i]);
       }
+      gprof(2 + 4 * pass);
       grid.sync();
-      if (warp == 0) {  // every CTA selects the same bin from the merged histogram
-        Hist hg{gc, gd};
+      gprof(3 + 4 * pass);
+      // every CTA stages the merged histogram in shared memory and selects
+      // the same bin from it
+      for (u32 i = tid; i < nbins; i += nt) {
+        scnt[i] = __ldcg(&gc[i]);
+        if (last) sdmax[i] = __ldcg(&gd[i]);
+      }
+      __syncthreads();
+      if (warp == 0) {
         u64 rank = 0;
-        const u32 bin = select_bin(op, hg, nbins, d, lane, &rank);
-        if (last && lane == 0) op.cut_depth = static_cast<u64>(__ldcg(&gd[bin])) + 1 - rank;
+        const u32 bin = select_bin_s(op, scnt, nbins, d, lane, &rank);
+        if (last && lane == 0) op.cut_depth = static_cast<u64>(sdmax[bin]) + 1 - rank;
       }
       if (blockIdx.x == 0) {  // the buffer of pass + 2 (read last in pass - 1)
         u32* z = A.ghist + static_cast<size_t>((pass + 2) % 3) * 2 * kGridBins;
         for (u32 i = tid; i < 2 * kGridBins; i += nt) z[i] = 0;
       }
       __syncthreads();
+      gprof(4 + 4 * pass);
       lo_bits = shift;
       ++pass;
     }
@@ -258,26 +389,31 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
     cut = op.cut_depth;
   }
   unsigned int freed = 0;
-  scan_summ<kGridSumDepth>(op, gw, lane, GW, [&](bool valid, u32 b, const Summ& e) {
-    if (!valid) return;
-    if (e.sf & kMixed) {
-      freed += scatter_mixed(op, b, all, T, cut);
-      return;
+  grid_scan_summ<kGridSumDepth>(op, gw, lane, GW, [&](bool valid, u32 b, const Summ& e) {
+    u32 v = 0;
+    u64 st = 0;
+    if (valid) {
+      if (e.sf & kMixed) {
+        freed += scatter_mixed(op, b, all, T, cut);
+      } else if (e.dev != 0) {
+        st = e.sf & kStampMask;
+        v = (all || st < T) ? e.dev : (st == T ? e.dev & ge_mask(e.tag & 0xffffffffull, cut) : 0u);
+      }
     }
-    const u32 c = e.dev;
-    if (c == 0) return;
-    const u64 st = e.sf & kStampMask;
-    const u32 v = (all || st < T) ? c : (st == T ? c & ge_mask(e.tag & 0xffffffffull, cut) : 0u);
-    if (v == 0) return;
-    freed += __popc(v);
-    Slot* bk = &op.table[(size_t)b * kChunk];
-    for (u32 m = v; m != 0; m &= m - 1) {
-      const int l = __ffs(m) - 1;
-      st_meta(&bk[l], 0ull);
-      emit_victim(op, e.tag + l, st, 0);
+    if (v) {
+      freed += __popc(v);
+      if (op.vic)
+        for (u32 m = v; m != 0; m &= m - 1) emit_victim(op, e.tag + (__ffs(m) - 1), st, 0);
+      __stcg(&op.summ[b].dev, e.dev & ~v);
     }
-    __stcg(&op.summ[b].dev, e.dev & ~v);
+    // the victims' slots, one coalesced bucket store per bucket with victims
+    for (unsigned todo = __ballot_sync(FULL, v != 0); todo != 0; todo &= todo - 1) {
+      const int j = __ffs(todo) - 1;
+      const u32 bj = __shfl_sync(FULL, b, j), vj = __shfl_sync(FULL, v, j);
+      if ((vj >> lane) & 1u) st_meta(&op.table[(size_t)bj * kChunk + lane], 0ull);
+    }
   });
+  gprof(30);
   freed = __reduce_add_sync(FULL, freed);
   if (lane == 0 && freed) atomicAdd(A.freed, freed);
   if (tid == 0 && op.err) atomicMax(A.err, op.err);

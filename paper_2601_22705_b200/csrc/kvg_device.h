@@ -128,6 +128,10 @@ struct HeapEnt {
   u64 k;
 };
 constexpr int kAgentBits = 20;  // <= 1,048,575 agents per simulation
+// key = ordinal << kKeyShift | group flag | (agent id, or member count of a
+// completion group: its members wait at the group ring's head, FIFO)
+constexpr int kKeyShift = kAgentBits + 1;
+constexpr u64 kGroupFlag = 1ull << kAgentBits;
 
 struct Member {       // one dispatched batch member (engine.cpp:293-299)
   u32 id, pad;
@@ -164,6 +168,9 @@ struct SimDev {
   u32* rbits;         // ready bitmap: in_active && AwaitingAdmission
   u32* rl1;           // second level: non-empty words of rbits
   u32* lru;           // [2 * n_agents] chain LRU links {prev, next} (leader.cuh)
+  u32* gring;         // [n_agents] completion-group member ring (FIFO of batches)
+  u32 group_min;      // dispatch batches of >= group_min members complete as a group
+  u32 pad_g;
   u32* pin_hist;      // [shared_pages+1]: agents per shared-pin depth
   u32* pin_lvl;       // bitmap of non-empty pin_hist levels
   u32* hist;          // [2 * 512]: eviction radix-select histogram scratch
@@ -232,9 +239,10 @@ struct GridMatchArgs {
   u64 clock0;        // cache clock before the batch
   const u32* agents; // [n]
   const u64* lens;   // [n] sequence lengths, tokens
-  u32 n_items, pad;
-  const u32* item_q; // [n_items] query of each work item
-  const u32* item_c; // [n_items] first private chunk (~0: no private pages)
+  u32 max_groups;    // most private chunk groups of any query
+  u32 pad;
+  u32* cont;         // [n] queries whose first group was fully resident
+  unsigned int* n_cont;
   u32* fm;           // [n] first missing private page (NIL32 = none), atomicMin
   u32* res;          // [n] resident private pages, atomicAdd
   u32* smask;        // [S/32 + 1] resident pages of each shared chunk

@@ -21,6 +21,7 @@
 namespace kvg {
 
 constexpr u32 NIL = 0xffffffffu;
+constexpr uint8_t EV_GROUP_POP = 0xff;  // popped heap key of a completion group
 
 // Leader helpers called from many phases. Inlined: measured on C4, calls
 // (register save/restore through local memory) cost more than the smaller
@@ -47,6 +48,7 @@ enum Phase : int {
   PH_M_RESTORED,
   PH_BATCH_END,
   PH_GEN_DISCARDED,
+  PH_GROUP_DONE,
   // offload mode (node-level tree, tree.cuh)
   PH_O_MEMBER,
   PH_O_RELOAD_CHUNK,
@@ -118,6 +120,11 @@ struct Lead {
   u32* lru;
   u32 lru_head, lru_tail;
   int chain;
+  // completion groups (kernel 4): member ring gring[0, n) (FIFO: groups
+  // complete in dispatch order); the group being advanced starts at grp_start
+  u32* gring;
+  u32 gr_head, gr_n, grp_start, grp_cnt;
+  u32 group_min;
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
 #ifdef KVG_PROFILE
   // dev-only phase profile (tools/probe_phases.py): cycles per leader phase,
@@ -375,11 +382,29 @@ __device__ __forceinline__ void lru_touch(Lead& L, u32 id) {
 // chain from the LRU head loses its unpinned tail (pages [max(S, pinned),
 // S + priv), deepest first), then the shared chain [pin_max, L0). Victims are
 // logged in that order. Chains visited count as scanned (roofline).
+// Without the LRU (the one-warp kernel's small simulations, whose shared
+// memory holds no links) the next chain is found by a scan for the smallest
+// stamp among agents with candidates: stamps are distinct per agent.
+__device__ __forceinline__ u32 chain_min(const Lead& L, u64 S) {
+  u32 best = NIL;
+  u64 best_st = 0;
+  for (u32 i = 0; i < L.n; ++i) {
+    const AgentDev& a = L.ag[i];
+    const u64 lo = a.pinned_pg > S ? a.pinned_pg : S;
+    if (S + a.priv > lo && (best == NIL || a.lazy < best_st)) {
+      best = i;
+      best_st = a.lazy;
+    }
+  }
+  return best;
+}
+
 __device__ __noinline__ void chain_evict(const SimDev& D, Lead& L, u64 need) {
   const u64 S = L.S;
-  u32 id = L.lru_head;
+  const bool scan = L.lru == nullptr;
+  u32 id = scan ? chain_min(L, S) : L.lru_head;
   while (need > 0 && id != NIL) {
-    const u32 nx = L.lru[2 * id + 1];
+    const u32 nx = scan ? NIL : L.lru[2 * id + 1];
     AgentDev& a = L.ag[id];
     const u64 lo = a.pinned_pg > S ? a.pinned_pg : S;
     const u64 hi = S + a.priv;
@@ -395,9 +420,9 @@ __device__ __noinline__ void chain_evict(const SimDev& D, Lead& L, u64 need) {
       }
       a.priv -= static_cast<u32>(t);
       need -= t;
-      if (a.priv == 0) lru_unlink(L, id);
+      if (a.priv == 0 && !scan) lru_unlink(L, id);
     }
-    id = nx;
+    id = scan ? (need > 0 ? chain_min(L, S) : NIL) : nx;
   }
   if (need > 0 && L.L0 > L.pin_max) {
     const u64 t = L.L0 - L.pin_max < need ? L.L0 - L.pin_max : need;
@@ -416,6 +441,8 @@ __device__ __forceinline__ bool heap_less(const HeapEnt& x, const HeapEnt& y) {
   return x.t < y.t || (x.t == y.t && x.k < y.k);
 }
 
+__device__ KVG_MID_FN void heap_push(Lead& L, const HeapEnt e);
+
 // Engine::schedule for agent events (engine.cpp:143-145)
 __device__ KVG_MID_FN void sched_agent(const SimDev& D, Lead& L, u32 id, double t,
                                             uint8_t kind) {
@@ -425,7 +452,10 @@ __device__ KVG_MID_FN void sched_agent(const SimDev& D, Lead& L, u32 id, double 
     return;
   }
   a.ev_kind = kind;
-  const HeapEnt e{t, (L.ord++ << kAgentBits) | id};
+  heap_push(L, HeapEnt{t, (L.ord++ << kKeyShift) | id});
+}
+
+__device__ KVG_MID_FN void heap_push(Lead& L, const HeapEnt e) {
   HeapEnt* h = L.heap;
   u32 i = L.hsize++;
   while (i > 0) {
@@ -747,7 +777,9 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.pin_max = L.pin_priv = 0;
   L.L0 = L.lazy_sh = 0;
   L.verify = D.verify != 0;
+  L.group_min = D.group_min;
   L.lru_head = L.lru_tail = NIL;
+  L.gr_head = L.gr_n = 0;
   L.hit_pages = L.created_pages = L.refreshed_pages = L.evict_scanned = L.agent_events = 0;
   L.hit_m = L.hit_r = 0.0;
   L.n = D.n_agents;
@@ -1423,10 +1455,15 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         u32 agent = 0;
         uint8_t kind = EV_NONE;
         if (which == 0) {
-          agent = static_cast<u32>(L.heap[0].k & ((1u << kAgentBits) - 1));
+          const u64 key = L.heap[0].k;
+          agent = static_cast<u32>(key & ((1u << kAgentBits) - 1));
           heap_pop(D, L);
-          kind = L.ag[agent].ev_kind;
-          L.ag[agent].ev_kind = EV_NONE;
+          if (key & kGroupFlag) {
+            kind = EV_GROUP_POP;
+          } else {
+            kind = L.ag[agent].ev_kind;
+            L.ag[agent].ev_kind = EV_NONE;
+          }
         } else if (which == 1) {
           L.tick_on = 0;
         } else {
@@ -1458,6 +1495,16 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.m_next = ready_next(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
           L.phase = PH_MEMBER;
           continue;
+        }
+        if (kind == EV_GROUP_POP) {  // a dispatch batch completes (kernel 4)
+          L.grp_cnt = agent;  // the group's member count; members at the ring head
+          L.grp_start = L.gr_head;
+          L.gr_head = ring_at(L.gr_head, L.grp_cnt, L.n);
+          L.gr_n -= L.grp_cnt;
+          L.makespan = L.makespan < L.clock ? L.clock : L.makespan;
+          op.kind = OP_GROUP;
+          L.phase = PH_GROUP_DONE;
+          return;
         }
         L.ev_agent = agent;
         ++L.agent_events;
@@ -1576,7 +1623,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         }
         a.lazy = L.m_now;
         L.lazy_sh = L.m_now;
-        if (L.lru[2 * id] != kLruOut) lru_touch(L, id);
+        if (L.lru && L.lru[2 * id] != kLruOut) lru_touch(L, id);
         L.phase = PH_M_MATCHED;
         if (L.verify && L.m_nctx > 0) {
           post_range(op, id, 0, L.m_nctx, 0, 0, 0);
@@ -1705,7 +1752,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           const u64 sh = L.m_nafter < L.S ? L.m_nafter : L.S;
           if (sh > L.L0) L.L0 = sh;
           a.priv = static_cast<u32>(L.m_nafter > L.S ? L.m_nafter - L.S : 0);
-          if (a.priv > 0) lru_touch(L, L.m_id);
+          if (a.priv > 0 && L.lru) lru_touch(L, L.m_id);
         }
         const u64 stored = a.ctx - pmod(L, a.ctx);
         const u64 matched = L.m_f * L.ps;
@@ -1741,12 +1788,30 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.gpu_busy = start + wall;
           L.device_busy += wall;
           const double share = total > 0 ? wall / total : 0.0;
+          const bool group = !(kOff && L.offload) && nb >= L.group_min;
+          u32 tail = ring_at(L.gr_head, L.gr_n, L.n);
           for (u32 i = 0; i < nb; ++i) {
             const Member& m = D.batch[i];
             L.ledger.prefill_fresh += share * m.f;
             L.ledger.prefill_recompute += share * m.r;
             L.ledger.decode += share * m.d;
-            sched_agent(D, L, m.id, start + wall, EV_GEN);
+            if (!group) {
+              sched_agent(D, L, m.id, start + wall, EV_GEN);
+              continue;
+            }
+            // every member completes at start + wall with consecutive
+            // ordinals: nothing can order between them, so the batch
+            // completes as ONE group (kernel 4, coop_group)
+            AgentDev& a = L.ag[m.id];
+            if (a.ev_kind != EV_NONE) fail(L, E_EVENT_BUSY);
+            a.ev_kind = EV_GEN;
+            L.gring[tail] = m.id;
+            tail = ring_at(tail, 1, L.n);
+          }
+          if (group) {
+            L.gr_n += nb;
+            heap_push(L, HeapEnt{start + wall, (L.ord << kKeyShift) | kGroupFlag | nb});
+            L.ord += nb;  // the members' ordinals (engine.cpp:331)
           }
         }
         ++L.events;
@@ -1764,7 +1829,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           const u64 keep = fp > L.S ? fp - L.S : 0;
           AgentDev& a = L.ag[id];
           if (a.priv > keep) a.priv = static_cast<u32>(keep);
-          if (a.priv == 0 && L.lru[2 * id] != kLruOut) lru_unlink(L, id);
+          if (a.priv == 0 && L.lru && L.lru[2 * id] != kLruOut) lru_unlink(L, id);
         }
         log_rec(D, L, KVG_LOG_DISCARD, id, 0, op.freed);
         act_erase(D, L, id);  // on_request_complete / on_agent_finished
@@ -1777,6 +1842,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         L.phase = PH_EVENT;
         continue;
       }
+      case PH_GROUP_DONE:  // coop_group did every member's completion
+        if (op.err) fail(L, op.err);
+        L.phase = PH_EVENT;
+        continue;
       case PH_O_MEMBER:
       case PH_O_RELOAD_CHUNK:
       case PH_O_RELOAD_EVICTED:
@@ -1806,6 +1875,135 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
   }
 }
 
+// ------------------------------------------------------ kernel 4: group advance
+// OP_GROUP (warp 0): the completions of one dispatch batch. Every member of a
+// batch completes at start + wall (engine.cpp:317-332) with consecutive event
+// ordinals, so the reference processes them back to back — no other event can
+// order between them (ticks and admission checks rank after completions at
+// equal times, new events get later ordinals). The agent state machines
+// (on_generation_complete, engine.cpp:184-222: unpin, statistics, step,
+// Generating -> Finished | ToolExecuting | AwaitingAdmission, discard_suffix
+// of finishers) therefore advance one member per LANE; the order-dependent
+// side effects — event ordinals of tool completions and of the admission
+// check, the ledger's tool-wait sum, pending-FIFO pushes, finish ordinals,
+// the event log — are applied by lane 0 in member order afterwards, with the
+// same operations in the same order as the per-event path.
+__device__ __noinline__ void coop_group(const SimDev& D, Lead& L, Op& op, int lane) {
+  const u32 cnt = L.grp_cnt, n = L.n;
+  const double T = L.clock;
+  const u64 S = L.S;
+  const bool req = L.kind == KVG_POLICY_REQUEST_CAP;
+  const u64 fp = pdiv(L, L.shared_len + L.ps - 1);
+  const u64 keep = fp > S ? fp - S : 0;  // discard_suffix keeps page_ceil(shared) (Q2)
+  const u64 ev0 = L.events;
+  u64 gen = 0, rec = 0, ppriv = 0;
+  u32 finished = 0, erased = 0, readied = 0;
+  int bad = 0;
+  for (u32 off = 0; off < cnt; off += 32) {
+    const u32 k = off + lane;
+    if (k < cnt) {
+      const u32 id = L.gring[ring_at(L.grp_start, k, n)];
+      AgentDev& a = L.ag[id];
+      if (a.ev_kind != EV_GEN || a.state != S_GEN) bad = E_ILLEGAL_TRANSITION;
+      a.ev_kind = EV_NONE;
+      // unpin(pinned_len) (engine.cpp:188-191): implicit pins, histogram
+      const u64 old_pg = a.pinned_pg;
+      a.pinned_pg = 0;
+      ppriv += old_pg > S ? old_pg - S : 0;
+      const u64 jo = old_pg < S ? old_pg : S;
+      if (jo > 0 && atomicSub(&D.pin_hist[jo], 1u) == 1u)
+        atomicAnd(&D.pin_lvl[jo >> 5], ~(1u << (jo & 31)));
+      kvg_agent_stats& st = D.stats[id];
+      gen += a.f_gen;
+      rec += a.f_rec;
+      st_add(st.generated_tokens, a.f_gen);
+      st_add(st.recompute_tokens, a.f_rec);
+      if (a.f_rec > 0) st_add(st.recompute_events, 1);
+      ++a.step;
+      if (a.step >= L.steps) {  // Finished: discard_suffix (lane 0, below) + on_agent_finished
+        a.state = S_DONE;
+        if (!a.in_active) bad = E_NOT_ACTIVE;
+        a.in_active = 0;
+        ++erased;
+        ++finished;
+        st.finish_time = T;
+        st.finish_ordinal = ev0 + k;
+      } else if (a.f_has_tool) {
+        a.state = S_TOOL;
+        if (req) {
+          if (!a.in_active) bad = E_NOT_ACTIVE;
+          a.in_active = 0;
+          ++erased;
+        }
+      } else {
+        a.state = S_AWAIT;
+        a.ready_since = T;
+        if (req) {
+          if (!a.in_active) bad = E_NOT_ACTIVE;
+          a.in_active = 0;
+          ++erased;
+        } else if (a.in_active) {  // ready_sync: active and at a step boundary
+          a.ready = 1;
+          const u32 w = id >> 5;
+          if (atomicOr(&L.rbits[w], 1u << (id & 31)) == 0u) atomicOr(&L.rl1[w >> 5], 1u << (w & 31));
+          ++readied;
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gen += __shfl_xor_sync(FULL, gen, o);
+    rec += __shfl_xor_sync(FULL, rec, o);
+    ppriv += __shfl_xor_sync(FULL, ppriv, o);
+  }
+  finished = __reduce_add_sync(FULL, finished);
+  erased = __reduce_add_sync(FULL, erased);
+  readied = __reduce_add_sync(FULL, readied);
+  bad = static_cast<int>(__reduce_max_sync(FULL, static_cast<u32>(bad)));
+  __syncwarp();
+  if (lane != 0) return;
+  op.err = bad;
+  L.decoded_cum += gen;
+  L.rec_cum += rec;
+  L.pin_priv -= ppriv;
+  if (S > 0 && L.pin_max > 0 && D.pin_hist[L.pin_max] == 0) {  // highest pinned level left
+    u64 w = L.pin_max >> 5;
+    u32 bits = D.pin_lvl[w] & ((1u << (L.pin_max & 31)) - 1);
+    while (bits == 0 && w > 0) bits = D.pin_lvl[--w];
+    L.pin_max = bits ? (w << 5) + 31 - __clz(bits) : 0;
+  }
+  L.finished += finished;
+  L.act_size -= erased;
+  L.n_ready += readied;
+  L.agent_events += cnt;
+  // member order: the sequential side effects of each completion handler
+  for (u32 k = 0; k < cnt; ++k) {
+    const u32 id = L.gring[ring_at(L.grp_start, k, n)];
+    AgentDev& a = L.ag[id];
+    if (a.state == S_DONE) {  // PH_GEN_DISCARDED's order
+      const u64 fr = a.priv > keep ? a.priv - keep : 0;
+      if (fr) {
+        a.priv = static_cast<u32>(keep);
+        L.used -= fr;
+        L.discarded += fr * L.ps;
+      }
+      if (a.priv == 0 && L.lru && L.lru[2 * id] != kLruOut) lru_unlink(L, id);
+      if (L.log_on) {
+        log_store(D, L, KVG_LOG_DISCARD, id, 0, fr);
+        log_store(D, L, KVG_LOG_FINISH, id, __double_as_longlong(T), ev0 + k);
+      }
+    } else if (a.state == S_TOOL) {
+      L.ledger.tool_wait += a.f_tool;
+      a.ev_kind = EV_TOOL;
+      heap_push(L, HeapEnt{T + a.f_tool, (L.ord++ << kKeyShift) | id});
+    } else if (req) {
+      pend_push(D, L, id);
+    }
+    sched_admission(L);
+  }
+  L.events += cnt;
+}
+
 // ==========================================================================
 // Kernels
 // ==========================================================================
@@ -1825,9 +2023,9 @@ __device__ __forceinline__ void run_op(Op& op, Hist& h, int tid, int warp, int l
 // Hot agent records / event heap / ready bitmaps go to dynamic shared memory
 // when the host sized it for them (capi.cu hot_smem).
 
-__device__ __forceinline__ size_t smem_bytes_for(u32 n) {
+__device__ __forceinline__ size_t smem_bytes_for(u32 n, bool lru) {
   const u32 nwords = (n + 31) / 32;
-  return static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt) + 2 * sizeof(u32)) +
+  return static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt) + 4 + (lru ? 8 : 0)) +
          (nwords + (nwords + 31) / 32) * sizeof(u32);
 }
 
@@ -1865,7 +2063,7 @@ __device__ __noinline__ void flush_rows(const SimDev& D, Lead& L, int t, int nt,
   if (t == 0) L.n_flushed = n;
 }
 
-template <int kDepth, bool kOff, bool kSmemDesc>
+template <int kDepth, bool kOff, bool kSmemDesc, bool kLru>
 __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   __shared__ Lead L;
   __shared__ Op op;
@@ -1891,17 +2089,22 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     unsigned int dyn_bytes;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn_bytes));
     size_t used = 0;
-    if (n > 0 && smem_bytes_for(n) <= dyn_bytes) {  // the host sized it (capi.cu hot_smem)
-      used = (smem_bytes_for(n) + 15) / 16 * 16;
+    if (n > 0 && smem_bytes_for(n, kLru) <= dyn_bytes) {  // the host sized it (capi.cu hot_smem)
+      used = (smem_bytes_for(n, kLru) + 15) / 16 * 16;
       L.ag = reinterpret_cast<AgentDev*>(dyn);
       L.heap = reinterpret_cast<HeapEnt*>(dyn + static_cast<size_t>(n) * sizeof(AgentDev));
-      L.lru = reinterpret_cast<u32*>(dyn + static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt)));
-      L.rbits = L.lru + 2 * static_cast<size_t>(n);
+      u32* w = reinterpret_cast<u32*>(dyn + static_cast<size_t>(n) * (sizeof(AgentDev) + sizeof(HeapEnt)));
+      L.gring = w;
+      w += n;
+      L.lru = kLru ? w : nullptr;
+      if (kLru) w += 2 * static_cast<size_t>(n);
+      L.rbits = w;
       L.rl1 = L.rbits + nwords;
     } else {
       L.ag = D.agents;
       L.heap = D.heap;
-      L.lru = D.lru;
+      L.lru = kLru ? D.lru : nullptr;
+      L.gring = D.gring;
       L.rbits = D.rbits;
       L.rl1 = D.rl1;
     }
@@ -1932,7 +2135,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     a.act_seq = 0;
     a.ready = 0;
     ag[i] = a;
-    L.lru[2 * i] = kLruOut;
+    if (kLru) L.lru[2 * i] = kLruOut;
     D.pend[i] = i;
     D.stats[i] = kvg_agent_stats{0, 0, 0, 0, 0, 0.0, -1.0, 0};
   }
@@ -1966,6 +2169,8 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
       }
     } else if (op.kind == OP_PHASES) {
       if (warp == 0) coop_phases(D, L, lane);
+    } else if (op.kind == OP_GROUP) {
+      if (warp == 0) coop_group(D, L, op, lane);
     } else {
       run_op<kDepth>(op, h, tid, warp, lane, nw);
     }
@@ -1998,17 +2203,17 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
 #define KVG_SMALL_MINB 28
 #endif
 __global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small(const SimDev* __restrict__ sims) {
-  engine_body<KVG_SMALL_DEPTH, false, true>(sims);
+  engine_body<KVG_SMALL_DEPTH, false, true, false>(sims);
 }
 
 // The same with the offload tier compiled in (batches holding offload sims).
 __global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small_off(const SimDev* __restrict__ sims) {
-  engine_body<KVG_SMALL_DEPTH, true, true>(sims);
+  engine_body<KVG_SMALL_DEPTH, true, true, false>(sims);
 }
 
 // Latency variant: up to 32 warps cooperate on one big simulation.
 __global__ void __launch_bounds__(1024, 1) engine_kernel_big(const SimDev* __restrict__ sims) {
-  engine_body<KVG_BIG_DEPTH, true, KVG_BIG_SMEM_DESC>(sims);
+  engine_body<KVG_BIG_DEPTH, true, KVG_BIG_SMEM_DESC, true>(sims);
 }
 
 }  // namespace kvg
