@@ -865,6 +865,13 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   if (L.finished == L.n || L.status != KVG_OK) return;
   const double t_agent = L.hsize > 0 ? L.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
   const double horizon = L.horizon;
+  {  // nothing to do unless a housekeeping event precedes the next agent
+     // event: leave before loading the whole state (most calls)
+    const bool tk = L.tick_on && (!L.adm_on || L.tick_t <= L.adm_t);
+    if (!tk && !L.adm_on) return;
+    const double t0 = tk ? L.tick_t : L.adm_t;
+    if (!(t0 < t_agent) || t0 > horizon) return;
+  }
   // state that no housekeeping event can change
   const bool nready0 = L.n_ready == 0;
   const u64 act = L.act_size;

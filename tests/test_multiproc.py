@@ -118,3 +118,40 @@ def test_bench_gpus_flag_spawns_ranks():
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+
+
+def _gpu_worker(rank, world, port, q):
+    """One rank of the strong split, computed by the DEVICE engine (both ranks
+    share cuda:0 here: the pool hands out one GPU), gathered over gloo."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = sweep.strong_shard(config.c4_sweep(64, seed=42), rank, world)
+        b = engine.Batch([engine.SimSpec.from_scenario(s) for s in mine], device=0, verify=False)
+        b.run()
+        recs = sweep.records(b.results_raw())
+        b.close()
+        q.put((rank, sweep.gather_records(recs, dist).tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(300)
+def test_gloo_world2_device_engine_shards_match_one_batch():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    b = engine.Batch([engine.SimSpec.from_scenario(s) for s in config.c4_sweep(64, seed=42)],
+                     verify=False)
+    b.run()
+    serial = sweep.records(b.results_raw())
+    b.close()
+    assert got[0] == serial and got[1] == serial
