@@ -63,6 +63,7 @@ def parse_args(argv=None):
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-probe-mode", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--c5-horizon", type=float, default=5e4)
     return p.parse_args(argv)
 
 
@@ -118,9 +119,12 @@ def build_scenarios(args, rank: int, world: int):
     if w == "c5":
         pol, seed = C5_REPLICAS[rank % len(C5_REPLICAS)]
         s = config.c5_stress(pol, seed=seed)
+        s.engine.horizon = args.c5_horizon
         return [s], (f"C5 stress replica {rank}: 65,536 agents x 16 steps, shared 8,192-token "
                      f"prompt, contexts to 107K tokens, 16,777,216-page cache, {pol}, seed {seed}, "
-                     f"horizon 1e6 s simulated")
+                     f"simulated to a {args.c5_horizon:g} s horizon (KVG_ERR_HORIZON, partial "
+                     f"results: the full run turns into a stall storm of ~1e8 failed dispatches "
+                     f"per 1e5 simulated s, DESIGN.md §6)")
     scen = sweep.weak_shard(w, rank, args.sims)
     desc = {
         "c2": "C2: 1024 agents x 16 steps, 4K->55.7K contexts, 2,038,926-page cache, aimd",

@@ -115,10 +115,11 @@ struct Lead {
   double pcie_busy, link_busy;
   double abort_t;    // event time that passed the horizon (KVG_ERR_HORIZON)
   // chain mode (discard, verify off): the cache is held as chains, no page
-  // table. lru = per-agent {prev, next} links of the agents holding private
+  // table. lru = the chain heap (big-sim kernel; nullptr: scan the records):
+  // lru[0, n) heap of agent ids, lru[n, 2n) each agent's heap position
   // pages, in chain-stamp order
   u32* lru;
-  u32 lru_head, lru_tail;
+  u32 ch_n;
   int chain;
   // completion groups (kernel 4): member ring gring[0, n) (FIFO: groups
   // complete in dispatch order); the group being advanced starts at grp_start
@@ -354,37 +355,63 @@ __device__ KVG_LEADER_FN void set_pinned(const SimDev& D, Lead& L, u32 id, u64 t
 // therefore takes chain tails from the LRU head on, then the shared chain's
 // tail (its stamp ties only with the newest agent's chain, whose pages are
 // deeper and go first). The list holds exactly the agents with priv > 0.
-constexpr u32 kLruOut = 0xfffffffeu;  // prev link of an agent not in the list
+// The chain heap: a min-heap (by chain stamp) of the agents whose private
+// chain is evictable right now — resident (priv > 0) and unpinned. An agent
+// pins its whole path from its match until its generation completes (or its
+// insert fails), so it leaves the heap at its match and returns at the unpin
+// with the stamp of its last refresh; pinned agents (thousands in a big
+// dispatch batch) are never walked over. O(log n) per move.
+__device__ __forceinline__ bool ch_has(const Lead& L, u32 id) { return L.lru[L.n + id] != NIL; }
 
-__device__ __forceinline__ void lru_unlink(Lead& L, u32 id) {
-  u32* e = &L.lru[2 * id];
-  const u32 p = e[0], nx = e[1];
-  if (p != NIL) L.lru[2 * p + 1] = nx; else L.lru_head = nx;
-  if (nx != NIL) L.lru[2 * nx] = p; else L.lru_tail = p;
-  e[0] = kLruOut;
+__device__ __forceinline__ void ch_place(Lead& L, u32 i, u32 id) {
+  L.lru[i] = id;
+  L.lru[L.n + id] = i;
 }
 
-// Agent `id` was just refreshed (its stamp is the newest): move / append it
-// to the tail.
-__device__ __forceinline__ void lru_touch(Lead& L, u32 id) {
-  u32* e = &L.lru[2 * id];
-  if (e[0] != kLruOut) {
-    if (L.lru_tail == id) return;
-    lru_unlink(L, id);
+__device__ __noinline__ void ch_sift(Lead& L, u32 i) {
+  u32* h = L.lru;
+  const u32 id = h[i];
+  const u64 key = L.ag[id].lazy;
+  while (i > 0) {  // up
+    const u32 p = (i - 1) >> 1;
+    if (L.ag[h[p]].lazy <= key) break;
+    ch_place(L, i, h[p]);
+    i = p;
   }
-  e[0] = L.lru_tail;
-  e[1] = NIL;
-  if (L.lru_tail != NIL) L.lru[2 * L.lru_tail + 1] = id; else L.lru_head = id;
-  L.lru_tail = id;
+  for (;;) {  // down
+    u32 c = 2 * i + 1;
+    if (c >= L.ch_n) break;
+    if (c + 1 < L.ch_n && L.ag[h[c + 1]].lazy < L.ag[h[c]].lazy) ++c;
+    if (L.ag[h[c]].lazy >= key) break;
+    ch_place(L, i, h[c]);
+    i = c;
+  }
+  ch_place(L, i, id);
 }
 
-// Frees `need` (> 0, <= evictable) pages in reference eviction order: each
-// chain from the LRU head loses its unpinned tail (pages [max(S, pinned),
-// S + priv), deepest first), then the shared chain [pin_max, L0). Victims are
-// logged in that order. Chains visited count as scanned (roofline).
-// Without the LRU (the one-warp kernel's small simulations, whose shared
-// memory holds no links) the next chain is found by a scan for the smallest
-// stamp among agents with candidates: stamps are distinct per agent.
+// agent `id` became evictable (unpinned with priv > 0)
+__device__ __forceinline__ void ch_insert(Lead& L, u32 id) {
+  if (!L.lru || ch_has(L, id)) return;
+  const u32 i = L.ch_n++;
+  ch_place(L, i, id);
+  ch_sift(L, i);
+}
+
+// agent `id` pins its path or lost its last private page
+__device__ __forceinline__ void ch_remove(Lead& L, u32 id) {
+  if (!L.lru || !ch_has(L, id)) return;
+  const u32 i = L.lru[L.n + id];
+  L.lru[L.n + id] = NIL;
+  const u32 last = L.lru[--L.ch_n];
+  if (i < L.ch_n) {
+    ch_place(L, i, last);
+    ch_sift(L, i);
+  }
+}
+
+// Without the heap (the one-warp kernel's small simulations, whose shared
+// memory holds no extra links) the next chain is found by a scan for the
+// smallest stamp among agents with candidates: stamps are distinct per agent.
 __device__ __forceinline__ u32 chain_min(const Lead& L, u64 S) {
   u32 best = NIL;
   u64 best_st = 0;
@@ -399,12 +426,15 @@ __device__ __forceinline__ u32 chain_min(const Lead& L, u64 S) {
   return best;
 }
 
+// Frees `need` (> 0, <= evictable) pages in reference eviction order: each
+// chain from the LRU head loses its unpinned tail (pages [max(S, pinned),
+// S + priv), deepest first), then the shared chain [pin_max, L0). Victims are
+// logged in that order. Chains visited count as scanned (roofline).
 __device__ __noinline__ void chain_evict(const SimDev& D, Lead& L, u64 need) {
   const u64 S = L.S;
   const bool scan = L.lru == nullptr;
-  u32 id = scan ? chain_min(L, S) : L.lru_head;
+  u32 id = scan ? chain_min(L, S) : (L.ch_n ? L.lru[0] : NIL);
   while (need > 0 && id != NIL) {
-    const u32 nx = scan ? NIL : L.lru[2 * id + 1];
     AgentDev& a = L.ag[id];
     const u64 lo = a.pinned_pg > S ? a.pinned_pg : S;
     const u64 hi = S + a.priv;
@@ -420,9 +450,13 @@ __device__ __noinline__ void chain_evict(const SimDev& D, Lead& L, u64 need) {
       }
       a.priv -= static_cast<u32>(t);
       need -= t;
-      if (a.priv == 0 && !scan) lru_unlink(L, id);
+    } else if (!scan) {
+      fail(L, E_EVICT_MISMATCH);  // a heap member must be evictable
+      return;
     }
-    id = scan ? (need > 0 ? chain_min(L, S) : NIL) : nx;
+    if (!scan && a.priv == 0) ch_remove(L, id);
+    if (need == 0) break;
+    id = scan ? chain_min(L, S) : (L.ch_n ? L.lru[0] : NIL);
   }
   if (need > 0 && L.L0 > L.pin_max) {
     const u64 t = L.L0 - L.pin_max < need ? L.L0 - L.pin_max : need;
@@ -778,7 +812,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.L0 = L.lazy_sh = 0;
   L.verify = D.verify != 0;
   L.group_min = D.group_min;
-  L.lru_head = L.lru_tail = NIL;
+  L.ch_n = 0;
   L.gr_head = L.gr_n = 0;
   L.hit_pages = L.created_pages = L.refreshed_pages = L.evict_scanned = L.agent_events = 0;
   L.hit_m = L.hit_r = 0.0;
@@ -1520,6 +1554,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.makespan = L.makespan < L.clock ? L.clock : L.makespan;
           if (!(kOff && L.offload)) {
             set_pinned(D, L, agent, 0);  // unpin(pinned_len) — implicit pins
+            if (a.priv > 0) ch_insert(L, agent);
           } else if (a.pinned_pg > 0) {  // engine.cpp:188-191 on the tree
             t_pin(D, L, agent, static_cast<u64>(a.pinned_pg) * L.ps, -1);
             a.pinned_pg = 0;
@@ -1630,7 +1665,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         }
         a.lazy = L.m_now;
         L.lazy_sh = L.m_now;
-        if (L.lru && L.lru[2 * id] != kLruOut) lru_touch(L, id);
+        ch_remove(L, id);  // its path is pinned from the match on
         L.phase = PH_M_MATCHED;
         if (L.verify && L.m_nctx > 0) {
           post_range(op, id, 0, L.m_nctx, 0, 0, 0);
@@ -1759,7 +1794,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           const u64 sh = L.m_nafter < L.S ? L.m_nafter : L.S;
           if (sh > L.L0) L.L0 = sh;
           a.priv = static_cast<u32>(L.m_nafter > L.S ? L.m_nafter - L.S : 0);
-          if (a.priv > 0 && L.lru) lru_touch(L, L.m_id);
+
         }
         const u64 stored = a.ctx - pmod(L, a.ctx);
         const u64 matched = L.m_f * L.ps;
@@ -1781,6 +1816,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       case PH_M_RESTORED: {
         if (op.err) fail(L, op.err);
         set_pinned(D, L, L.m_id, 0);  // unpin(matched); pinned_len = 0
+        if (L.ag[L.m_id].priv > 0) ch_insert(L, L.m_id);
         st_add(D.stats[L.m_id].stall_events, 1);
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 0, 0);
         L.m_next = ready_next(D, L, L.m_id + 1);
@@ -1836,7 +1872,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           const u64 keep = fp > L.S ? fp - L.S : 0;
           AgentDev& a = L.ag[id];
           if (a.priv > keep) a.priv = static_cast<u32>(keep);
-          if (a.priv == 0 && L.lru && L.lru[2 * id] != kLruOut) lru_unlink(L, id);
+          if (a.priv == 0) ch_remove(L, id);
         }
         log_rec(D, L, KVG_LOG_DISCARD, id, 0, op.freed);
         act_erase(D, L, id);  // on_request_complete / on_agent_finished
@@ -1994,17 +2030,19 @@ __device__ __noinline__ void coop_group(const SimDev& D, Lead& L, Op& op, int la
         L.used -= fr;
         L.discarded += fr * L.ps;
       }
-      if (a.priv == 0 && L.lru && L.lru[2 * id] != kLruOut) lru_unlink(L, id);
+      if (a.priv > 0) ch_insert(L, id);
       if (L.log_on) {
         log_store(D, L, KVG_LOG_DISCARD, id, 0, fr);
         log_store(D, L, KVG_LOG_FINISH, id, __double_as_longlong(T), ev0 + k);
       }
     } else if (a.state == S_TOOL) {
+      if (a.priv > 0) ch_insert(L, id);
       L.ledger.tool_wait += a.f_tool;
       a.ev_kind = EV_TOOL;
       heap_push(L, HeapEnt{T + a.f_tool, (L.ord++ << kKeyShift) | id});
-    } else if (req) {
-      pend_push(D, L, id);
+    } else {
+      if (a.priv > 0) ch_insert(L, id);
+      if (req) pend_push(D, L, id);
     }
     sched_admission(L);
   }
@@ -2142,7 +2180,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     a.act_seq = 0;
     a.ready = 0;
     ag[i] = a;
-    if (kLru) L.lru[2 * i] = kLruOut;
+    if (kLru) L.lru[n + i] = NIL;  // not in the chain heap
     D.pend[i] = i;
     D.stats[i] = kvg_agent_stats{0, 0, 0, 0, 0, 0.0, -1.0, 0};
   }
