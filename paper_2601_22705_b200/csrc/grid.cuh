@@ -70,21 +70,57 @@ __global__ void __launch_bounds__(1024) grid_match_prep_kernel(GridMatchArgs A) 
 // query's accumulators. Returns true when the group had no miss.
 __device__ __forceinline__ bool match_group(const GridMatchArgs& A, Op& op, u32 i, u64 n, u64 g,
                                             int lane) {
+  (void)op;
+  const u64 owner = (static_cast<u64>(A.agents[i]) + 1) << 32;
   const u64 c0 = (A.S >> 5) + g * kGridItemChunks;
-  const u64 lo = c0 * 32 > A.S ? c0 * 32 : A.S;
-  const u64 hi_c = (c0 + kGridItemChunks) * 32;
-  const u64 hi = hi_c < n ? hi_c : n;
-  if (lane == 0) post_range(op, A.agents[i], lo, hi, RF_STAMP, 0, A.clock0 + i + 1);
-  __syncwarp();
-  coop_range<kGridItemChunks>(op, 0, lane, 1);
-  __syncwarp();
-  const bool clean = op.first_miss == ~0ull;
-  if (lane == 0) {
-    if (!clean) atomicMin(&A.fm[i], static_cast<u32>(op.first_miss));
-    if (op.resident) atomicAdd(&A.res[i], op.resident);
+  const u64 stamp = A.clock0 + i + 1;
+  // every probe of the group in flight: one coalesced 512 B bucket load each
+  u32 b[kGridItemChunks];
+  Slot sl[kGridItemChunks];
+#pragma unroll
+  for (int j = 0; j < kGridItemChunks; ++j) {
+    const u64 c = c0 + j;
+    b[j] = 0;
+    sl[j] = Slot{kEmptyKey, 0};
+    if (c * 32 < n) {
+      b[j] = static_cast<u32>(hash64(owner | (c * 32))) & A.mask;
+      sl[j] = ld_slot(&A.table[(size_t)b[j] * kChunk + lane]);
+    }
   }
-  __syncwarp();
-  return clean;
+  u32 miss = NIL32, res = 0;
+#pragma unroll
+  for (int j = 0; j < kGridItemChunks; ++j) {
+    const u64 c = c0 + j;
+    if (c * 32 >= n) break;  // warp-uniform
+    const u64 tag = owner | (c * 32);
+    Slot cur = sl[j];
+    u32 cb = b[j];
+    const u64 k0 = __shfl_sync(FULL, cur.key, 0);
+    bool found = k0 == tag;
+    if (!found && k0 != kEmptyKey) {  // collision: continue the linear probe
+      Op po;
+      po.table = A.table;
+      po.mask = A.mask;
+      found = probe_from(po, tag, (cb + 1) & A.mask, lane, &cb, &cur);
+    }
+    const u64 page = c * 32 + lane;
+    const bool in = page >= A.S && page < n;
+    const bool r = found && in && (cur.meta & kResident);
+    if (in && !r && page < miss) miss = static_cast<u32>(page);
+    res += r;
+    if (__any_sync(FULL, r)) {  // refresh: every resident page in range takes the stamp
+      const u64 nm = r ? m_make(stamp, m_pins(cur.meta)) : cur.meta;
+      if (r) st_meta(&A.table[(size_t)cb * kChunk + lane], nm);
+      summ_write(A.summ, cb, nm, lane);
+    }
+  }
+  miss = __reduce_min_sync(FULL, miss);
+  res = __reduce_add_sync(FULL, res);
+  if (lane == 0) {
+    if (miss != NIL32) atomicMin(&A.fm[i], miss);
+    if (res) atomicAdd(&A.res[i], res);
+  }
+  return miss == NIL32;
 }
 
 __device__ __forceinline__ void match_warp_init(const GridMatchArgs& A, Op& op, int lane) {

@@ -1466,6 +1466,8 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
     switch (L.phase) {
       // ------------------------------------------------ event loop (98-136)
       case PH_EVENT: {
+        for (;;) {
+        if (L.status == KVG_ERR_STATE) break;
         if (ticks_apply(L)) {  // pipelined ticks on warp 0, then back here
           op.kind = OP_TICKS;
           return;
@@ -1491,7 +1493,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         if (which < 0) {
           if (L.finished != L.n) fail(L, E_DRAINED);
           L.phase = PH_DONE;
-          continue;
+          break;  // phase changed: through the dispatch
         }
         u32 agent = 0;
         uint8_t kind = EV_NONE;
@@ -1515,7 +1517,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.status = KVG_ERR_HORIZON;
           L.abort_t = bt;
           L.phase = PH_DONE;
-          continue;
+          break;  // phase changed: through the dispatch
         }
         L.clock = bt;
         if (which == 1) {
@@ -1535,7 +1537,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.b_wall = L.b_total = 0.0;
           L.m_next = ready_next(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
           L.phase = PH_MEMBER;
-          continue;
+          break;  // phase changed: through the dispatch
         }
         if (kind == EV_GROUP_POP) {  // a dispatch batch completes (kernel 4)
           L.grp_cnt = agent;  // the group's member count; members at the ring head
@@ -1572,7 +1574,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
               op.freed = static_cast<unsigned int>(t_discard(D, L, agent, a.ctx, L.shared_len));
               op.err = E_NONE;
               L.phase = PH_GEN_DISCARDED;
-              continue;
+              break;  // phase changed: through the dispatch
             }
             // discard_suffix(context, shared_len) (cache_tree.cpp:404-437) on
             // the held state: the finished agent's private pages from
@@ -1587,7 +1589,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
             }
             op.err = E_NONE;
             L.phase = PH_GEN_DISCARDED;
-            continue;
+            break;  // phase changed: through the dispatch
           }
           const bool req = L.kind == KVG_POLICY_REQUEST_CAP;
           if (a.f_has_tool) {
@@ -1629,6 +1631,8 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           continue;
         }
         fail(L, E_OFFLOAD);
+        break;
+        }  // an event that leaves the phase at PH_EVENT loops here, not through the switch
         continue;
       }
       // --------------------------------------------- dispatch_member (337-396)

@@ -24,8 +24,8 @@ u = dict(zip(h, units))
 def num(k):
     x = float(m[k].replace(",", ""))
     unit = u.get(k, "")
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6,
-             "usecond": 1e-3, "msecond": 1, "second": 1e3}.get(unit, 1)
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "ns": 1e-6,
+             "usecond": 1e-3, "us": 1e-3, "msecond": 1, "ms": 1, "second": 1e3, "s": 1e3}[unit]
     return x * scale
 
 
