@@ -75,6 +75,7 @@ enum OpKind : int {
   OP_TICKS,      // warp 0: pipelined control ticks + no-op admission checks
   OP_PHASES,     // warp 0: phase labels over the trace rows
   OP_GROUP,      // warp 0: a dispatch batch's completions advanced together
+  OP_STORM,      // warp 0: a run of dispatch attempts that all stall, together
 };
 
 enum RangeFlags : u32 {

@@ -126,6 +126,7 @@ struct Lead {
   u32* gring;
   u32 gr_head, gr_n, grp_start, grp_cnt;
   u32 group_min;
+  u32 stall_streak;  // consecutive stalled members in the current dispatch batch
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
 #ifdef KVG_PROFILE
   // dev-only phase profile (tools/probe_phases.py): cycles per leader phase,
@@ -814,6 +815,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.group_min = D.group_min;
   L.ch_n = 0;
   L.gr_head = L.gr_n = 0;
+  L.stall_streak = 0;
   L.hit_pages = L.created_pages = L.refreshed_pages = L.evict_scanned = L.agent_events = 0;
   L.hit_m = L.hit_r = 0.0;
   L.n = D.n_agents;
@@ -1472,7 +1474,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           op.kind = OP_TICKS;
           return;
         }
-        PROF_MARK(L, 40);
+        PROF_MARK(L, 43);
         fast_housekeeping(D, L);
         PROF_MARK(L, PH_EVENT);
         int which = -1;  // 0 agent, 1 tick, 2 admission (the event ranks)
@@ -1526,7 +1528,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           continue;
         }
         if (which == 2) {  // on_admission_check (engine.cpp:268-291)
-          PROF_MARK(L, 41);
+          PROF_MARK(L, 44);
           admission_pass(D, L);
           PROF_MARK(L, PH_EVENT);
           if (L.n_ready == 0) {  // dispatch_batch with an empty ready set
@@ -1534,6 +1536,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
             continue;
           }
           L.batch_n = 0;
+          L.stall_streak = 0;
           L.b_wall = L.b_total = 0.0;
           L.m_next = ready_next(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
           L.phase = PH_MEMBER;
@@ -1651,6 +1654,11 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         if (a.pinned_pg > 0) {  // only reachable with offload transfers
           fail(L, E_OFFLOAD);
           continue;
+        }
+        if (L.chain && L.stall_streak > 0) {  // a stall storm: the warp takes the run
+          op.kind = OP_STORM;
+          op.err = E_NONE;
+          return;  // (coop_storm leaves L.phase at PH_MEMBER)
         }
         L.m_ctx0 = a.ctx;
         L.m_nctx = pdiv(L, a.ctx);
@@ -1805,6 +1813,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 1, stored);
         set_pinned(D, L, L.m_id, stored);  // pin(stored), unpin(matched)
         member_success(D, L, L.m_id, L.m_ctx0, matched);
+        L.stall_streak = 0;
         L.m_next = ready_next(D, L, L.m_id + 1);
         L.phase = PH_MEMBER;
         continue;
@@ -1822,6 +1831,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         set_pinned(D, L, L.m_id, 0);  // unpin(matched); pinned_len = 0
         if (L.ag[L.m_id].priv > 0) ch_insert(L, L.m_id);
         st_add(D.stats[L.m_id].stall_events, 1);
+        ++L.stall_streak;
         log_rec(D, L, KVG_LOG_INSERT, L.m_id, 0, 0);
         L.m_next = ready_next(D, L, L.m_id + 1);
         L.phase = PH_MEMBER;
@@ -2053,6 +2063,149 @@ __device__ __noinline__ void coop_group(const SimDev& D, Lead& L, Op& op, int la
   L.events += cnt;
 }
 
+// ---------------------------------------------------- stall storms (dispatch)
+// OP_STORM (warp 0): in an overcommitted run every dispatch attempt of an
+// admission check can stall — insert finds need > free slots and nothing
+// evictable (cache_tree.cpp:176-186), the member is restored and stays ready
+// (engine.cpp:366-373). While attempts keep failing nothing they depend on
+// changes (used pages, resident chains, the other agents' pins: each attempt
+// pins its matched prefix and unpins it again), so every attempt's outcome
+// follows from the state at the start of the run plus its own match: lane k
+// evaluates the k-th next ready agent's match / insert / evictability exactly
+// as the per-member path would. The leading lanes that stall form the run;
+// lane 0 then applies the order-dependent effects member by member (clock
+// bumps and stamps, the hit-window sums, chain-heap moves, the log). The
+// first attempt that would not stall is left to the per-member path.
+__device__ __noinline__ void coop_storm(const SimDev& D, Lead& L, Op& op, int lane) {
+  const u64 S = L.S, ps = L.ps;
+  const u64 free_slots = L.capacity - L.used;
+  u32 cur = L.m_next;
+  for (;;) {
+    // lane k <- the k-th ready agent from `cur` on: the bitmap words from
+    // cur's on, 32 per round (one coalesced load), set bits ranked by a warp
+    // prefix sum of their popcounts
+    u32 id = NIL;
+    {
+      const u32 w0 = cur >> 5;
+      u32 found = 0;
+      for (u32 base = 0; base < 4 * 32 && found < 32; base += 32) {
+        const u32 w = w0 + base + static_cast<u32>(lane);
+        u32 word = w < L.nwords ? L.rbits[w] : 0u;
+        if (base == 0 && lane == 0) word &= ~0u << (cur & 31);
+        const u32 cnt = __popc(word);
+        u32 incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 v = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const u32 total = __shfl_sync(FULL, incl, 31);
+        const u32 want = static_cast<u32>(lane) - found;  // rank within this round
+        const bool mine = static_cast<u32>(lane) >= found && want < total;
+        u32 src = 0;  // the first lane whose inclusive count exceeds `want`
+        for (int bb = 16; bb > 0; bb >>= 1) {
+          const u32 v = __shfl_sync(FULL, incl, src + bb - 1);
+          if (mine && v <= want) src += bb;
+        }
+        const u32 wsrc = __shfl_sync(FULL, word, src);
+        const u32 before = __shfl_sync(FULL, incl - cnt, src);
+        if (mine) {
+          u32 m = wsrc;
+          for (u32 q = want - before; q > 0; --q) m &= m - 1;
+          id = ((w0 + base + src) << 5) + static_cast<u32>(__ffs(m) - 1);
+        }
+        found += total;
+      }
+    }
+    // this lane's attempt, evaluated on the state the run leaves unchanged
+    bool stalls = false, heaped = false;
+    u64 ctx0 = 0, nctx = 0, f = 0, k_evict = 0;
+    if (id != NIL) {
+      const AgentDev& a = L.ag[id];
+      heaped = L.lru != nullptr && (a.priv > 0 || ch_has(L, id));
+      ctx0 = a.ctx;
+      nctx = pdiv(L, ctx0);
+      const u64 fres = L.L0 < S ? L.L0 : S + a.priv;
+      f = fres < nctx ? fres : nctx;
+      const kvg_step_plan& plan = D.plans[static_cast<size_t>(id) * L.steps + a.step];
+      const u64 nafter = pdiv(L, ctx0 + plan.gen_tokens);
+      const u64 need = nafter - f;
+      // evictable with this attempt's own pin of [0, f) in place
+      const u64 jn = f < S ? f : S;
+      const u64 pmax = L.pin_max > jn ? L.pin_max : jn;
+      const u64 ppriv = L.pin_priv + (f > S ? f - S : 0);
+      const u64 e = L.used - (pmax + ppriv);
+      stalls = a.pinned_pg == 0 && nafter > 0 && need > free_slots && e == 0;
+      k_evict = need - free_slots;
+    }
+    const unsigned ok = __ballot_sync(FULL, !stalls);
+    const u32 run = ok ? static_cast<u32>(__ffs(ok) - 1) : 32u;
+    const u64 c0 = L.cclock;
+    const bool in_run = static_cast<u32>(lane) < run;
+    if (in_run) {
+      AgentDev& a = L.ag[id];
+      a.stalled = 1;
+      if (!heaped) a.lazy = c0 + lane + 1;  // match_prefix's refresh stamp
+      st_add(D.stats[id].stall_events, 1);
+    }
+    u32 lk = in_run ? static_cast<u32>(f + (f < nctx ? 1 : 0)) : 0u;
+    u32 hp = in_run ? static_cast<u32>(f) : 0u;
+    lk = __reduce_add_sync(FULL, lk);
+    hp = __reduce_add_sync(FULL, hp);
+    const unsigned hmask = __ballot_sync(FULL, in_run && heaped);
+    // member order on lane 0 (values of member k broadcast from lane k): the
+    // hit-window sums, chain-heap moves, the log
+    for (u32 k = 0; k < run; ++k) {
+      const u64 fk = __shfl_sync(FULL, f, k);
+      const u64 ck = __shfl_sync(FULL, ctx0, k);
+      if (lane == 0) {
+        L.hit_m += static_cast<double>(fk * ps);
+        L.hit_r += static_cast<double>(ck);
+      }
+      if ((hmask >> k) & 1u || L.log_on) {
+        const u32 idk = __shfl_sync(FULL, id, k);
+        const u64 kk = __shfl_sync(FULL, k_evict, k);
+        if (lane == 0) {
+          if ((hmask >> k) & 1u) {  // out at the match, back with the new stamp
+            ch_remove(L, idk);
+            L.ag[idk].lazy = c0 + k + 1;
+            if (L.ag[idk].priv > 0) ch_insert(L, idk);
+          }
+          if (L.log_on) {
+            L.cclock = c0 + k + 1;
+            log_store(D, L, KVG_LOG_MATCH, idk, fk * ps, 0);
+            log_store(D, L, KVG_LOG_EVICT, idk, kk, 0);
+            log_store(D, L, KVG_LOG_INSERT, idk, 0, 0);
+          }
+        }
+      }
+    }
+    const u32 next = __shfl_sync(FULL, id, run < 32 ? run : 31);
+    const u32 last = __shfl_sync(FULL, id, run > 0 ? run - 1 : 0);
+    u32 after = NIL;
+    if (run == 32) after = ready_next(D, L, last + 1);  // every lane: no broadcast
+    if (lane == 0) {
+      op.err = E_NONE;
+      L.cclock = c0 + run;
+      if (run > 0) {
+        L.lazy_sh = L.cclock;
+        L.lookups += lk;
+        L.hit_pages += hp;
+        L.evict_calls += run;
+        L.stall_streak += run;
+      }
+      if (run < 32) {  // lane `run` holds the next attempt, which does not stall
+        L.m_next = next;  // (NIL: the ready list ended)
+        L.stall_streak = 0;
+      } else {
+        L.m_next = after;
+      }
+    }
+    __syncwarp();
+    if (run < 32 || after == NIL) break;
+    cur = after;
+  }
+}
+
 // ==========================================================================
 // Kernels
 // ==========================================================================
@@ -2220,6 +2373,8 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
       if (warp == 0) coop_phases(D, L, lane);
     } else if (op.kind == OP_GROUP) {
       if (warp == 0) coop_group(D, L, op, lane);
+    } else if (op.kind == OP_STORM) {
+      if (warp == 0) coop_storm(D, L, op, lane);
     } else {
       run_op<kDepth>(op, h, tid, warp, lane, nw);
     }

@@ -7,13 +7,14 @@ sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2601_22705_b200 import config, engine  # noqa: E402
 
 PH = ["EVENT", "MEMBER", "M_MATCHED", "M_INSERT", "M_EVICTED", "M_COMMIT", "M_CREATED", "M_FAIL",
-      "M_RESTORED", "BATCH_END", "GEN_DISCARDED", "O_MEMBER", "O_RELOAD_CHUNK",
+      "M_RESTORED", "BATCH_END", "GEN_DISCARDED", "GROUP_DONE", "O_MEMBER", "O_RELOAD_CHUNK",
       "O_RELOAD_EVICTED", "O_RELOAD_END", "O_INSERT_START", "O_INSERT_COUNT",
       "O_INSERT_EVICTED", "O_INSERT_FAIL", "O_EVICT_POP", "DONE", "FINAL", "EXITED"]
 names = {i: "leader:" + n for i, n in enumerate(PH)}
 names.update({32 + k: "coop:" + n for k, n in enumerate(
-    ["NONE", "EXIT", "RANGE", "EVICT", "REBUILD", "SCANFREE", "FRONTIER", "TICKS", "PHASES"])})
-names.update({41: "admission_pass", 40: "fast_housekeeping", 46: "leader_step entry+sync", 47: "init/finalize"})
+    ["NONE", "EXIT", "RANGE", "EVICT", "REBUILD", "SCANFREE", "FRONTIER", "TICKS", "PHASES",
+     "GROUP"])})
+names.update({44: "admission_pass", 43: "fast_housekeeping", 46: "leader_step entry+sync", 47: "init/finalize"})
 which = sys.argv[1] if len(sys.argv) > 1 else "c4"
 if which == "c4":
     pop = engine.Population(config.c1_toy().workload, 42)
@@ -39,7 +40,7 @@ else:
     specs = [engine.SimSpec.from_scenario(s)]
 lib = engine.lib()
 prof = hasattr(lib, "kvg_debug_profile")  # only in -DKVG_PROFILE builds
-b = engine.Batch(specs)
+b = engine.Batch(specs, verify=False)
 buf = (C.c_ulonglong * 48)()
 if prof:
     lib.kvg_debug_profile.argtypes = [C.POINTER(C.c_ulonglong)]
