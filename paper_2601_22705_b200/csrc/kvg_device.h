@@ -170,7 +170,7 @@ struct SimDev {
   u32* lru;           // [2 * n_agents] chain LRU links {prev, next} (leader.cuh)
   u32* gring;         // [n_agents] completion-group member ring (FIFO of batches)
   u32 group_min;      // dispatch batches of >= group_min members complete as a group
-  u32 pad_g;
+  u32 storm_on;       // stall runs advance on the warp (coop_storm); 0: per member
   u32* pin_hist;      // [shared_pages+1]: agents per shared-pin depth
   u32* pin_lvl;       // bitmap of non-empty pin_hist levels
   u32* hist;          // [2 * 512]: eviction radix-select histogram scratch

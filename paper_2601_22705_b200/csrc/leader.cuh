@@ -127,6 +127,7 @@ struct Lead {
   u32 gr_head, gr_n, grp_start, grp_cnt;
   u32 group_min;
   u32 stall_streak;  // consecutive stalled members in the current dispatch batch
+  u32 storm_on;
   u64 o_matched, o_hm, o_promoted, o_offl, o_pos, o_ka, o_now, o_ev_need, o_ev_rec;
 #ifdef KVG_PROFILE
   // dev-only phase profile (tools/probe_phases.py): cycles per leader phase,
@@ -816,6 +817,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.ch_n = 0;
   L.gr_head = L.gr_n = 0;
   L.stall_streak = 0;
+  L.storm_on = D.storm_on;
   L.hit_pages = L.created_pages = L.refreshed_pages = L.evict_scanned = L.agent_events = 0;
   L.hit_m = L.hit_r = 0.0;
   L.n = D.n_agents;
@@ -1655,7 +1657,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           fail(L, E_OFFLOAD);
           continue;
         }
-        if (L.chain && L.stall_streak > 0) {  // a stall storm: the warp takes the run
+        if (L.chain && L.stall_streak > 0 && L.storm_on) {  // a stall storm: the warp takes the run
           op.kind = OP_STORM;
           op.err = E_NONE;
           return;  // (coop_storm leaves L.phase at PH_MEMBER)
@@ -2088,7 +2090,7 @@ __device__ __noinline__ void coop_storm(const SimDev& D, Lead& L, Op& op, int la
     {
       const u32 w0 = cur >> 5;
       u32 found = 0;
-      for (u32 base = 0; base < 4 * 32 && found < 32; base += 32) {
+      for (u32 base = 0; found < 32 && w0 + base < L.nwords; base += 32) {
         const u32 w = w0 + base + static_cast<u32>(lane);
         u32 word = w < L.nwords ? L.rbits[w] : 0u;
         if (base == 0 && lane == 0) word &= ~0u << (cur & 31);
@@ -2194,7 +2196,7 @@ __device__ __noinline__ void coop_storm(const SimDev& D, Lead& L, Op& op, int la
         L.stall_streak += run;
       }
       if (run < 32) {  // lane `run` holds the next attempt, which does not stall
-        L.m_next = next;  // (NIL: the ready list ended)
+        L.m_next = next;  // (NIL: the ready list ended; the gather covers it all)
         L.stall_streak = 0;
       } else {
         L.m_next = after;
