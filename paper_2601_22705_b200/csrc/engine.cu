@@ -76,6 +76,7 @@ enum OpKind : int {
   OP_PHASES,     // warp 0: phase labels over the trace rows
   OP_GROUP,      // warp 0: a dispatch batch's completions advanced together
   OP_STORM,      // warp 0: a run of dispatch attempts that all stall, together
+  OP_FLUSH,      // warp 0: stream pending trace rows to the host block
 };
 
 enum RangeFlags : u32 {

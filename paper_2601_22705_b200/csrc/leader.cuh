@@ -108,6 +108,7 @@ struct Lead {
   u32 t_alloc, t_free_n, x_head, x_size, o_node, o_c;
   u64 t_next_ord, offloaded, reloaded;
   u64 n_flushed;     // trace rows already streamed to D.trace_out (flush_rows)
+  int stream_on;     // D.trace_out != nullptr and rows are not written through
   u32 log_on;        // D.log != nullptr
   double b_wall, b_total;  // dispatch batch: max and sum of member times so far
   int ps_shift;      // log2(ps) when ps is a power of two, else -1 (pdiv / pmod)
@@ -163,6 +164,24 @@ __device__ __noinline__ void log_store(const SimDev& D, Lead& L, u32 kind, u32 a
 __device__ __forceinline__ void log_rec(const SimDev& D, Lead& L, u32 kind, u32 agent, u64 a,
                                         u64 b) {
   if (L.log_on) log_store(D, L, kind, agent, a, b);
+}
+
+// Trace rows go to HBM (the phase classifier reads them back); a batch
+// delivering to the host streams them to its slice of the mapped pinned host
+// block in warp-wide flushes (flush_rows: after pipelined tick rounds and,
+// through OP_FLUSH, whenever kFlushRows are pending at an event), so the PCIe
+// writes spread over the run instead of queueing behind its end.
+// (KVG_ROW_WT=1: write every row through from the producing thread.)
+#ifndef KVG_FLUSH_ROWS
+#define KVG_FLUSH_ROWS 128
+#endif
+constexpr u64 kFlushRows = KVG_FLUSH_ROWS;
+#ifndef KVG_ROW_WT  // measured: single-thread 8 B stores to host memory, 2x slower
+#define KVG_ROW_WT 0
+#endif
+__device__ __forceinline__ void put_row(const SimDev& D, u64 i, const kvg_trace_row& row) {
+  D.trace[i] = row;
+  if (KVG_ROW_WT && D.trace_out) D.trace_out[i] = row;
 }
 
 // lifecycle_edge (workload.cpp:110-128)
@@ -638,7 +657,7 @@ __device__ __noinline__ void on_tick(const SimDev& D, Lead& L) {
     row.transfers = L.offload ? x_in_flight(D, L, L.clock) : 0;
     row.hit_matched = m;
     row.hit_requested = r;
-    D.trace[i] = row;
+    put_row(D, i, row);
   }
   L.hit_m *= L.decay;  // CacheTree::decay_hit_window (cache_tree.cpp:453-456)
   L.hit_r *= L.decay;
@@ -808,6 +827,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.n_ready = 0;
   L.used = L.cclock = L.discarded = L.lookups = 0;
   L.n_flushed = 0;
+  L.stream_on = D.trace_out != nullptr && !KVG_ROW_WT;
   L.log_on = D.log != nullptr;
   L.agent_steps = L.events = L.evict_calls = L.evicted = 0;
   L.pin_max = L.pin_priv = 0;
@@ -920,7 +940,6 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   const u64 pending = static_cast<u64>(L.pend_size) + L.paus_size;
   const u64 dec = L.decoded_cum, rec = L.rec_cum;
   const u64 trace_cap = D.trace_cap;
-  kvg_trace_row* const trace = D.trace;
   const kvg_controller_config c = L.cfg;
   // evolving state
   double clock = L.clock, tick_t = L.tick_t, adm_t = L.adm_t;
@@ -982,7 +1001,7 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
         row.transfers = L.offload ? x_in_flight(D, L, clock) : 0;
         row.hit_matched = m;
         row.hit_requested = r;
-        trace[i] = row;
+        put_row(D, i, row);
       }
       hit_m = m * decay;
       hit_r = r * decay;
@@ -1127,7 +1146,7 @@ __device__ __noinline__ void coop_ticks(const SimDev& D, Lead& L, int lane) {
       row.transfers = 0;
       row.hit_matched = m;
       row.hit_requested = r;
-      D.trace[n_trace + lane] = row;
+      put_row(D, n_trace + lane, row);
     }
     // carry the state of the last processed tick
     const int last = K - 1;
@@ -1472,6 +1491,13 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
       case PH_EVENT: {
         for (;;) {
         if (L.status == KVG_ERR_STATE) break;
+        if (L.stream_on) {  // streamed host delivery: flush pending rows on the warp
+          const u64 nt = L.n_trace < D.trace_cap ? L.n_trace : D.trace_cap;
+          if (nt >= L.n_flushed + kFlushRows) {
+            op.kind = OP_FLUSH;
+            return;
+          }
+        }
         if (ticks_apply(L)) {  // pipelined ticks on warp 0, then back here
           op.kind = OP_TICKS;
           return;
@@ -2238,10 +2264,7 @@ __device__ __forceinline__ size_t smem_bytes_for(u32 n, bool lru) {
 // consecutive lanes (full PCIe write bursts). Rows are append-only, so a
 // flushed row never changes. Called by warp 0 after a control-tick round
 // (when at least `min_rows` are pending) and by the whole CTA at the end.
-#ifndef KVG_FLUSH_ROWS
-#define KVG_FLUSH_ROWS 128
-#endif
-constexpr u64 kFlushRows = KVG_FLUSH_ROWS;
+
 __device__ __noinline__ void flush_rows(const SimDev& D, Lead& L, int t, int nt, u64 min_rows) {
   const u64 n = L.n_trace < D.trace_cap ? L.n_trace : D.trace_cap;
   const u64 f = L.n_flushed;
@@ -2366,7 +2389,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     if (op.kind == OP_TICKS) {
       if (warp == 0) {
         coop_ticks(D, L, lane);
-        if (stream) {
+        if (stream && !KVG_ROW_WT) {
           __syncwarp();
           flush_rows(D, L, lane, 32, kFlushRows);
         }
@@ -2377,13 +2400,15 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
       if (warp == 0) coop_group(D, L, op, lane);
     } else if (op.kind == OP_STORM) {
       if (warp == 0) coop_storm(D, L, op, lane);
+    } else if (op.kind == OP_FLUSH) {
+      if (warp == 0) flush_rows(D, L, lane, 32, 0);
     } else {
       run_op<kDepth>(op, h, tid, warp, lane, nw);
     }
     __syncthreads();
     if (tid == 0) PROF_MARK(L, 46);
   }
-  if (stream) flush_rows(D, L, tid, blockDim.x, 0);  // the rest
+  if (stream && !KVG_ROW_WT) flush_rows(D, L, tid, blockDim.x, 0);  // the rest
 #ifdef KVG_PROFILE
   if (tid == 0) {
     PROF_MARK(L, 47);
