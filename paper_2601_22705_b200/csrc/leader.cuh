@@ -1479,6 +1479,80 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
 // Runs the state machine until a cooperative op is posted in `op`.
 // kOff = false compiles the discard-only state machine: no offload phases,
 // no tree code, a smaller hot loop for sweeps of discard-mode simulations.
+// dispatch_member (engine.cpp:337-396) in chain mode after its match_prefix
+// (PH_MEMBER): the insert loop with chain evictions, the commit / leaf and the
+// success or stall bookkeeping — the same statements as the phases
+// PH_M_MATCHED .. PH_M_RESTORED, straight through: no cooperative op is ever
+// needed in chain mode, so the member does not return to the phase dispatch
+// between them.
+__device__ __forceinline__ void chain_member(const SimDev& D, Lead& L) {
+  const u64 f = L.m_f;
+  const u64 matched = f * L.ps;
+  L.lookups += f + (f < L.m_nctx ? 1 : 0);
+  L.hit_pages += f;
+  L.hit_m += static_cast<double>(matched);
+  L.hit_r += static_cast<double>(L.m_ctx0);
+  log_rec(D, L, KVG_LOG_MATCH, L.m_id, matched, 0);
+  set_pinned(D, L, L.m_id, matched);  // pin(matched) (engine.cpp:340-342)
+  AgentDev& a = L.ag[L.m_id];
+  const kvg_step_plan& plan = D.plans[static_cast<size_t>(L.m_id) * L.steps + a.step];
+  a.ctx += plan.gen_tokens;  // append_tokens
+  L.m_nafter = pdiv(L, a.ctx);
+  u64 created = 0;
+  bool ok = true;
+  if (L.m_nafter > 0) {  // (nothing to cache: ok, no clock bump)
+    for (;;) {  // CacheTree::insert loop (cache_tree.cpp:170-187)
+      const u64 need = L.m_nafter - f;  // path [0,f) is pinned: recount is constant
+      const u64 free_slots = L.capacity - L.used;
+      if (need <= free_slots) {
+        ++L.cclock;  // insert clock bump (cache_tree.cpp:188)
+        a.lazy = L.cclock;
+        L.lazy_sh = L.cclock;
+        created = f < L.m_nafter ? L.m_nafter - f : 0;  // the leaf extends the chain
+        break;
+      }
+      const u64 k = need - free_slots;
+      const u64 e = L.used - (L.pin_max + L.pin_priv);
+      ++L.evict_calls;
+      log_rec(D, L, KVG_LOG_EVICT, L.m_id, k, k < e ? k : e);
+      if (e == 0) {  // O(1) nothing-evictable fast path
+        ok = false;
+        break;
+      }
+      const u64 r = k < e ? k : e;
+      chain_evict(D, L, r);
+      if (L.status == KVG_ERR_STATE) return;
+      L.used -= r;
+      L.discarded += r * L.ps;
+      L.evicted += r;
+    }
+  }
+  if (ok) {  // PH_M_CREATED
+    L.used += created;
+    L.created_pages += created;
+    if (L.m_nafter > 0) {  // the whole path [0, n_after) is resident now
+      L.refreshed_pages += f;
+      const u64 sh = L.m_nafter < L.S ? L.m_nafter : L.S;
+      if (sh > L.L0) L.L0 = sh;
+      a.priv = static_cast<u32>(L.m_nafter > L.S ? L.m_nafter - L.S : 0);
+    }
+    const u64 stored = a.ctx - pmod(L, a.ctx);
+    log_rec(D, L, KVG_LOG_INSERT, L.m_id, 1, stored);
+    set_pinned(D, L, L.m_id, stored);  // pin(stored), unpin(matched)
+    member_success(D, L, L.m_id, L.m_ctx0, matched);
+    L.stall_streak = 0;
+  } else {  // PH_M_FAIL + PH_M_RESTORED (engine.cpp:366-373)
+    a.ctx = static_cast<u32>(L.m_ctx0);  // context.resize + token_counter rollback
+    a.stalled = 1;
+    set_pinned(D, L, L.m_id, 0);  // unpin(matched); pinned_len = 0
+    if (a.priv > 0) ch_insert(L, L.m_id);
+    st_add(D.stats[L.m_id].stall_events, 1);
+    ++L.stall_streak;
+    log_rec(D, L, KVG_LOG_INSERT, L.m_id, 0, 0);
+  }
+  L.m_next = ready_next(D, L, L.m_id + 1);
+}
+
 template <bool kOff>
 __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
   op.kind = OP_NONE;
@@ -1672,16 +1746,17 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.phase = PH_O_MEMBER;
           continue;
         }
+        for (;;) {  // chain mode: whole member attempts inline, one after another
         const u32 id = L.m_next;
         if (id == NIL) {
           L.phase = PH_BATCH_END;
-          continue;
+          break;
         }
         AgentDev& a = L.ag[id];
         L.m_id = id;
         if (a.pinned_pg > 0) {  // only reachable with offload transfers
           fail(L, E_OFFLOAD);
-          continue;
+          break;
         }
         if (L.chain && L.stall_streak > 0 && L.storm_on) {  // a stall storm: the warp takes the run
           op.kind = OP_STORM;
@@ -1706,12 +1781,19 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         a.lazy = L.m_now;
         L.lazy_sh = L.m_now;
         ch_remove(L, id);  // its path is pinned from the match on
+        if (L.chain) {
+          chain_member(D, L);
+          if (L.status == KVG_ERR_STATE) break;
+          continue;  // the next member
+        }
         L.phase = PH_M_MATCHED;
         if (L.verify && L.m_nctx > 0) {
           post_range(op, id, 0, L.m_nctx, 0, 0, 0);
           return;
         }
         op.err = E_NONE;
+        break;
+        }  // member loop
         continue;
       }
       case PH_M_MATCHED: {
