@@ -1553,6 +1553,47 @@ __device__ __forceinline__ void chain_member(const SimDev& D, Lead& L) {
   L.m_next = ready_next(D, L, L.m_id + 1);
 }
 
+// dispatch_batch's end (engine.cpp:317-332): the batch wall starts at
+// max(clock, device busy), the ledger shares, and the completions (one group
+// entry for a batch of >= group_min members, kernel 4).
+template <bool kOff>
+__device__ __forceinline__ void batch_end(const SimDev& D, Lead& L) {
+  const u32 nb = L.batch_n;
+  if (nb > 0) {
+    const double wall = L.b_wall, total = L.b_total;
+    const double start = L.clock < L.gpu_busy ? L.gpu_busy : L.clock;
+    L.gpu_busy = start + wall;
+    L.device_busy += wall;
+    const double share = total > 0 ? wall / total : 0.0;
+    const bool group = !(kOff && L.offload) && nb >= L.group_min;
+    u32 tail = ring_at(L.gr_head, L.gr_n, L.n);
+    for (u32 i = 0; i < nb; ++i) {
+      const Member& m = D.batch[i];
+      L.ledger.prefill_fresh += share * m.f;
+      L.ledger.prefill_recompute += share * m.r;
+      L.ledger.decode += share * m.d;
+      if (!group) {
+        sched_agent(D, L, m.id, start + wall, EV_GEN);
+        continue;
+      }
+      // every member completes at start + wall with consecutive
+      // ordinals: nothing can order between them, so the batch
+      // completes as ONE group (kernel 4, coop_group)
+      AgentDev& a = L.ag[m.id];
+      if (a.ev_kind != EV_NONE) fail(L, E_EVENT_BUSY);
+      a.ev_kind = EV_GEN;
+      L.gring[tail] = m.id;
+      tail = ring_at(tail, 1, L.n);
+    }
+    if (group) {
+      L.gr_n += nb;
+      heap_push(L, HeapEnt{start + wall, (L.ord << kKeyShift) | kGroupFlag | nb});
+      L.ord += nb;  // the members' ordinals (engine.cpp:331)
+    }
+  }
+  ++L.events;
+}
+
 template <bool kOff>
 __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
   op.kind = OP_NONE;
@@ -1749,7 +1790,12 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         for (;;) {  // chain mode: whole member attempts inline, one after another
         const u32 id = L.m_next;
         if (id == NIL) {
-          L.phase = PH_BATCH_END;
+          if (L.chain) {  // the batch ends here, straight back to the event loop
+            batch_end<kOff>(D, L);
+            L.phase = PH_EVENT;
+          } else {
+            L.phase = PH_BATCH_END;
+          }
           break;
         }
         AgentDev& a = L.ag[id];
@@ -1948,40 +1994,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         continue;
       }
       case PH_BATCH_END: {  // engine.cpp:317-332
-        const u32 nb = L.batch_n;
-        if (nb > 0) {
-          const double wall = L.b_wall, total = L.b_total;
-          const double start = L.clock < L.gpu_busy ? L.gpu_busy : L.clock;
-          L.gpu_busy = start + wall;
-          L.device_busy += wall;
-          const double share = total > 0 ? wall / total : 0.0;
-          const bool group = !(kOff && L.offload) && nb >= L.group_min;
-          u32 tail = ring_at(L.gr_head, L.gr_n, L.n);
-          for (u32 i = 0; i < nb; ++i) {
-            const Member& m = D.batch[i];
-            L.ledger.prefill_fresh += share * m.f;
-            L.ledger.prefill_recompute += share * m.r;
-            L.ledger.decode += share * m.d;
-            if (!group) {
-              sched_agent(D, L, m.id, start + wall, EV_GEN);
-              continue;
-            }
-            // every member completes at start + wall with consecutive
-            // ordinals: nothing can order between them, so the batch
-            // completes as ONE group (kernel 4, coop_group)
-            AgentDev& a = L.ag[m.id];
-            if (a.ev_kind != EV_NONE) fail(L, E_EVENT_BUSY);
-            a.ev_kind = EV_GEN;
-            L.gring[tail] = m.id;
-            tail = ring_at(tail, 1, L.n);
-          }
-          if (group) {
-            L.gr_n += nb;
-            heap_push(L, HeapEnt{start + wall, (L.ord << kKeyShift) | kGroupFlag | nb});
-            L.ord += nb;  // the members' ordinals (engine.cpp:331)
-          }
-        }
-        ++L.events;
+        batch_end<kOff>(D, L);
         L.phase = PH_EVENT;
         continue;
       }
