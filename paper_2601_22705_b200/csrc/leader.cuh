@@ -1594,6 +1594,68 @@ __device__ __forceinline__ void batch_end(const SimDev& D, Lead& L) {
   ++L.events;
 }
 
+// dispatch_batch's member loop (engine.cpp:305-333) from L.m_next on. Returns
+// true when it posted a cooperative op (the caller returns to the CTA);
+// otherwise L.phase says where to go on (PH_EVENT after an inline batch end in
+// chain mode; a member phase in table / verify mode).
+template <bool kOff>
+__device__ __forceinline__ bool member_loop(const SimDev& D, Lead& L, Op& op) {
+  for (;;) {  // chain mode: whole member attempts inline, one after another
+  const u32 id = L.m_next;
+  if (id == NIL) {
+    if (L.chain) {  // the batch ends here, straight back to the event loop
+      batch_end<kOff>(D, L);
+      L.phase = PH_EVENT;
+    } else {
+      L.phase = PH_BATCH_END;
+    }
+    break;
+  }
+  AgentDev& a = L.ag[id];
+  L.m_id = id;
+  if (a.pinned_pg > 0) {  // only reachable with offload transfers
+    fail(L, E_OFFLOAD);
+    break;
+  }
+  if (L.chain && L.stall_streak > 0 && L.storm_on) {  // a stall storm: the warp takes the run
+    op.kind = OP_STORM;
+    op.err = E_NONE;
+    return true;  // (coop_storm leaves L.phase at PH_MEMBER)
+  }
+  L.m_ctx0 = a.ctx;
+  L.m_nctx = pdiv(L, a.ctx);
+  L.m_now = ++L.cclock;  // match_prefix clock bump (cache_tree.cpp:115)
+  // match_prefix (cache_tree.cpp:114-142). Residency is prefix-closed
+  // along a path and chains only gain pages at their ends (insert) and
+  // lose tails (eviction, discard), so the first miss is held
+  // incrementally: L0 resident shared pages, a.priv resident private
+  // ones. The refresh stamps the whole resident path; every resident
+  // page of a chain carries its chain's latest stamp, so the refresh is
+  // two scalar writes. verify=1 re-derives f with the
+  // block-hash probe (kernel 1) and checks it.
+  {
+    const u64 fres = L.L0 < L.S ? L.L0 : L.S + a.priv;
+    L.m_f = fres < L.m_nctx ? fres : L.m_nctx;
+  }
+  a.lazy = L.m_now;
+  L.lazy_sh = L.m_now;
+  ch_remove(L, id);  // its path is pinned from the match on
+  if (L.chain) {
+    chain_member(D, L);
+    if (L.status == KVG_ERR_STATE) break;
+    continue;  // the next member
+  }
+  L.phase = PH_M_MATCHED;
+  if (L.verify && L.m_nctx > 0) {
+    post_range(op, id, 0, L.m_nctx, 0, 0, 0);
+    return true;
+  }
+  op.err = E_NONE;
+  break;
+  }  // member loop
+  return false;
+}
+
 template <bool kOff>
 __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
   op.kind = OP_NONE;
@@ -1683,6 +1745,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.b_wall = L.b_total = 0.0;
           L.m_next = ready_next(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
           L.phase = PH_MEMBER;
+          if (L.chain) {  // members and the batch end inline, then this loop
+            if (member_loop<kOff>(D, L, op)) return;
+            if (L.phase == PH_EVENT) continue;
+          }
           break;  // phase changed: through the dispatch
         }
         if (kind == EV_GROUP_POP) {  // a dispatch batch completes (kernel 4)
@@ -1787,59 +1853,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.phase = PH_O_MEMBER;
           continue;
         }
-        for (;;) {  // chain mode: whole member attempts inline, one after another
-        const u32 id = L.m_next;
-        if (id == NIL) {
-          if (L.chain) {  // the batch ends here, straight back to the event loop
-            batch_end<kOff>(D, L);
-            L.phase = PH_EVENT;
-          } else {
-            L.phase = PH_BATCH_END;
-          }
-          break;
-        }
-        AgentDev& a = L.ag[id];
-        L.m_id = id;
-        if (a.pinned_pg > 0) {  // only reachable with offload transfers
-          fail(L, E_OFFLOAD);
-          break;
-        }
-        if (L.chain && L.stall_streak > 0 && L.storm_on) {  // a stall storm: the warp takes the run
-          op.kind = OP_STORM;
-          op.err = E_NONE;
-          return;  // (coop_storm leaves L.phase at PH_MEMBER)
-        }
-        L.m_ctx0 = a.ctx;
-        L.m_nctx = pdiv(L, a.ctx);
-        L.m_now = ++L.cclock;  // match_prefix clock bump (cache_tree.cpp:115)
-        // match_prefix (cache_tree.cpp:114-142). Residency is prefix-closed
-        // along a path and chains only gain pages at their ends (insert) and
-        // lose tails (eviction, discard), so the first miss is held
-        // incrementally: L0 resident shared pages, a.priv resident private
-        // ones. The refresh stamps the whole resident path; every resident
-        // page of a chain carries its chain's latest stamp, so the refresh is
-        // two scalar writes. verify=1 re-derives f with the
-        // block-hash probe (kernel 1) and checks it.
-        {
-          const u64 fres = L.L0 < L.S ? L.L0 : L.S + a.priv;
-          L.m_f = fres < L.m_nctx ? fres : L.m_nctx;
-        }
-        a.lazy = L.m_now;
-        L.lazy_sh = L.m_now;
-        ch_remove(L, id);  // its path is pinned from the match on
-        if (L.chain) {
-          chain_member(D, L);
-          if (L.status == KVG_ERR_STATE) break;
-          continue;  // the next member
-        }
-        L.phase = PH_M_MATCHED;
-        if (L.verify && L.m_nctx > 0) {
-          post_range(op, id, 0, L.m_nctx, 0, 0, 0);
-          return;
-        }
-        op.err = E_NONE;
-        break;
-        }  // member loop
+        if (member_loop<kOff>(D, L, op)) return;
         continue;
       }
       case PH_M_MATCHED: {
