@@ -511,7 +511,6 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
   CUDA_TRY(cudaSetDevice(c->device));
   c->last_ms = 0;
   const u64 S = c->shared_pages, ps = c->page_size;
-  std::vector<kvg_cache_op_result> out(n);
   size_t i = 0;
   while (i < n) {
     // one sub-batch: no agent twice, so a private chunk has a single writer
@@ -624,7 +623,6 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
     c->hit_r = st.hit_r;
     i = j;
   }
-  (void)out;
   return KVG_OK;
 }
 

@@ -10,19 +10,22 @@
 //    all scalar bookkeeping as an explicit state machine, in IEEE double with
 //    FMA contraction disabled (-fmad=false) so every simulated time is
 //    bit-identical to the reference;
-//  * whenever the leader needs page-level work it posts a COOPERATIVE OP in
-//    shared memory and the whole CTA executes it:
+//  * the discard-mode cache is held in CHAIN form on the benchmarked path
+//    (verify off: per-agent chains, stamp-ordered eviction, no page table,
+//    leader.cuh); with verify on, and in the CacheTree seam, it is the page
+//    table below and the leader posts COOPERATIVE OPS the CTA executes:
 //      RANGE   warp-cooperative block-hash prefix lookup / stamp refresh /
 //              pin / create / free over an agent's page range (kernel 1),
-//      EVICT   shared-memory radix select over page last-use stamps plus a
-//              scatter that frees the chosen pages (kernel 2),
-//      REBUILD rehash of live buckets into the alternate table.
-//    The event heap, ready set and pin bookkeeping are leader-only O(log n) /
-//    O(1) structures (leader.cuh), so ticks and admissions never need the CTA.
-//  * tick signals (kernel 3) and the agent state machine (kernel 4) are
-//    leader-side O(1) steps fused into the same persistent kernel, because the
+//      EVICT   radix select over the bucket summaries' last-use stamps plus
+//              a scatter that frees the chosen pages (kernel 2),
+//      REBUILD rehash of live buckets into the alternate table;
+//    grid-wide forms of kernels 1-2 for big tables are in grid.cuh;
+//  * warp-cooperative leader steps: pipelined control ticks (kernel 3),
+//    completion-group advance of the agent state machines and stall-storm
+//    runs (kernel 4), phase labels, trace-row streaming (leader.cuh). The
 //    reference's strictly sequential event order (engine.cpp:98-136) leaves no
-//    independent work to spread over a launch per tick.
+//    independent work for a launch per tick, so all of it lives in one
+//    persistent kernel per batch.
 #include <cuda_runtime.h>
 #include <stdint.h>
 

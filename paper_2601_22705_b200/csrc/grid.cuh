@@ -2,17 +2,20 @@
 // bandwidth form of kernels 1 and 2 on C2 / C5-size tables, where one CTA per
 // operation (cache_kernel) cannot pull more than a single SM's share of HBM.
 //
-//  * grid_match_kernel / grid_match_shared_kernel — a BATCH of match_prefix
-//    calls (cache_tree.cpp:114-142) that leaves the table exactly as the same
-//    calls issued one by one: query i runs at clock0 + i + 1, every resident
-//    page a query's range covers is refreshed, so a page's final stamp is the
-//    clock of the LAST query covering it (residency never changes inside a
-//    match batch). One warp per query (dynamic work queue over all SMs) probes
-//    its shared-prompt chunks read-only and refreshes its private chunks in
-//    place (the host splits batches so an agent appears at most once, making a
-//    private chunk single-writer); shared-prompt pages get max{i : query i
-//    covers p} through one atomicMax per query and a suffix max, and are
-//    rewritten by one small CTA afterwards.
+//  * grid_match_prep_kernel / grid_match_kernel / grid_match_rest_kernel /
+//    grid_match_shared_kernel — a BATCH of match_prefix calls
+//    (cache_tree.cpp:114-142) that leaves the table exactly as the same calls
+//    issued one by one: query i runs at clock0 + i + 1, every resident page a
+//    query's range covers is refreshed, so a page's final stamp is the clock
+//    of the LAST query covering it (residency never changes inside a match
+//    batch). The shared prompt, common to every query, is probed once (prep);
+//    each query's first group of 8 private chunks is probed by one warp (all 8
+//    bucket loads in flight) and refreshed in place — the host splits batches
+//    so an agent appears at most once, making a private chunk single-writer;
+//    the remaining groups of queries whose first group was fully resident are
+//    flattened over (query, group) across all warps (rest); shared-prompt
+//    pages get max{i : query i covers p} through one atomicMax per query and a
+//    suffix max, and are rewritten by one small CTA (shared).
 //  * grid_evict_kernel — evict(needed) (cache_tree.cpp:270-319, per-page form
 //    SURVEY.md A.2) as ONE cooperative launch over every SM: the radix select
 //    of coop_evict with 11-bit digits, per-CTA shared-memory histograms
@@ -68,9 +71,8 @@ __global__ void __launch_bounds__(1024) grid_match_prep_kernel(GridMatchArgs A) 
 // clock (a private chunk has one writer per batch: the host splits batches so
 // an agent appears once) and folds first miss / resident count into the
 // query's accumulators. Returns true when the group had no miss.
-__device__ __forceinline__ bool match_group(const GridMatchArgs& A, Op& op, u32 i, u64 n, u64 g,
+__device__ __forceinline__ bool match_group(const GridMatchArgs& A, u32 i, u64 n, u64 g,
                                             int lane) {
-  (void)op;
   const u64 owner = (static_cast<u64>(A.agents[i]) + 1) << 32;
   const u64 c0 = (A.S >> 5) + g * kGridItemChunks;
   const u64 stamp = A.clock0 + i + 1;
@@ -123,21 +125,6 @@ __device__ __forceinline__ bool match_group(const GridMatchArgs& A, Op& op, u32 
   return miss == NIL32;
 }
 
-__device__ __forceinline__ void match_warp_init(const GridMatchArgs& A, Op& op, int lane) {
-  if (lane == 0) {
-    op.table = A.table;
-    op.summ = A.summ;
-    op.mask = A.mask;
-    op.shared_pages = A.S;
-    op.implicit_pins = 0;
-    op.agents = nullptr;
-    op.log = nullptr;
-    op.vic = nullptr;
-    op.log_victims = 0;
-  }
-  __syncwarp();
-}
-
 __device__ __forceinline__ u64 match_groups(const GridMatchArgs& A, u64 n) {
   if (n <= A.S) return 0;
   return (((n - 1) >> 5) - (A.S >> 5)) / kGridItemChunks + 1;
@@ -147,10 +134,7 @@ __device__ __forceinline__ u64 match_groups(const GridMatchArgs& A, u64 n) {
 // pass and probes the first private chunk group. Queries whose first group
 // is fully resident (and that have more) go on the continuation list.
 __global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMatchArgs A) {
-  __shared__ Op wops[kGridMatchWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  Op& op = wops[w];
-  match_warp_init(A, op, lane);
   const u32 gw = blockIdx.x * kGridMatchWarps + w, GW = gridDim.x * kGridMatchWarps;
   for (u32 i = gw; i < A.n; i += GW) {
     const u64 n = A.lens[i] / A.ps;
@@ -160,7 +144,7 @@ __global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMa
     }
     const u64 groups = match_groups(A, n);
     if (groups == 0) continue;
-    if (match_group(A, op, i, n, 0, lane) && groups > 1 && lane == 0)
+    if (match_group(A, i, n, 0, lane) && groups > 1 && lane == 0)
       A.cont[atomicAdd(A.n_cont, 1u)] = i;
   }
 }
@@ -168,10 +152,7 @@ __global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMa
 // Pass 2: the remaining groups of the continued queries, flattened over
 // (continued query, group) so a long resident context spreads over many warps.
 __global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_rest_kernel(GridMatchArgs A) {
-  __shared__ Op wops[kGridMatchWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  Op& op = wops[w];
-  match_warp_init(A, op, lane);
   const u64 gw = blockIdx.x * kGridMatchWarps + w, GW = gridDim.x * kGridMatchWarps;
   const u64 per = A.max_groups - 1;
   const u64 total = static_cast<u64>(*A.n_cont) * per;
@@ -180,7 +161,7 @@ __global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_rest_kernel(G
     const u64 g = 1 + k % per;
     const u64 n = A.lens[i] / A.ps;
     if (g >= match_groups(A, n)) continue;
-    match_group(A, op, i, n, g, lane);
+    match_group(A, i, n, g, lane);
   }
 }
 

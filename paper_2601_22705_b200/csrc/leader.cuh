@@ -5,17 +5,20 @@
 // work is needed it posts a cooperative op (engine.cu) and returns; the CTA
 // executes the op and thread 0 resumes at the continuation phase.
 //
-// Leader-only structures (no CTA involvement, L1-resident for small sims):
+// Leader-only structures (no CTA involvement, shared memory for small sims):
 //   * agent events: binary min-heap of (time, ordinal, agent) — equivalent to
 //     the reference's priority queue since an agent has at most one pending
-//     event; tick and admission are two scalar slots;
+//     event; a dispatch batch's completions are ONE entry (a
+//     completion group, kernel 4); tick and admission are two scalar slots;
 //   * ready set: two-level bitmap of (active && AwaitingAdmission) agents,
 //     iterated in id order exactly like dispatch_batch's sorted vector;
 //   * pins: each agent holds at most one pin, on its own root prefix
 //     [0, pinned_len) (engine.cpp:340-342, 374-377). The pin count of private
 //     page (a, k) is [k < pinned_pg(a)] and of shared page k is
 //     #{a : pinned_pg(a) > k}; only the prefix max matters for eviction, kept
-//     with a histogram. No page-table pass is ever spent on pin/unpin.
+//     with a histogram. No page-table pass is ever spent on pin/unpin;
+//   * chain form of the discard-mode cache: per-agent chains
+//     with one stamp each, evicted in stamp order (chain heap / scan).
 #pragma once
 
 namespace kvg {
