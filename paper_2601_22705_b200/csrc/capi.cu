@@ -19,6 +19,7 @@ __global__ void engine_kernel_small(const SimDev* __restrict__ sims);
 __global__ void engine_kernel_small_off(const SimDev* __restrict__ sims);
 __global__ void engine_kernel_big(const SimDev* __restrict__ sims);
 __global__ void engine_kernel_lone(const SimDev* __restrict__ sims);
+__global__ void engine_kernel_mid(const SimDev* __restrict__ sims);
 __global__ void cache_kernel(const CacheDev* __restrict__ cd);
 __global__ void pack_traces(const SimDev* __restrict__ sims, const u64* __restrict__ dst_off,
                             kvg_trace_row* __restrict__ packed);

@@ -2559,6 +2559,11 @@ __global__ void __launch_bounds__(1024, 1) engine_kernel_big(const SimDev* __res
   engine_body<KVG_BIG_DEPTH, true, KVG_BIG_SMEM_DESC, true>(sims);
 }
 
+// Up to 16 warps (table / offload mode lone simulations): 128 registers.
+__global__ void __launch_bounds__(512, 1) engine_kernel_mid(const SimDev* __restrict__ sims) {
+  engine_body<KVG_BIG_DEPTH, true, KVG_BIG_SMEM_DESC, true>(sims);
+}
+
 // Lone chain-mode simulations (1-2 warps, nothing to parallelise inside an
 // event but the warp steps): the same body with the register budget of a
 // 64-thread CTA, so the leader's state machine does not spill.
