@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(1024) cache_kernel(const CacheDev* __restrict_
   __shared__ CLead L;
   __shared__ Op op;
   const CacheDev& C = *cd;
-  Hist h{C.hist, C.hist + kBins};
+  __shared__ unsigned int shist[2 * kBins];  // radix-select bins in shared memory
+  Hist h{shist, shist + kBins, true};
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   CacheState* st = reinterpret_cast<CacheState*>(C.state);
   if (tid == 0) {

@@ -166,13 +166,23 @@ struct Op {
 
 constexpr int kBins = 512;
 
-// Radix-select histogram. Lives in per-simulation global scratch (L2): it is
-// touched only by eviction selects, and keeping it out of shared memory leaves
-// the SM's unified L1 to the leader's hot agent records.
+// Radix-select histogram: in shared memory wherever the CTA has room (the
+// one-CTA-per-SM kernels, the CacheTree seam, the grid select); in
+// per-simulation global scratch (L2) in the 28-CTA/SM sweep kernel, whose
+// shared memory holds the hot agent records. Global bins are read with
+// L1-bypassing loads (other warps update them with L2 atomics).
 struct Hist {
   unsigned int* cnt;   // [kBins]
   unsigned int* dmax;  // [kBins]
+  bool smem;
 };
+__device__ __forceinline__ u32 hist_ld(const Hist& h, const unsigned int* p) {
+  return h.smem ? *reinterpret_cast<const volatile unsigned int*>(p) : __ldcg(p);
+}
+__device__ __forceinline__ void hist_zero(const Hist& h, unsigned int* p) {
+  if (h.smem) *p = 0u;
+  else __stcg(p, 0u);
+}
 
 __device__ __forceinline__ Summ ld_summ(const Summ* p) {
   const ulonglong2* q = reinterpret_cast<const ulonglong2*>(p);
@@ -571,7 +581,7 @@ __device__ __noinline__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int la
   const u32 base = lane * per;
   u32 local = 0;
   for (u32 i = 0; i < per; ++i)
-    if (base + i < nbins) local += __ldcg(&h.cnt[base + i]);
+    if (base + i < nbins) local += hist_ld(h, &h.cnt[base + i]);
   u32 incl = local;
   for (int o = 1; o < 32; o <<= 1) {
     u32 v = __shfl_up_sync(FULL, incl, o);
@@ -590,7 +600,7 @@ __device__ __noinline__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int la
   if (lane == L) {
     u32 i = 0;
     for (; i + 1 < per; ++i) {
-      const u32 c = __ldcg(&h.cnt[base + i]);
+      const u32 c = hist_ld(h, &h.cnt[base + i]);
       if (cum + c >= need) break;
       cum += c;
     }
@@ -671,8 +681,8 @@ __device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int 
       const bool last = shift == 0;
       const u32 nbins = 1u << d;
       for (u32 i = tid; i < nbins; i += nt) {
-        __stcg(&h.cnt[i], 0u);
-        __stcg(&h.dmax[i], 0u);
+        hist_zero(h, &h.cnt[i]);
+        hist_zero(h, &h.dmax[i]);
       }
       __syncthreads();
       const u64 prefix = op.prefix;
@@ -703,7 +713,7 @@ __device__ __noinline__ void coop_evict(Op& op, Hist& h, int tid, int warp, int 
       if (warp == 0) {
         u64 rank = 0;
         const u32 bin = select_bin(op, h, nbins, d, lane, &rank);
-        if (last && lane == 0) op.cut_depth = static_cast<u64>(__ldcg(&h.dmax[bin])) + 1 - rank;
+        if (last && lane == 0) op.cut_depth = static_cast<u64>(hist_ld(h, &h.dmax[bin])) + 1 - rank;
       }
       __syncthreads();
       lo_bits = shift;

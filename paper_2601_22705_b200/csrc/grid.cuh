@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
   const bool all = op.all;
   u64 T = 0, cut = 0;
   if (!all) {
-    Hist hs{scnt, sdmax};
+    Hist hs{scnt, sdmax, true};
     int lo_bits = 64 - __clzll(A.clock | 1ull);
     int pass = 0;
     while (lo_bits > 0) {

@@ -2420,7 +2420,9 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     __syncthreads();
   }
   const SimDev& D = kSmemDesc ? Ds[0] : sims[blockIdx.x];
-  Hist h{D.hist, D.hist + kBins};
+  // radix-select bins: shared memory in the one-CTA-per-SM kernels
+  __shared__ unsigned int shist[kLru ? 2 * kBins : 1];
+  Hist h{kLru ? shist : D.hist, kLru ? shist + kBins : D.hist + kBins, kLru};
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const u32 n = D.n_agents;
   const u32 nwords = (n + 31) / 32;
