@@ -16,6 +16,7 @@
 
 namespace kvg {
 __global__ void engine_kernel_small(const SimDev* __restrict__ sims);
+__global__ void engine_kernel_small_chain(const SimDev* __restrict__ sims);
 __global__ void engine_kernel_small_off(const SimDev* __restrict__ sims);
 __global__ void engine_kernel_big(const SimDev* __restrict__ sims);
 __global__ void engine_kernel_lone(const SimDev* __restrict__ sims);

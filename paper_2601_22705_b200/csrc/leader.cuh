@@ -1601,12 +1601,12 @@ __device__ __forceinline__ void batch_end(const SimDev& D, Lead& L) {
 // true when it posted a cooperative op (the caller returns to the CTA);
 // otherwise L.phase says where to go on (PH_EVENT after an inline batch end in
 // chain mode; a member phase in table / verify mode).
-template <bool kOff>
+template <bool kOff, bool kChain>
 __device__ __forceinline__ bool member_loop(const SimDev& D, Lead& L, Op& op) {
   for (;;) {  // chain mode: whole member attempts inline, one after another
   const u32 id = L.m_next;
   if (id == NIL) {
-    if (L.chain) {  // the batch ends here, straight back to the event loop
+    if (kChain || L.chain) {  // the batch ends here, straight back to the event loop
       batch_end<kOff>(D, L);
       L.phase = PH_EVENT;
     } else {
@@ -1620,7 +1620,7 @@ __device__ __forceinline__ bool member_loop(const SimDev& D, Lead& L, Op& op) {
     fail(L, E_OFFLOAD);
     break;
   }
-  if (L.chain && L.stall_streak > 0 && L.storm_on) {  // a stall storm: the warp takes the run
+  if ((kChain || L.chain) && L.stall_streak > 0 && L.storm_on) {  // a stall storm: the warp takes the run
     op.kind = OP_STORM;
     op.err = E_NONE;
     return true;  // (coop_storm leaves L.phase at PH_MEMBER)
@@ -1643,7 +1643,7 @@ __device__ __forceinline__ bool member_loop(const SimDev& D, Lead& L, Op& op) {
   a.lazy = L.m_now;
   L.lazy_sh = L.m_now;
   ch_remove(L, id);  // its path is pinned from the match on
-  if (L.chain) {
+  if (kChain || L.chain) {
     chain_member(D, L);
     if (L.status == KVG_ERR_STATE) break;
     continue;  // the next member
@@ -1659,7 +1659,7 @@ __device__ __forceinline__ bool member_loop(const SimDev& D, Lead& L, Op& op) {
   return false;
 }
 
-template <bool kOff>
+template <bool kOff, bool kChain>
 __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
   op.kind = OP_NONE;
   for (;;) {
@@ -1748,8 +1748,8 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.b_wall = L.b_total = 0.0;
           L.m_next = ready_next(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
           L.phase = PH_MEMBER;
-          if (L.chain) {  // members and the batch end inline, then this loop
-            if (member_loop<kOff>(D, L, op)) return;
+          if (kChain || L.chain) {  // members and the batch end inline, then this loop
+            if (member_loop<kOff, kChain>(D, L, op)) return;
             if (L.phase == PH_EVENT) continue;
           }
           break;  // phase changed: through the dispatch
@@ -1856,10 +1856,11 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.phase = PH_O_MEMBER;
           continue;
         }
-        if (member_loop<kOff>(D, L, op)) return;
+        if (member_loop<kOff, kChain>(D, L, op)) return;
         continue;
       }
       case PH_M_MATCHED: {
+        if constexpr (kChain) __builtin_unreachable();
         const u64 f = L.m_f;
         if (L.verify && L.m_nctx > 0) {  // the probe must agree with the held state
           if (op.err) fail(L, op.err);
@@ -1883,6 +1884,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         continue;
       }
       case PH_M_INSERT: {  // CacheTree::insert loop (cache_tree.cpp:170-187)
+        if constexpr (kChain) __builtin_unreachable();
         if (L.m_nafter == 0) {  // nothing to cache: ok, no clock bump
           op.created = 0;
           L.phase = PH_M_CREATED;
@@ -1927,6 +1929,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         return;
       }
       case PH_M_EVICTED: {
+        if constexpr (kChain) __builtin_unreachable();
         const u64 r = op.freed;
         const u64 expect = L.m_k < L.m_e ? L.m_k : L.m_e;
         if (r != expect || op.err) fail(L, E_EVICT_MISMATCH);
@@ -1938,6 +1941,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         continue;
       }
       case PH_M_COMMIT: {
+        if constexpr (kChain) __builtin_unreachable();
         if (!L.chain && static_cast<u64>(op.occ_n) + range_chunks(L.m_f, L.m_nafter) >
                             (static_cast<u64>(op.mask) + 1) / 2) {
           if (L.rebuilt) {
@@ -1970,6 +1974,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         continue;
       }
       case PH_M_CREATED: {
+        if constexpr (kChain) __builtin_unreachable();
         if (op.err) fail(L, op.err);
         L.used += op.created;
         L.created_pages += op.created;
@@ -1992,6 +1997,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         continue;
       }
       case PH_M_FAIL: {  // insert failed: engine.cpp:366-373
+        if constexpr (kChain) __builtin_unreachable();
         AgentDev& a = L.ag[L.m_id];
         a.ctx = static_cast<u32>(L.m_ctx0);  // context.resize + token_counter rollback
         a.stalled = 1;
@@ -2000,6 +2006,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
         continue;
       }
       case PH_M_RESTORED: {
+        if constexpr (kChain) __builtin_unreachable();
         if (op.err) fail(L, op.err);
         set_pinned(D, L, L.m_id, 0);  // unpin(matched); pinned_len = 0
         if (L.ag[L.m_id].priv > 0) ch_insert(L, L.m_id);
@@ -2402,7 +2409,7 @@ __device__ __noinline__ void flush_rows(const SimDev& D, Lead& L, int t, int nt,
   if (t == 0) L.n_flushed = n;
 }
 
-template <int kDepth, bool kOff, bool kSmemDesc, bool kLru>
+template <int kDepth, bool kOff, bool kSmemDesc, bool kLru, bool kChain = false>
 __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   __shared__ Lead L;
   __shared__ Op op;
@@ -2496,7 +2503,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
 #endif
   const bool stream = D.trace_out != nullptr;  // streamed host delivery
   for (;;) {
-    if (tid == 0) leader_step<kOff>(D, L, op);
+    if (tid == 0) leader_step<kOff, kChain>(D, L, op);
     __syncthreads();
     if (op.kind == OP_EXIT) break;
     if (tid == 0) PROF_MARK(L, 32 + op.kind);
@@ -2516,7 +2523,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
       if (warp == 0) coop_storm(D, L, op, lane);
     } else if (op.kind == OP_FLUSH) {
       if (warp == 0) flush_rows(D, L, lane, 32, 0);
-    } else {
+    } else if constexpr (!kChain) {  // (the chain kernel posts no page op)
       run_op<kDepth>(op, h, tid, warp, lane, nw);
     }
     __syncthreads();
@@ -2551,6 +2558,13 @@ __global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small(const 
   engine_body<KVG_SMALL_DEPTH, false, true, false>(sims);
 }
 
+// The same for batches whose small simulations are all in chain form (discard
+// mode, verify off): the table-mode phases and page ops compile out, so the
+// hot state machine is smaller (the kernel is instruction-fetch bound).
+__global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small_chain(const SimDev* __restrict__ sims) {
+  engine_body<KVG_SMALL_DEPTH, false, true, false, true>(sims);
+}
+
 // The same with the offload tier compiled in (batches holding offload sims).
 __global__ void __launch_bounds__(32, KVG_SMALL_MINB) engine_kernel_small_off(const SimDev* __restrict__ sims) {
   engine_body<KVG_SMALL_DEPTH, true, true, false>(sims);
@@ -2566,11 +2580,12 @@ __global__ void __launch_bounds__(512, 1) engine_kernel_mid(const SimDev* __rest
   engine_body<KVG_BIG_DEPTH, true, KVG_BIG_SMEM_DESC, true>(sims);
 }
 
-// Lone chain-mode simulations (1-2 warps, nothing to parallelise inside an
-// event but the warp steps): the same body with the register budget of a
-// 64-thread CTA, so the leader's state machine does not spill.
+// Lone chain-form simulations (discard mode, verify off; 1-2 warps: nothing to
+// parallelise inside an event but the warp steps): the register budget of a
+// 64-thread CTA, so the leader's state machine does not spill, and only the
+// chain-form code (no table phases, page ops or offload tier).
 __global__ void __launch_bounds__(64, 1) engine_kernel_lone(const SimDev* __restrict__ sims) {
-  engine_body<KVG_BIG_DEPTH, true, KVG_BIG_SMEM_DESC, true>(sims);
+  engine_body<KVG_BIG_DEPTH, false, KVG_BIG_SMEM_DESC, true, true>(sims);
 }
 
 }  // namespace kvg
