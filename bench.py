@@ -257,6 +257,16 @@ def algorithmic_bytes(results, tree: bool = False, probed: bool = False,
                 total=look + ins + ev + state + tick)
 
 
+def model_bytes(results) -> int:
+    """The §8(d) per-page byte model of the REFERENCE algorithm's work for the
+    same simulations (what a page-table implementation moves: 16 B per counted
+    lookup + 8 B per hit page, 16 B per created page + 8 B per refreshed page,
+    16 B per evicted page, agent state and trace rows). Reported for context
+    next to the bytes the chain-form kernel actually moves."""
+    return int(sum(16 * r.lookups + 8 * r.hit_pages + 16 * r.created_pages + 8 * r.refreshed_pages
+                   + 16 * r.evicted_pages + 192 * r.agent_events + 88 * r.ticks for r in results))
+
+
 def load_peak():
     try:
         with open(PEAKS_PATH) as fh:
@@ -412,8 +422,12 @@ def run_b200(args):
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic, "traffic_capture": tsrc,
             "peak_source": peak_kind,
-            "kernel": "kvg::engine_kernel_small" if len(specs) >= 296 else "kvg::engine_kernel_big",
+            "kernel": ("kvg::engine_kernel_small_chain" if len(specs) >= 296 else
+                       "kvg::engine_kernel_mid" if args.workload == "c3off" else
+                       "kvg::engine_kernel_lone"),
             "algorithmic_bytes_per_launch": ab, "kernel_ms_per_launch": kern_ms / args.steps,
+            "reference_model_bytes_per_launch": model_bytes(results),
+            "reference_model_gbs": model_bytes(results) / kernel_s / 1e9,
             "limiter": "latency of each simulation's sequential event chain (ncu: issue-bound "
                        "at low eligible warps, DESIGN.md §5); the page kernels alone: "
                        "bench.py --workload kernels"}
