@@ -87,7 +87,7 @@ def maybe_respawn(args, argv) -> bool:
         if "WORLD_SIZE" in os.environ and world != args.gpus:
             sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
         return False
-    if args.impl == "b200":
+    if args.impl == "b200" and os.environ.get("KVG_DIST_BACKEND", "nccl") == "nccl":
         import torch
         have = torch.cuda.device_count()
         if have < args.gpus:
@@ -365,8 +365,11 @@ def run_b200(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # KVG_DIST_BACKEND=gloo (dev / CI check of the multi-rank path on one
+        # GPU: ranks share the device, timings are not scaling numbers)
+        backend = os.environ.get("KVG_DIST_BACKEND", "nccl")
+        torch.cuda.set_device(local % max(1, torch.cuda.device_count()))
+        dist.init_process_group(backend)
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the engine has no CPU path)")
     device = torch.cuda.current_device()
@@ -517,8 +520,9 @@ def run_b200(args):
                                       f"({args.split} split), NCCL all_gather of records",
                        "l2": "flushed between timed steps (256 MiB device memset outside "
                              "the CUDA-event window)",
-                       "cache_state": "chain mode: per-agent chains + LRU, no page table "
-                                      "(DESIGN.md §4.1); probe_mode runs the page table",
+                       "cache_state": "chain form: per-agent chains, stamp-ordered eviction, no "
+                                      "page table (DESIGN.md §4.1); probe_mode runs the page "
+                                      "table",
                        "verify": 0},
             "lookups_per_s": all_lookups * args.steps / (max_ms / 1e3),
             "lookups_note": "EQUIVALENT lookups: counted per SURVEY §8(d) (resolved pages + "

@@ -155,3 +155,29 @@ def test_gloo_world2_device_engine_shards_match_one_batch():
     serial = sweep.records(b.results_raw())
     b.close()
     assert got[0] == serial and got[1] == serial
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_bench_multi_rank_path_on_one_gpu():
+    """`bench.py --gpus 2` end to end through the device engine — re-exec
+    under torchrun, per-rank shards, barriers, max-over-ranks timing, the
+    record all_gather — with the gloo backend so both ranks can share the one
+    GPU this suite runs on (KVG_DIST_BACKEND; NCCL needs a GPU per rank)."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    env["KVG_DIST_BACKEND"] = "gloo"
+    for split in ("weak", "strong"):
+        r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2",
+                            "--split", split, "--sims", "256", "--steps", "1", "--warmup", "3",
+                            "--no-probe-mode", "--no-cpu-baseline", "--e2e-steps", "1"],
+                           capture_output=True, text=True, env=env, timeout=540)
+        assert r.returncode == 0, r.stderr[-2000:]
+        lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+        assert len(lines) == 1 and lines[0]["n_gpus"] == 2
+        d = lines[0]
+        assert d["scaling"] == split and d["value"] > 0 and d["parity"]["bad_status"] == 0
+        assert d["parity"]["sims"] == (512 if split == "weak" else 256)
