@@ -163,3 +163,18 @@ def test_horizon_abort_matches_reference():
             shutil.rmtree(root)
     assert outs[0][0] == 3 and "exceeded horizon" in outs[0][1]
     assert outs[1] == outs[0]
+
+
+ADAPTER_CHECK = os.path.join(REF_OUT, "adapter_check")
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(ADAPTER_CHECK), reason="oracle/_ref/adapter_check not built")
+def test_run_simulations_batch_equals_reference_run_simulation():
+    """kvgpu::run_simulations (one device batch of 16 jobs: every preset under
+    uncontrolled / aimd / agent_cap / request_cap / offload, plus a job the
+    reference rejects) against the reference run_simulation in-process:
+    SimulationResult field by field, bit for bit, and the same per-job error."""
+    r = subprocess.run([ADAPTER_CHECK, CONFIGS], cwd=REPO, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ALL OK"), r.stdout + r.stderr
