@@ -400,6 +400,7 @@ def run_b200(args):
         dist.barrier()
     sampler.stop()
     results = batch.results_raw()
+    geom = batch.geometry()  # one-warp kernel: CTAs per SM, waves
     units = sum(r.agent_steps for r in results)          # per step, this rank
     lookups = sum(r.lookups for r in results)
     bad = [i for i, r in enumerate(results) if r.status not in (0, abi.KVG_ERR_HORIZON)]
@@ -523,7 +524,7 @@ def run_b200(args):
                        "cache_state": "chain form: per-agent chains, stamp-ordered eviction, no "
                                       "page table (DESIGN.md §4.1); probe_mode runs the page "
                                       "table",
-                       "verify": 0},
+                       "verify": 0, "launch_geometry": geom},
             "lookups_per_s": all_lookups * args.steps / (max_ms / 1e3),
             "lookups_note": "EQUIVALENT lookups: counted per SURVEY §8(d) (resolved pages + "
                             "terminating miss) but answered from the held prefix state; the "

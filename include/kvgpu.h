@@ -275,6 +275,11 @@ KVG_API kvg_status kvg_batch_run(kvg_batch* b);
 /* Device time of the last kvg_batch_run, milliseconds (CUDA events on the
  * launching stream): whole step (workspace init + kernels) and kernels only. */
 KVG_API kvg_status kvg_batch_last_ms(const kvg_batch* b, double* ms);
+/* Launch geometry of the one-warp (small-simulation) kernel: how many
+ * simulations it runs, how many of its CTAs fit on one SM with this batch's
+ * shared memory, and the SM count (one wave iff small_sims <= ctas * sms). */
+KVG_API kvg_status kvg_batch_geometry(const kvg_batch* b, uint32_t* small_sims,
+                                      uint32_t* small_ctas_per_sm, uint32_t* sms);
 KVG_API kvg_status kvg_batch_timing(const kvg_batch* b, double* step_ms,
                                     double* kernel_ms);
 /* Copies results device->host (done once per run, lazily). */

@@ -78,11 +78,12 @@ struct Lead {
   u64 used, cclock, discarded, lookups, agent_steps, events, evict_calls, evicted;
   u64 pin_max, pin_priv;  // implicit pins: shared prefix max, private pinned pages
   u64 L0, lazy_sh;        // discard mode: resident shared pages, their stamp
-  kvg_phase_label ph[3];  // classify_phases result (coop_phases)
-  u32 n_ph, pad5;
   int verify, pad4;
   u64 hit_pages, created_pages, refreshed_pages, evict_scanned, agent_events;
   long long t_start;
+#ifdef KVG_GTIMER
+  u64 g_start;
+#endif
   double hit_m, hit_r;
   // controller (controller.hpp:117-126)
   double window, su, sh;
@@ -771,8 +772,8 @@ __device__ __noinline__ void admission_pass(const SimDev& D, Lead& L) {
 __device__ __noinline__ void finalize(const SimDev& D, Lead& L) {
   kvg_sim_result* r = D.result;
   r->status = L.status;
-  r->n_phases = L.n_ph;  // classify_phases (metrics.cpp:41-81), coop_phases
-  for (u32 k = 0; k < 3; ++k) r->phases[k] = L.ph[k];
+  // r->n_phases / r->phases: written by coop_phases (classify_phases,
+  // metrics.cpp:41-81), which every run passes through (PH_DONE) before this
   r->ledger = L.ledger;
   r->makespan = L.makespan < L.pcie_busy ? L.pcie_busy : L.makespan;  // engine.cpp:400
   r->device_busy = L.device_busy;
@@ -812,6 +813,18 @@ __device__ __noinline__ void finalize(const SimDev& D, Lead& L) {
   r->agent_events = L.agent_events;
   r->device_cycles = static_cast<u64>(clock64() - L.t_start);
   r->abort_time = L.status == KVG_ERR_HORIZON ? L.abort_t : 0.0;
+#ifdef KVG_GTIMER  // dev probe only: start / end in globaltimer ns, SM id
+  {
+    u64 g_end;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    r->evict_scanned = r->device_cycles;
+    r->device_cycles = g_end;
+    r->abort_time = static_cast<double>(L.g_start);
+    r->evicted_pages = smid;
+  }
+#endif
   r->unfinished = L.n - L.finished;
   D.counts[0] = L.n_trace;
   D.counts[1] = L.n_log;
@@ -823,6 +836,9 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.err = E_NONE;
   L.rebuilt = 0;
   L.t_start = clock64();
+#ifdef KVG_GTIMER  // dev probe: wall-clock placement of each simulation in the launch
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(L.g_start));
+#endif
   L.clock = L.gpu_busy = L.makespan = L.device_busy = 0.0;
   L.ord = 0;
   L.hsize = 0;
@@ -1237,9 +1253,10 @@ __device__ __noinline__ void coop_phases(const SimDev& D, Lead& L, int lane) {
       }
     }
   }
-  if (lane == 0) {
-    L.n_ph = np;
-    for (u32 k = 0; k < 3; ++k) L.ph[k] = k < np ? ph[k] : kvg_phase_label{0, 0, 0.0, 0.0};
+  if (lane == 0) {  // straight into the result (not held in Lead: shared memory per CTA)
+    kvg_sim_result* r = D.result;
+    r->n_phases = np;
+    for (u32 k = 0; k < 3; ++k) r->phases[k] = k < np ? ph[k] : kvg_phase_label{0, 0, 0.0, 0.0};
   }
 }
 
@@ -2541,6 +2558,12 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
 // Throughput variant: one warp per simulation, register budget (72) sized so 28
 // simulations stay resident per SM: 148 x 28 = 4144 >= the 4096 C4 sweep sims,
 // all in flight in one wave (measured: 24/SM leaves a 544-sim second wave).
+// Shared memory is the other limit: per CTA, static (Lead + Op + descriptor
+// copy) + dynamic (64 agents: 5,392 B) rounded up to 128 B, + 1 KB reserved:
+// 28 x 8,320 B fits the SM's 228 KB with 512 B to spare, so Lead must not
+// grow by a 128 B granule (measured: at 27 CTAs/SM the last 100 C4 sims ran
+// as a second wave, 18.5 ms instead of 13.7 ms; tests/test_gpu_batch.py
+// test_c4_sweep_runs_in_one_wave guards it via kvg_batch_geometry).
 
 #ifndef KVG_SMALL_DEPTH
 #define KVG_SMALL_DEPTH 2

@@ -58,6 +58,7 @@ def lib():
     L.kvg_batch_run.argtypes = [C.c_void_p]
     L.kvg_batch_last_ms.argtypes = [C.c_void_p, P(C.c_double)]
     L.kvg_batch_timing.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double)]
+    L.kvg_batch_geometry.argtypes = [C.c_void_p, P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
     L.kvg_batch_result.argtypes = [C.c_void_p, C.c_size_t, P(abi.SimResult)]
     L.kvg_batch_trace.argtypes = [C.c_void_p, C.c_size_t, P(abi.TraceRow), C.c_size_t,
                                   P(C.c_size_t)]
@@ -229,6 +230,15 @@ class Batch:
         a, k = C.c_double(), C.c_double()
         _check(lib().kvg_batch_timing(self.h, C.byref(a), C.byref(k)))
         return a.value, k.value
+
+    def geometry(self) -> dict:
+        """One-warp kernel geometry: small simulations, CTAs per SM at this
+        batch's shared memory (CUDA occupancy calculator), SM count, waves."""
+        n, occ, sms = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        _check(lib().kvg_batch_geometry(self.h, C.byref(n), C.byref(occ), C.byref(sms)))
+        slots = occ.value * sms.value
+        waves = -(-n.value // slots) if slots else 0
+        return {"small_sims": n.value, "ctas_per_sm": occ.value, "sms": sms.value, "waves": waves}
 
     def result(self, i: int) -> dict:
         r = abi.SimResult()

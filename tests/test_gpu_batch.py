@@ -135,3 +135,17 @@ def test_run_simulation_mirror():
     out = engine.run_simulation(engine.Population(s.workload, s.seed), *s.resolved()[:1],
                                 s.cost.to_abi(), s.resolved()[1].to_abi())
     assert out["result"]["makespan"] == oracle_run(s)["result"]["makespan"]
+
+
+@pytest.mark.parametrize("verify", [False, True])
+def test_c4_sweep_runs_in_one_wave(verify):
+    # all 4,096 C4 simulations resident at once (148 SMs x 28 one-warp CTAs):
+    # a second wave of even a few simulations doubles the kernel time
+    pop = engine.Population(config.c1_toy().workload, 42)
+    specs = [engine.SimSpec.from_scenario(s, population=pop) for s in config.c4_sweep(4096)]
+    b = engine.Batch(specs, verify=verify)
+    g = b.geometry()
+    b.close()
+    assert g["small_sims"] == 4096
+    assert g["ctas_per_sm"] >= 28, g
+    assert g["waves"] == 1, g
