@@ -272,6 +272,16 @@ KVG_API kvg_status kvg_batch_create(int device, const kvg_sim_desc* sims,
  * simulation hit its horizon (per-sim status in kvg_batch_result), with the
  * partial results still readable, as run_simulation's partial_on_abort. */
 KVG_API kvg_status kvg_batch_run(kvg_batch* b);
+/* kvg_batch_run in two halves, so a caller can pipeline batches (create /
+ * read back one batch while another runs; the reference's run_rows keeps its
+ * thread pool busy the same way, experiment.cpp:75-108): kvg_batch_launch
+ * enqueues the run on the batch's own stream and returns at once;
+ * kvg_batch_wait blocks until it ends and then does everything kvg_batch_run
+ * does after the kernels (trace regrow + re-run, host delivery, status). In
+ * between, the batch's results / traces / stats are not readable
+ * (KVG_ERR_CONFIG); kvg_batch_free waits for the launch. */
+KVG_API kvg_status kvg_batch_launch(kvg_batch* b);
+KVG_API kvg_status kvg_batch_wait(kvg_batch* b);
 /* Device time of the last kvg_batch_run, milliseconds (CUDA events on the
  * launching stream): whole step (workspace init + kernels) and kernels only. */
 KVG_API kvg_status kvg_batch_last_ms(const kvg_batch* b, double* ms);

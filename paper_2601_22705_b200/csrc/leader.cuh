@@ -38,6 +38,12 @@ constexpr uint8_t EV_GROUP_POP = 0xff;  // popped heap key of a completion group
 #ifndef KVG_LEADER_FN
 #define KVG_LEADER_FN __forceinline__
 #endif
+#ifndef KVG_PIN_FN  // set_pinned (8 call sites)
+#define KVG_PIN_FN KVG_LEADER_FN
+#endif
+#ifndef KVG_READY_FN  // ready_sync / ready_next
+#define KVG_READY_FN KVG_LEADER_FN
+#endif
 
 enum Phase : int {
   PH_EVENT = 0,
@@ -233,7 +239,7 @@ __device__ __forceinline__ void fail(Lead& L, int code) {
 }
 
 // ready bitmap: bit a <=> agent a is active and AwaitingAdmission
-__device__ KVG_LEADER_FN void ready_sync(const SimDev& D, Lead& L, AgentDev& a, u32 id) {
+__device__ KVG_READY_FN void ready_sync(const SimDev& D, Lead& L, AgentDev& a, u32 id) {
   const uint8_t want = a.in_active && a.state == S_AWAIT;
   if (want == a.ready) return;
   a.ready = want;
@@ -252,7 +258,7 @@ __device__ KVG_LEADER_FN void ready_sync(const SimDev& D, Lead& L, AgentDev& a, 
 }
 
 // smallest ready agent id >= from, or NIL
-__device__ KVG_LEADER_FN u32 ready_next(const SimDev& D, const Lead& L, u32 from) {
+__device__ KVG_READY_FN u32 ready_next(const SimDev& D, const Lead& L, u32 from) {
   if (from >= L.n) return NIL;
   const u32 w = from >> 5;
   const u32 bits = L.rbits[w] & (~0u << (from & 31));
@@ -346,7 +352,7 @@ __device__ __forceinline__ u32 paus_pop(const SimDev& D, Lead& L) {
 }
 
 // Implicit pins: agent `id` now pins its path prefix [0, tokens).
-__device__ KVG_LEADER_FN void set_pinned(const SimDev& D, Lead& L, u32 id, u64 tokens) {
+__device__ KVG_PIN_FN void set_pinned(const SimDev& D, Lead& L, u32 id, u64 tokens) {
   AgentDev& a = L.ag[id];
   const u64 old_pg = a.pinned_pg, new_pg = pdiv(L, tokens);
   a.pinned_pg = static_cast<u32>(new_pg);
@@ -1699,7 +1705,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           op.kind = OP_TICKS;
           return;
         }
-        PROF_MARK(L, 43);
+        PROF_MARK(L, 24);
         fast_housekeeping(D, L);
         PROF_MARK(L, PH_EVENT);
         int which = -1;  // 0 agent, 1 tick, 2 admission (the event ranks)
@@ -1753,7 +1759,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           continue;
         }
         if (which == 2) {  // on_admission_check (engine.cpp:268-291)
-          PROF_MARK(L, 44);
+          PROF_MARK(L, 27);
           admission_pass(D, L);
           PROF_MARK(L, PH_EVENT);
           if (L.n_ready == 0) {  // dispatch_batch with an empty ready set
@@ -1766,7 +1772,10 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.m_next = ready_next(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
           L.phase = PH_MEMBER;
           if (kChain || L.chain) {  // members and the batch end inline, then this loop
-            if (member_loop<kOff, kChain>(D, L, op)) return;
+            PROF_MARK(L, 25);
+            const bool posted = member_loop<kOff, kChain>(D, L, op);
+            PROF_MARK(L, PH_EVENT);
+            if (posted) return;
             if (L.phase == PH_EVENT) continue;
           }
           break;  // phase changed: through the dispatch
@@ -1782,6 +1791,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           return;
         }
         L.ev_agent = agent;
+        PROF_MARK(L, 26);
         ++L.agent_events;
         AgentDev& a = L.ag[agent];
         if (kind == EV_GEN) {  // on_generation_complete (engine.cpp:184-222)

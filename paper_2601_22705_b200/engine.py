@@ -56,6 +56,8 @@ def lib():
     L.kvg_batch_create.argtypes = [C.c_int, P(abi.SimDesc), C.c_size_t, P(abi.BatchOptions),
                                    P(C.c_void_p)]
     L.kvg_batch_run.argtypes = [C.c_void_p]
+    L.kvg_batch_launch.argtypes = [C.c_void_p]
+    L.kvg_batch_wait.argtypes = [C.c_void_p]
     L.kvg_batch_last_ms.argtypes = [C.c_void_p, P(C.c_double)]
     L.kvg_batch_timing.argtypes = [C.c_void_p, P(C.c_double), P(C.c_double)]
     L.kvg_batch_geometry.argtypes = [C.c_void_p, P(C.c_uint32), P(C.c_uint32), P(C.c_uint32)]
@@ -219,6 +221,14 @@ class Batch:
 
     def run(self, allow_horizon: bool = True) -> int:
         return _check(lib().kvg_batch_run(self.h), allow_horizon=allow_horizon)
+
+    def launch(self) -> None:
+        """First half of run(): enqueue on the batch's stream, return at once."""
+        _check(lib().kvg_batch_launch(self.h))
+
+    def wait(self, allow_horizon: bool = True) -> int:
+        """Second half of run(): block until the launch ends, deliver results."""
+        return _check(lib().kvg_batch_wait(self.h), allow_horizon=allow_horizon)
 
     def last_ms(self) -> float:
         v = C.c_double()

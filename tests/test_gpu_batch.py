@@ -149,3 +149,50 @@ def test_c4_sweep_runs_in_one_wave(verify):
     assert g["small_sims"] == 4096
     assert g["ctas_per_sm"] >= 28, g
     assert g["waves"] == 1, g
+
+
+def test_launch_wait_pipeline_matches_run():
+    # kvg_batch_launch / kvg_batch_wait with two batches in flight (the bench's
+    # pipelined e2e leg) give the same records as a blocking kvg_batch_run
+    pop = engine.Population(config.c1_toy().workload, 42)
+    specs = [engine.SimSpec.from_scenario(s, population=pop) for s in config.c4_sweep(512)]
+    ref = engine.Batch(specs, verify=False, host_outputs=True)
+    ref.run()
+    want = ref.results_array()
+    want_tr = [ref.trace(i) for i in (0, 255, 511)]
+    ref.close()
+    prev = None
+    got = []
+    for _ in range(3):
+        b = engine.Batch(specs, verify=False, host_outputs=True)
+        b.launch()
+        with pytest.raises(Exception):
+            b.result(0)  # not readable while in flight
+        with pytest.raises(Exception):
+            b.launch()   # one launch at a time
+        if prev is not None:
+            prev.wait()
+            got.append((prev.results_array(), [prev.trace(i) for i in (0, 255, 511)]))
+            prev.close()
+        prev = b
+    prev.wait()
+    got.append((prev.results_array(), [prev.trace(i) for i in (0, 255, 511)]))
+    prev.close()
+    skip = {"device_cycles"}
+    for arr, tr in got:
+        for name in want.dtype.names:
+            if name not in skip:
+                assert (arr[name] == want[name]).all(), name
+        assert tr == want_tr
+
+
+def test_free_while_in_flight_waits():
+    pop = engine.Population(config.c1_toy().workload, 42)
+    specs = [engine.SimSpec.from_scenario(s, population=pop) for s in config.c4_sweep(64)]
+    b = engine.Batch(specs, verify=False)
+    b.launch()
+    b.close()  # kvg_batch_free synchronises the stream before releasing memory
+    c = engine.Batch(specs, verify=False)
+    c.run()
+    assert all(r.status == 0 for r in c.results_raw())
+    c.close()
