@@ -521,15 +521,19 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
     size_t j = i;
     while (j < n && seen.emplace(agents[j], 0).second) ++j;
     const size_t m = j - i;
-    u64 max_groups = 0;
+    u64 max_groups = 0, n_items = 0;
     for (size_t k = 0; k < m; ++k) {
       const u64 np = lens[i + k] / ps;
-      if (np > S)
-        max_groups = std::max<u64>(
-            max_groups, (((np - 1) >> 5) - (S >> 5)) / kvg::kGridItemChunks + 1);
+      if (np > S) {
+        const u64 g = (((np - 1) >> 5) - (S >> 5)) / kvg::kGridItemChunks + 1;
+        max_groups = std::max<u64>(max_groups, g);
+        n_items += g - 1;
+      }
     }
+    if (n_items >= (1ull << 32))
+      return (kvg_status)set_error(KVG_ERR_CONFIG, "match_batch: too many chunk groups");
     const size_t words = S / 32 + 1;
-    const size_t need = m * (8 + 4 + 4 + 4 + 4) + words * 4 + 256;
+    const size_t need = 16 * (n_items + 1) + m * (8 + 4 + 4 + 4) + words * 4 + 256;
     if (need > c->gq_cap) {
       cudaFree(c->gq);
       c->gq = nullptr;
@@ -538,12 +542,12 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
       c->gq_cap = need;
     }
     char* p = c->gq;
-    u64* d_lens = reinterpret_cast<u64*>(p);
+    ulonglong2* d_items = reinterpret_cast<ulonglong2*>(p);  // 16 B aligned (cudaMalloc)
+    u64* d_lens = reinterpret_cast<u64*>(d_items + n_items + 1);
     u32* d_agents = reinterpret_cast<u32*>(d_lens + m);
     u32* d_fm = d_agents + m;
     u32* d_res = d_fm + m;
-    u32* d_cont = d_res + m;
-    u32* d_smask = d_cont + m;
+    u32* d_smask = d_res + m;
     unsigned int* d_ncont = d_smask + words;
     kvg::CacheState st{};
     kvg_status rc = cache_state(c, &st);
@@ -567,8 +571,8 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
     a.agents = d_agents;
     a.lens = d_lens;
     a.max_groups = static_cast<u32>(max_groups);
-    a.cont = d_cont;
-    a.n_cont = d_ncont;
+    a.items = d_items;
+    a.n_items = d_ncont;
     a.fm = d_fm;
     a.res = d_res;
     a.smask = d_smask;

@@ -29,6 +29,9 @@
 namespace kvg {
 
 constexpr int kGridMatchWarps = 8;
+#ifndef KVG_GM_MINB  // resident grid-match CTAs per SM the register budget allows
+#define KVG_GM_MINB 4  // measured 3 (71 registers) / 4 / 5 / 6: C5 lookup 0.425 / 0.323 / 0.328 / 0.353 ms
+#endif
 
 #ifdef KVG_GRID_PROF  // dev-only phase timestamps of CTA 0 (tools/probe_grid.py)
 __device__ unsigned long long g_gprof[32];
@@ -79,6 +82,7 @@ __device__ __forceinline__ bool match_group(const GridMatchArgs& A, u32 i, u64 n
   // every probe of the group in flight: one coalesced 512 B bucket load each
   u32 b[kGridItemChunks];
   Slot sl[kGridItemChunks];
+  u32 pend = 0, fnd = 0;  // (warp-uniform) chunks still probing / found
 #pragma unroll
   for (int j = 0; j < kGridItemChunks; ++j) {
     const u64 c = c0 + j;
@@ -87,24 +91,39 @@ __device__ __forceinline__ bool match_group(const GridMatchArgs& A, u32 i, u64 n
     if (c * 32 < n) {
       b[j] = static_cast<u32>(hash64(owner | (c * 32))) & A.mask;
       sl[j] = ld_slot(&A.table[(size_t)b[j] * kChunk + lane]);
+      pend |= 1u << j;
     }
+  }
+  // linear-probe continuations of every colliding chunk in flight together:
+  // one memory round trip per probe step of the group, not per collision
+  for (;;) {
+    u32 more = 0;
+#pragma unroll
+    for (int j = 0; j < kGridItemChunks; ++j) {
+      if (!((pend >> j) & 1u)) continue;
+      const u64 tag = owner | ((c0 + j) * 32);
+      const u64 k0 = __shfl_sync(FULL, sl[j].key, 0);
+      if (k0 == tag) {
+        fnd |= 1u << j;
+      } else if (k0 != kEmptyKey) {
+        b[j] = (b[j] + 1) & A.mask;
+        more |= 1u << j;
+      }
+    }
+    if (!more) break;
+#pragma unroll
+    for (int j = 0; j < kGridItemChunks; ++j)
+      if ((more >> j) & 1u) sl[j] = ld_slot(&A.table[(size_t)b[j] * kChunk + lane]);
+    pend = more;
   }
   u32 miss = NIL32, res = 0;
 #pragma unroll
   for (int j = 0; j < kGridItemChunks; ++j) {
     const u64 c = c0 + j;
     if (c * 32 >= n) break;  // warp-uniform
-    const u64 tag = owner | (c * 32);
-    Slot cur = sl[j];
-    u32 cb = b[j];
-    const u64 k0 = __shfl_sync(FULL, cur.key, 0);
-    bool found = k0 == tag;
-    if (!found && k0 != kEmptyKey) {  // collision: continue the linear probe
-      Op po;
-      po.table = A.table;
-      po.mask = A.mask;
-      found = probe_from(po, tag, (cb + 1) & A.mask, lane, &cb, &cur);
-    }
+    const Slot cur = sl[j];
+    const u32 cb = b[j];
+    const bool found = (fnd >> j) & 1u;
     const u64 page = c * 32 + lane;
     const bool in = page >= A.S && page < n;
     const bool r = found && in && (cur.meta & kResident);
@@ -133,7 +152,7 @@ __device__ __forceinline__ u64 match_groups(const GridMatchArgs& A, u64 n) {
 // Pass 1, one warp per query: files the shared range for the shared-stamp
 // pass and probes the first private chunk group. Queries whose first group
 // is fully resident (and that have more) go on the continuation list.
-__global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMatchArgs A) {
+__global__ void __launch_bounds__(kGridMatchWarps * 32, KVG_GM_MINB) grid_match_kernel(GridMatchArgs A) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const u32 gw = blockIdx.x * kGridMatchWarps + w, GW = gridDim.x * kGridMatchWarps;
   for (u32 i = gw; i < A.n; i += GW) {
@@ -144,24 +163,29 @@ __global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_kernel(GridMa
     }
     const u64 groups = match_groups(A, n);
     if (groups == 0) continue;
-    if (match_group(A, i, n, 0, lane) && groups > 1 && lane == 0)
-      A.cont[atomicAdd(A.n_cont, 1u)] = i;
+    if (match_group(A, i, n, 0, lane) && groups > 1) {  // (warp-uniform)
+      // file groups [1, groups) as work items: one contiguous range per query
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(A.n_items, static_cast<unsigned>(groups - 1));
+      base = __shfl_sync(FULL, base, 0);
+      for (u64 t = lane; t + 1 < groups; t += 32)
+        A.items[base + t] = make_ulonglong2((static_cast<u64>(i) << 32) | (t + 1), n);
+    }
   }
 }
 
-// Pass 2: the remaining groups of the continued queries, flattened over
-// (continued query, group) so a long resident context spreads over many warps.
-__global__ void __launch_bounds__(kGridMatchWarps * 32) grid_match_rest_kernel(GridMatchArgs A) {
+// Pass 2: the remaining groups of the continued queries as a dense list of
+// (query, group, pages) items filed by pass 1, so a long resident context
+// spreads over many warps and no warp walks empty (query, group) slots
+// (measured: the flattened query x max_groups enumeration spent a dependent
+// load pair on every empty slot).
+__global__ void __launch_bounds__(kGridMatchWarps * 32, KVG_GM_MINB) grid_match_rest_kernel(GridMatchArgs A) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const u64 gw = blockIdx.x * kGridMatchWarps + w, GW = gridDim.x * kGridMatchWarps;
-  const u64 per = A.max_groups - 1;
-  const u64 total = static_cast<u64>(*A.n_cont) * per;
+  const u64 total = *A.n_items;
   for (u64 k = gw; k < total; k += GW) {
-    const u32 i = A.cont[k / per];
-    const u64 g = 1 + k % per;
-    const u64 n = A.lens[i] / A.ps;
-    if (g >= match_groups(A, n)) continue;
-    match_group(A, i, n, g, lane);
+    const ulonglong2 it = A.items[k];  // {query << 32 | group, pages}
+    match_group(A, static_cast<u32>(it.x >> 32), it.y, it.x & 0xffffffffu, lane);
   }
 }
 

@@ -241,8 +241,9 @@ struct GridMatchArgs {
   const u64* lens;   // [n] sequence lengths, tokens
   u32 max_groups;    // most private chunk groups of any query
   u32 pad;
-  u32* cont;         // [n] queries whose first group was fully resident
-  unsigned int* n_cont;
+  ulonglong2* items; // continuation work items {query << 32 | group, pages}: the groups
+                     // past the first of queries whose first group was fully resident
+  unsigned int* n_items;
   u32* fm;           // [n] first missing private page (NIL32 = none), atomicMin
   u32* res;          // [n] resident private pages, atomicAdd
   u32* smask;        // [S/32 + 1] resident pages of each shared chunk
