@@ -1038,6 +1038,19 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
         adm_on = 1;
         adm_t = clock;
         adm_o = ord++;
+        ++events;
+        // the admission check just scheduled is the very next event (agent
+        // events are later than this tick and, unless clock + interval
+        // rounds to clock, so is the next tick): a no-op check is taken here
+        // without another loop turn
+        const u64 limit = kind == KVG_POLICY_UNCONTROLLED ? ~0ull
+                          : kind == KVG_POLICY_AIMD ? static_cast<u64>(floor(window))
+                                                    : static_cast<u64>(L.cap);
+        if (tick_t > clock && nready0 && !(act < limit && admit_src)) {
+          adm_on = 0;
+          ++events;
+        }
+        continue;
       }
       ++events;
     } else {
