@@ -954,11 +954,14 @@ unsigned match_blocks(int dev) {
 }
 
 // no more CTAs than 32-bucket lane groups to scan (a grid barrier costs the
-// same either way)
+// same either way): one CTA per KVG_EVICT_UNIT claimed buckets
+#ifndef KVG_EVICT_UNIT
+#define KVG_EVICT_UNIT 512  // measured 4,096 / 2,048 / 1,024 / 512 / 256: C2-size evict 38 / 33 / 29 / 27 / 28 us
+#endif
 unsigned evict_blocks(int dev, unsigned occ_n) {
   const Geom g = geom_of(dev);
   unsigned blocks = static_cast<unsigned>(g.sms * g.evict_per_sm);
-  const unsigned need = (occ_n + 16 * 32 * kvg::kGridSumDepth - 1) / (16 * 32 * kvg::kGridSumDepth);
+  const unsigned need = (occ_n + KVG_EVICT_UNIT - 1) / KVG_EVICT_UNIT;
   if (blocks > need) blocks = need > 0 ? need : 1;
   return blocks;
 }

@@ -277,48 +277,71 @@ __device__ __forceinline__ void grid_scan_summ(const Op& op, u32 gw, int lane, u
   }
 }
 
-// select_bin over a histogram in SHARED memory (the merged grid histogram is
-// staged there first: one coalesced 8 KB load instead of ~64 dependent L2
-// reads per lane).
-__device__ __forceinline__ u32 select_bin_s(Op& op, const u32* cnt, u32 nbins, int d, int lane,
-                                            u64* rank_in_bin) {
-  const u32 per = (nbins + 31) / 32;
-  const u32 base = lane * per;
-  u32 local = 0;
-  for (u32 i = 0; i < per; ++i)
-    if (base + i < nbins) local += cnt[base + i];
-  u32 incl = local;
-  for (int o = 1; o < 32; o <<= 1) {
-    const u32 v = __shfl_up_sync(FULL, incl, o);
-    if (lane >= o) incl += v;
+// select_bin over the staged histogram by the whole CTA (every thread calls
+// it): each warp sums one contiguous segment (conflict-free: lane-strided
+// reads), warp 0 scans the segment sums, then the 32-bin rounds of the one
+// segment that crosses `need`: the smallest bin whose inclusive count
+// reaches `need`, and the rank inside it. (The one-warp form it replaces
+// read 64 consecutive bins per lane: a 32-way bank conflict on every read,
+// 4-6 us per pass on the C5-size select.)
+__device__ __forceinline__ u32 select_bin_cta(Op& op, const u32* cnt, u32 nbins, int d, int lane,
+                                              int warp, int nw, u32* wsum, u64* sel,
+                                              u64* rank_in_bin) {
+  const u32 seg = (nbins + nw - 1) / nw;
+  u32 s = 0;
+  for (u32 i = lane; i < seg; i += 32) {
+    const u32 b = warp * seg + i;
+    if (b < nbins) s += cnt[b];
   }
-  const u64 need = op.need;
-  const unsigned ballot = __ballot_sync(FULL, static_cast<u64>(incl) >= need);
-  if (ballot == 0) {
-    if (lane == 0) op.err = E_EVICT_MISMATCH;
-    *rank_in_bin = 1;
-    return 0;
-  }
-  const int L = __ffs(ballot) - 1;
-  u64 cum = __shfl_sync(FULL, incl - local, L);
-  u32 bin = 0;
-  if (lane == L) {
-    u32 i = 0;
-    for (; i + 1 < per; ++i) {
-      const u32 c = cnt[base + i];
-      if (cum + c >= need) break;
-      cum += c;
+  s = __reduce_add_sync(FULL, s);
+  if (lane == 0) wsum[warp] = s;
+  __syncthreads();
+  if (warp == 0) {
+    const u32 v = lane < nw ? wsum[lane] : 0u;
+    u32 incl = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 x = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += x;
     }
-    bin = base + i;
+    const u64 need = op.need;
+    const unsigned ballot = __ballot_sync(FULL, static_cast<u64>(incl) >= need);
+    u32 bin = 0;
+    u64 before = need - 1;  // (rank 1 on a mismatch)
+    if (ballot == 0) {
+      if (lane == 0) op.err = E_EVICT_MISMATCH;
+    } else {
+      const int W = __ffs(ballot) - 1;
+      u64 cum = __shfl_sync(FULL, incl - v, W);
+      for (u32 r = 0; r < seg; r += 32) {
+        const u32 b = W * seg + r + lane;
+        const u32 c = (r + lane < seg && b < nbins) ? cnt[b] : 0u;
+        u32 in2 = c;
+        for (int o = 1; o < 32; o <<= 1) {
+          const u32 x = __shfl_up_sync(FULL, in2, o);
+          if (lane >= o) in2 += x;
+        }
+        const unsigned hit = __ballot_sync(FULL, cum + in2 >= need);
+        if (hit) {
+          const int j = __ffs(hit) - 1;
+          bin = W * seg + r + j;
+          before = cum + __shfl_sync(FULL, in2 - c, j);
+          break;
+        }
+        cum += __shfl_sync(FULL, in2, 31);
+      }
+      if (lane == 0) {
+        op.need = need - before;
+        op.prefix = (op.prefix << d) | bin;
+      }
+    }
+    if (lane == 0) {
+      sel[0] = bin;
+      sel[1] = need - before;
+    }
   }
-  bin = __shfl_sync(FULL, bin, L);
-  cum = __shfl_sync(FULL, cum, L);
-  *rank_in_bin = need - cum;
-  if (lane == 0) {
-    op.need = need - cum;
-    op.prefix = (op.prefix << d) | bin;
-  }
-  return bin;
+  __syncthreads();
+  *rank_in_bin = sel[1];
+  return static_cast<u32>(sel[0]);
 }
 
 __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
@@ -326,6 +349,8 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
   cg::grid_group grid = cg::this_grid();
   __shared__ Op op;
   __shared__ u32 scnt[kGridBins], sdmax[kGridBins];
+  __shared__ u32 swsum[32];
+  __shared__ u64 ssel[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int nt = blockDim.x;
   const int gw = blockIdx.x * nw + warp, GW = gridDim.x * nw;
@@ -412,10 +437,10 @@ __global__ void __launch_bounds__(512) grid_evict_kernel(GridEvictArgs A) {
         if (last) sdmax[i] = __ldcg(&gd[i]);
       }
       __syncthreads();
-      if (warp == 0) {
+      {
         u64 rank = 0;
-        const u32 bin = select_bin_s(op, scnt, nbins, d, lane, &rank);
-        if (last && lane == 0) op.cut_depth = static_cast<u64>(sdmax[bin]) + 1 - rank;
+        const u32 bin = select_bin_cta(op, scnt, nbins, d, lane, warp, nw, swsum, ssel, &rank);
+        if (last && tid == 0) op.cut_depth = static_cast<u64>(sdmax[bin]) + 1 - rank;
       }
       if (blockIdx.x == 0) {  // the buffer of pass + 2 (read last in pass - 1)
         u32* z = A.ghist + static_cast<size_t>((pass + 2) % 3) * 2 * kGridBins;
