@@ -580,8 +580,10 @@ __device__ __noinline__ u32 select_bin(Op& op, Hist& h, u32 nbins, int d, int la
   const u32 per = (nbins + 31) / 32;
   const u32 base = lane * per;
   u32 local = 0;
-  for (u32 i = 0; i < per; ++i)
+  for (u32 k = 0; k < per; ++k) {  // lane-rotated order: ~no bank conflicts in shared memory
+    const u32 i = (k + lane) % per;
     if (base + i < nbins) local += hist_ld(h, &h.cnt[base + i]);
+  }
   u32 incl = local;
   for (int o = 1; o < 32; o <<= 1) {
     u32 v = __shfl_up_sync(FULL, incl, o);
