@@ -28,7 +28,13 @@
 
 namespace kvg {
 
-constexpr int kGridMatchWarps = 8;
+#ifndef KVG_GRID_MATCH_WARPS
+#define KVG_GRID_MATCH_WARPS 8
+#endif
+constexpr int kGridMatchWarps = KVG_GRID_MATCH_WARPS;
+#ifndef KVG_GM_TMA  // bucket loads of the batched lookup as bulk async copies to shared memory
+#define KVG_GM_TMA 1   // measured on the C5-size table: 0.29 ms (register form) -> 0.25 ms
+#endif
 #ifndef KVG_GM_MINB  // resident grid-match CTAs per SM the register budget allows
 #define KVG_GM_MINB 4  // measured 3 (71 registers) / 4 / 5 / 6: C5 lookup 0.425 / 0.323 / 0.328 / 0.353 ms
 #endif
@@ -144,6 +150,121 @@ __device__ __forceinline__ bool match_group(const GridMatchArgs& A, u32 i, u64 n
   return miss == NIL32;
 }
 
+#if KVG_GM_TMA
+// ---- bulk-copy form of match_group (sm_90+/sm_100a async copy engine) ----
+// Each warp owns kGridItemChunks 512 B bucket buffers in shared memory and
+// one mbarrier. Lanes 0..7 each issue one cp.async.bulk of their chunk's
+// bucket (global -> shared, completion counted in bytes on the mbarrier), the
+// warp waits on the barrier phase once, and every later read of the group's
+// slots is a shared-memory load: the 8 buckets in flight no longer occupy 32
+// registers per lane, so more warps fit an SM. Collision steps re-issue the
+// colliding chunks' copies as one more round.
+__device__ __forceinline__ void mbar_init(u64* bar) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(u64* bar, unsigned bytes) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, u64* bar) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, unsigned parity) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}" ::"r"(a), "r"(parity) : "memory");
+}
+
+struct GmWarp {
+  Slot* buf;      // [kGridItemChunks][kChunk] this warp's bucket buffers
+  u64* bar;
+  unsigned phase; // parity of the barrier's current phase
+};
+
+__device__ __forceinline__ bool match_group(const GridMatchArgs& A, u32 i, u64 n, u64 g,
+                                            int lane, GmWarp& W) {
+  const u64 owner = (static_cast<u64>(A.agents[i]) + 1) << 32;
+  const u64 c0 = (A.S >> 5) + g * kGridItemChunks;
+  const u64 stamp = A.clock0 + i + 1;
+  // lane j < kGridItemChunks tracks chunk j's bucket
+  const u64 cj = c0 + (lane & (kGridItemChunks - 1));
+  u32 bj = static_cast<u32>(hash64(owner | (cj * 32))) & A.mask;
+  u32 pend = 0, fnd = 0;  // (warp-uniform)
+  for (int j = 0; j < kGridItemChunks; ++j)
+    if ((c0 + j) * 32 < n) pend |= 1u << j;
+  u32 round = pend;
+  for (;;) {
+    // WAR across proxies: the previous reads of these buffers are done
+    __syncwarp();
+    if (lane == 0) mbar_expect(W.bar, __popc(round) * static_cast<unsigned>(kChunk * sizeof(Slot)));
+    __syncwarp();
+    if (lane < kGridItemChunks && ((round >> lane) & 1u)) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      bulk_load(W.buf + lane * kChunk, A.table + static_cast<size_t>(bj) * kChunk,
+                kChunk * sizeof(Slot), W.bar);
+    }
+    mbar_wait(W.bar, W.phase);
+    W.phase ^= 1u;
+    u32 more = 0;
+    for (int j = 0; j < kGridItemChunks; ++j) {
+      if (!((round >> j) & 1u)) continue;
+      const u64 tag = owner | ((c0 + j) * 32);
+      const u64 k0 = W.buf[j * kChunk].key;  // (broadcast read)
+      if (k0 == tag) fnd |= 1u << j;
+      else if (k0 != kEmptyKey) more |= 1u << j;
+    }
+    if (!more) break;
+    if (lane < kGridItemChunks && ((more >> lane) & 1u)) bj = (bj + 1) & A.mask;
+    round = more;
+  }
+  u32 miss = NIL32, res = 0;
+  for (int j = 0; j < kGridItemChunks; ++j) {
+    const u64 c = c0 + j;
+    if (c * 32 >= n) break;  // warp-uniform
+    const Slot cur = W.buf[j * kChunk + lane];
+    const u32 cb = __shfl_sync(FULL, bj, j);
+    const bool found = (fnd >> j) & 1u;
+    const u64 page = c * 32 + lane;
+    const bool in = page >= A.S && page < n;
+    const bool r = found && in && (cur.meta & kResident);
+    if (in && !r && page < miss) miss = static_cast<u32>(page);
+    res += r;
+    if (__any_sync(FULL, r)) {  // refresh: every resident page in range takes the stamp
+      const u64 nm = r ? m_make(stamp, m_pins(cur.meta)) : cur.meta;
+      if (r) st_meta(&A.table[(size_t)cb * kChunk + lane], nm);
+      summ_write(A.summ, cb, nm, lane);
+    }
+  }
+  miss = __reduce_min_sync(FULL, miss);
+  res = __reduce_add_sync(FULL, res);
+  if (lane == 0) {
+    if (miss != NIL32) atomicMin(&A.fm[i], miss);
+    if (res) atomicAdd(&A.res[i], res);
+  }
+  return miss == NIL32;
+}
+
+#define KVG_GM_WARP_SETUP                                                          \
+  __shared__ __align__(128) Slot gm_buf[kGridMatchWarps][kGridItemChunks * kChunk]; \
+  __shared__ __align__(8) u64 gm_bar[kGridMatchWarps];                              \
+  GmWarp W{gm_buf[w], &gm_bar[w], 0u};                                              \
+  if (lane == 0) mbar_init(W.bar);                                                  \
+  __syncwarp();
+#define KVG_GM_W , W
+#else
+#define KVG_GM_WARP_SETUP
+#define KVG_GM_W
+#endif
+
 __device__ __forceinline__ u64 match_groups(const GridMatchArgs& A, u64 n) {
   if (n <= A.S) return 0;
   return (((n - 1) >> 5) - (A.S >> 5)) / kGridItemChunks + 1;
@@ -155,6 +276,7 @@ __device__ __forceinline__ u64 match_groups(const GridMatchArgs& A, u64 n) {
 __global__ void __launch_bounds__(kGridMatchWarps * 32, KVG_GM_MINB) grid_match_kernel(GridMatchArgs A) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const u32 gw = blockIdx.x * kGridMatchWarps + w, GW = gridDim.x * kGridMatchWarps;
+  KVG_GM_WARP_SETUP
   for (u32 i = gw; i < A.n; i += GW) {
     const u64 n = A.lens[i] / A.ps;
     if (lane == 0) {
@@ -163,7 +285,7 @@ __global__ void __launch_bounds__(kGridMatchWarps * 32, KVG_GM_MINB) grid_match_
     }
     const u64 groups = match_groups(A, n);
     if (groups == 0) continue;
-    if (match_group(A, i, n, 0, lane) && groups > 1) {  // (warp-uniform)
+    if (match_group(A, i, n, 0, lane KVG_GM_W) && groups > 1) {  // (warp-uniform)
       // file groups [1, groups) as work items: one contiguous range per query
       unsigned base = 0;
       if (lane == 0) base = atomicAdd(A.n_items, static_cast<unsigned>(groups - 1));
@@ -182,10 +304,11 @@ __global__ void __launch_bounds__(kGridMatchWarps * 32, KVG_GM_MINB) grid_match_
 __global__ void __launch_bounds__(kGridMatchWarps * 32, KVG_GM_MINB) grid_match_rest_kernel(GridMatchArgs A) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const u64 gw = blockIdx.x * kGridMatchWarps + w, GW = gridDim.x * kGridMatchWarps;
+  KVG_GM_WARP_SETUP
   const u64 total = *A.n_items;
   for (u64 k = gw; k < total; k += GW) {
     const ulonglong2 it = A.items[k];  // {query << 32 | group, pages}
-    match_group(A, static_cast<u32>(it.x >> 32), it.y, it.x & 0xffffffffu, lane);
+    match_group(A, static_cast<u32>(it.x >> 32), it.y, it.x & 0xffffffffu, lane KVG_GM_W);
   }
 }
 

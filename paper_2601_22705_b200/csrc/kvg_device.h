@@ -226,7 +226,10 @@ struct CacheState {
 };
 
 // Grid-wide seam kernels (grid.cuh): launch arguments.
-constexpr int kGridItemChunks = 8;  // private chunks per match work item (4 KB of slots)
+#ifndef KVG_GRID_ITEM_CHUNKS
+#define KVG_GRID_ITEM_CHUNKS 8
+#endif
+constexpr int kGridItemChunks = KVG_GRID_ITEM_CHUNKS;  // private chunks per match work item (8: 4 KB of slots)
 constexpr int kGridSumDepth = 8;    // bucket summaries in flight per lane (grid evict)
 
 struct GridMatchArgs {
