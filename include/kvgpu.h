@@ -247,14 +247,21 @@ KVG_API void kvg_engine_params_init(kvg_engine_params* e);
 
 typedef struct kvg_batch kvg_batch;
 
+enum { KVG_HOST_OUTPUTS_NONE = 0, KVG_HOST_OUTPUTS_STREAM = 1, KVG_HOST_OUTPUTS_COPY = 2 };
 typedef struct kvg_batch_options {
   uint32_t warps_per_sim; /* 0 = automatic (1 for small sims, up to 32)   */
   uint32_t log_capacity;  /* per-sim event-log records; 0 disables logging */
   uint64_t trace_capacity;/* per-sim trace rows; 0 = automatic (grows)     */
   uint32_t host_outputs;  /* 1: kvg_batch_run also delivers results, agent
-                             stats and (densely packed) trace rows into
-                             pinned host memory before returning; 0: they
-                             stay in HBM until first accessed */
+                             stats and trace rows into pinned host memory
+                             before returning, the rows streamed by the
+                             kernel while it runs (best for one blocking
+                             call); 2 (KVG_HOST_OUTPUTS_COPY): the same, the
+                             rows copied by one copy-engine DMA after the
+                             kernel (no SM work: best when batches are
+                             pipelined with kvg_batch_launch / _wait, the
+                             DMA overlapping the next batch's kernel); 0:
+                             outputs stay in HBM until first accessed */
   uint32_t verify;        /* 1: every prefix match is also re-derived by the
                              block-hash probe and checked (a mismatch fails
                              the simulation with KVG_ERR_STATE) */

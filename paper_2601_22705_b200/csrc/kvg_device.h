@@ -162,7 +162,7 @@ struct SimDev {
   AgentDev* agents;
   u32* pend;
   u32* paus;
-  u32* ready;         // unused (kept for layout stability)
+  unsigned long long* pack_cursor;  // pack_mode: batch-wide cursor of the dense row region
   Member* batch;
   HeapEnt* heap;      // agent events (leader-only binary heap)
   u32* rbits;         // ready bitmap: in_active && AwaitingAdmission
@@ -183,7 +183,9 @@ struct SimDev {
   u64* hkeys;         // [hmask+1] head-key hash: page key of a node's first page
   u32* hvals;         //           -> node id
   double* xring;      // [xcap] link transfer end times (FIFO: ends never decrease)
-  u32 tcap, hmask, xcap, pad1;
+  u32 tcap, hmask, xcap;
+  u32 pack_mode;      // 1: at its end the simulation copies its rows densely to trace_out
+                      // at a base taken from *pack_cursor (counts[3]); no streaming
   // ---- outputs
   kvg_agent_stats* stats;
   kvg_trace_row* trace;
@@ -195,7 +197,8 @@ struct SimDev {
   // host delivery (host_outputs): the simulation streams its trace rows into
   // its slice of a mapped pinned host array while it runs (in chunks after
   // control-tick rounds, the rest at its end), so the PCIe transfer overlaps
-  // the run instead of following it (nullptr: rows stay in HBM)
+  // the run instead of following it (nullptr: rows stay in HBM). With
+  // pack_mode it is the batch's dense device row region instead.
   kvg_trace_row* trace_out;
 };
 

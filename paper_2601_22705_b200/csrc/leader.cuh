@@ -191,7 +191,7 @@ constexpr u64 kFlushRows = KVG_FLUSH_ROWS;
 #endif
 __device__ __forceinline__ void put_row(const SimDev& D, u64 i, const kvg_trace_row& row) {
   D.trace[i] = row;
-  if (KVG_ROW_WT && D.trace_out) D.trace_out[i] = row;
+  if (KVG_ROW_WT && D.trace_out && !D.pack_mode) D.trace_out[i] = row;
 }
 
 // lifecycle_edge (workload.cpp:110-128)
@@ -852,7 +852,7 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
   L.n_ready = 0;
   L.used = L.cclock = L.discarded = L.lookups = 0;
   L.n_flushed = 0;
-  L.stream_on = D.trace_out != nullptr && !KVG_ROW_WT;
+  L.stream_on = D.trace_out != nullptr && !D.pack_mode && !KVG_ROW_WT;
   L.log_on = D.log != nullptr;
   L.agent_steps = L.events = L.evict_calls = L.evicted = 0;
   L.pin_max = L.pin_priv = 0;
@@ -2449,6 +2449,25 @@ __device__ __noinline__ void flush_rows(const SimDev& D, Lead& L, int t, int nt,
   if (t == 0) L.n_flushed = n;
 }
 
+// Copy-mode host delivery (host_outputs == 2): at its end the simulation
+// copies its rows into the batch's dense row region at a base taken from the
+// batch-wide cursor (published in counts word 3), so the host receives
+// exactly the rows produced in ONE copy-engine DMA after the kernel.
+__device__ __noinline__ void pack_rows(const SimDev& D, Lead& L, int t, int nt) {
+  const u64 n = L.n_trace < D.trace_cap ? L.n_trace : D.trace_cap;
+  if (t == 0) {
+    const u64 base = n ? atomicAdd(D.pack_cursor, static_cast<unsigned long long>(n)) : 0;
+    D.counts[3] = base;
+    L.n_flushed = base;  // (broadcast)
+  }
+  if (nt == 32) __syncwarp();
+  else __syncthreads();
+  constexpr u64 kW = sizeof(kvg_trace_row) / sizeof(u64);
+  const u64* src = reinterpret_cast<const u64*>(D.trace);
+  u64* dst = reinterpret_cast<u64*>(D.trace_out + L.n_flushed);
+  for (u64 w = t; w < n * kW; w += nt) dst[w] = src[w];
+}
+
 template <int kDepth, bool kOff, bool kSmemDesc, bool kLru, bool kChain = false>
 __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
   __shared__ Lead L;
@@ -2541,7 +2560,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     L.prof_ph = 47;
   }
 #endif
-  const bool stream = D.trace_out != nullptr;  // streamed host delivery
+  const bool stream = D.trace_out != nullptr && !D.pack_mode;  // streamed host delivery
   for (;;) {
     if (tid == 0) leader_step<kOff, kChain>(D, L, op);
     __syncthreads();
@@ -2570,6 +2589,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
     if (tid == 0) PROF_MARK(L, 46);
   }
   if (stream && !KVG_ROW_WT) flush_rows(D, L, tid, blockDim.x, 0);  // the rest
+  if (D.pack_mode) pack_rows(D, L, tid, blockDim.x);
 #ifdef KVG_PROFILE
   if (tid == 0) {
     PROF_MARK(L, 47);

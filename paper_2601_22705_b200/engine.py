@@ -192,13 +192,20 @@ class SimSpec:
         return SimSpec(pop, pol, s.cost.to_abi(), eng.to_abi())
 
 
+HOST_OUTPUTS_COPY = 2
+
+
 class Batch:
     """A set of independent simulations executed on one GPU in one launch."""
 
     def __init__(self, specs: list[SimSpec], device: int = 0, warps_per_sim: int = 0,
-                 log_capacity: int = 0, trace_capacity: int = 0, host_outputs: bool = False,
+                 log_capacity: int = 0, trace_capacity: int = 0, host_outputs: bool | int = False,
                  verify: bool | None = None):
-        """verify: re-derive every prefix match with the block-hash probe and
+        """host_outputs: False / 0 outputs stay in HBM; True / 1 delivered to
+        pinned host memory by run() / wait(), trace rows streamed by the kernel;
+        2 (HOST_OUTPUTS_COPY) the same with the rows copied by one DMA after
+        the kernel (for pipelined launch / wait).
+        verify: re-derive every prefix match with the block-hash probe and
         check it against the incrementally held state (default: the
         KVG_VERIFY environment variable; the GPU test suite sets it)."""
         if verify is None:

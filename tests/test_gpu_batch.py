@@ -151,7 +151,8 @@ def test_c4_sweep_runs_in_one_wave(verify):
     assert g["waves"] == 1, g
 
 
-def test_launch_wait_pipeline_matches_run():
+@pytest.mark.parametrize("mode", [1, engine.HOST_OUTPUTS_COPY], ids=["streamed", "dma"])
+def test_launch_wait_pipeline_matches_run(mode):
     # kvg_batch_launch / kvg_batch_wait with two batches in flight (the bench's
     # pipelined e2e leg) give the same records as a blocking kvg_batch_run
     pop = engine.Population(config.c1_toy().workload, 42)
@@ -164,7 +165,7 @@ def test_launch_wait_pipeline_matches_run():
     prev = None
     got = []
     for _ in range(3):
-        b = engine.Batch(specs, verify=False, host_outputs=True)
+        b = engine.Batch(specs, verify=False, host_outputs=mode)
         b.launch()
         with pytest.raises(Exception):
             b.result(0)  # not readable while in flight
@@ -196,3 +197,10 @@ def test_free_while_in_flight_waits():
     c.run()
     assert all(r.status == 0 for r in c.results_raw())
     c.close()
+
+
+def test_host_outputs_mode_checked():
+    pop = engine.Population(config.c1_toy().workload, 42)
+    specs = [engine.SimSpec.from_scenario(s, population=pop) for s in config.c4_sweep(4)]
+    with pytest.raises(Exception):
+        engine.Batch(specs, host_outputs=3)
