@@ -13,8 +13,9 @@ PH = ["EVENT", "MEMBER", "M_MATCHED", "M_INSERT", "M_EVICTED", "M_COMMIT", "M_CR
 names = {i: "leader:" + n for i, n in enumerate(PH)}
 names.update({32 + k: "coop:" + n for k, n in enumerate(
     ["NONE", "EXIT", "RANGE", "EVICT", "REBUILD", "SCANFREE", "FRONTIER", "TICKS", "PHASES",
-     "GROUP"])})
-names.update({44: "admission_pass", 43: "fast_housekeeping", 46: "leader_step entry+sync", 47: "init/finalize"})
+     "GROUP", "STORM", "FLUSH"])})
+names.update({24: "fast_housekeeping", 25: "member_loop (chain form)", 26: "agent event handler",
+              27: "admission_pass", 46: "leader_step entry+sync", 47: "init/finalize"})
 which = sys.argv[1] if len(sys.argv) > 1 else "c4"
 if which == "c4":
     pop = engine.Population(config.c1_toy().workload, 42)
