@@ -944,6 +944,11 @@ __device__ __noinline__ void lead_init(const SimDev& D, Lead& L, Op& op) {
 // an admission check that would admit / resume / pause / dispatch, the horizon,
 // or the end of the run. Same arithmetic, same order as on_tick /
 // on_admission_check (engine.cpp:245-291, controller.cpp:67-160).
+// kHoist: loop invariants of the trace row held in registers (the row stores
+// go through a generic pointer, after which the compiler reloads Lead
+// fields). Measured: C3 264 -> 254 ms in the one-CTA-per-SM kernels, C4 +8 %
+// in the 72-register sweep kernel (spills), so only the former hoist.
+template <bool kHoist>
 __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   if (L.finished == L.n || L.status != KVG_OK) return;
   const double t_agent = L.hsize > 0 ? L.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
@@ -966,6 +971,11 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   const u64 dec = L.decoded_cum, rec = L.rec_cum;
   const u64 trace_cap = D.trace_cap;
   const kvg_controller_config c = L.cfg;
+  const bool offload_h = kHoist ? L.offload : false;
+  const double win_fixed_h = !kHoist ? 0.0
+                             : kind == KVG_POLICY_UNCONTROLLED ? static_cast<double>(L.n)
+                                                               : static_cast<double>(L.cap);
+  const u64 cap_h = kHoist ? static_cast<u64>(L.cap) : 0;
   // evolving state
   double clock = L.clock, tick_t = L.tick_t, adm_t = L.adm_t;
   double hit_m = L.hit_m, hit_r = L.hit_r, window = L.window, su = L.su, sh = L.sh;
@@ -1016,14 +1026,17 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
         row.time = clock;
         row.usage = usage;
         row.hit_rate = hit;
-        row.window = kind == KVG_POLICY_AIMD ? window
-                     : kind == KVG_POLICY_UNCONTROLLED ? static_cast<double>(L.n)
-                                                       : static_cast<double>(L.cap);
+        if (kHoist)
+          row.window = kind == KVG_POLICY_AIMD ? window : win_fixed_h;
+        else
+          row.window = kind == KVG_POLICY_AIMD ? window
+                       : kind == KVG_POLICY_UNCONTROLLED ? static_cast<double>(L.n)
+                                                         : static_cast<double>(L.cap);
         row.active = act;
         row.pending = pending;
         row.decoded_cum = dec;
         row.recompute_cum = rec;
-        row.transfers = L.offload ? x_in_flight(D, L, clock) : 0;
+        row.transfers = (kHoist ? offload_h : L.offload) ? x_in_flight(D, L, clock) : 0;
         row.hit_matched = m;
         row.hit_requested = r;
         put_row(D, i, row);
@@ -1045,7 +1058,7 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
         // without another loop turn
         const u64 limit = kind == KVG_POLICY_UNCONTROLLED ? ~0ull
                           : kind == KVG_POLICY_AIMD ? static_cast<u64>(floor(window))
-                                                    : static_cast<u64>(L.cap);
+                                                    : kHoist ? cap_h : static_cast<u64>(L.cap);
         if (tick_t > clock && nready0 && !(act < limit && admit_src)) {
           adm_on = 0;
           ++events;
@@ -1056,7 +1069,7 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
     } else {
       const u64 limit = kind == KVG_POLICY_UNCONTROLLED ? ~0ull
                         : kind == KVG_POLICY_AIMD ? static_cast<u64>(floor(window))
-                                                  : static_cast<u64>(L.cap);
+                                                  : kHoist ? cap_h : static_cast<u64>(L.cap);
       // nothing ready => no pause victim and nothing to dispatch
       const bool noop = nready0 && !(act < limit && admit_src);
       if (!noop) break;  // the general path runs the real admission pass
@@ -1695,7 +1708,7 @@ __device__ __forceinline__ bool member_loop(const SimDev& D, Lead& L, Op& op) {
   return false;
 }
 
-template <bool kOff, bool kChain>
+template <bool kOff, bool kChain, bool kBig = false>  // kBig: a one-CTA-per-SM kernel
 __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
   op.kind = OP_NONE;
   for (;;) {
@@ -1719,7 +1732,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           return;
         }
         PROF_MARK(L, 24);
-        fast_housekeeping(D, L);
+        fast_housekeeping<kBig>(D, L);
         PROF_MARK(L, PH_EVENT);
         int which = -1;  // 0 agent, 1 tick, 2 admission (the event ranks)
         double bt = 0;
@@ -2562,7 +2575,7 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
 #endif
   const bool stream = D.trace_out != nullptr && !D.pack_mode;  // streamed host delivery
   for (;;) {
-    if (tid == 0) leader_step<kOff, kChain>(D, L, op);
+    if (tid == 0) leader_step<kOff, kChain, kLru>(D, L, op);
     __syncthreads();
     if (op.kind == OP_EXIT) break;
     if (tid == 0) PROF_MARK(L, 32 + op.kind);
