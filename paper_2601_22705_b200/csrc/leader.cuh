@@ -1244,31 +1244,54 @@ __device__ __noinline__ void coop_phases(const SimDev& D, Lead& L, int lane) {
   kvg_phase_label ph[3];
   if (mk > 0) {
     u64 enter = n, leave = n;  // first hot row; row that ends the middle
-    int bad = 0;
+    long long bad = 0;         // non-hot rows since the last hot one (after enter)
+    const long long H = pp.hysteresis;
+    // each lane reads two fields of one row; the next 32 rows are loaded
+    // while lane 0 walks the current ballot run by run (ffs), not bit by bit
+    double u_nx = 0.0, h_nx = 0.0;
+    if (static_cast<u64>(lane) < n) {
+      u_nx = D.trace[lane].usage;
+      h_nx = D.trace[lane].hit_rate;
+    }
     for (u64 base = 0; base < n && leave == n; base += 32) {
       const u64 i = base + lane;
-      bool hot = false;
-      if (i < n) {
-        const kvg_trace_row& r = D.trace[i];
-        hot = r.usage >= pp.sat_threshold && r.hit_rate < pp.hit_threshold;
+      const bool hot = i < n && u_nx >= pp.sat_threshold && h_nx < pp.hit_threshold;
+      if (i + 32 < n) {
+        u_nx = D.trace[i + 32].usage;
+        h_nx = D.trace[i + 32].hit_rate;
       }
       const unsigned m = __ballot_sync(FULL, hot);
       if (lane == 0) {
         const u32 cnt = n - base < 32 ? static_cast<u32>(n - base) : 32u;
-        for (u32 k = 0; k < cnt; ++k) {
-          const bool h = (m >> k) & 1u;
-          if (enter == n) {
-            if (h) enter = base + k;
-            continue;
+        u32 p = 0;
+        if (enter == n) {  // warmup until the first hot row
+          if (m) {
+            const u32 k0 = __ffs(m) - 1;
+            enter = base + k0;
+            p = k0 + 1;
+          } else {
+            p = cnt;
           }
-          if (h) {
+        }
+        while (p < cnt) {
+          const u32 rest = m >> p;
+          if (rest & 1u) {  // a run of hot rows resets the count
+            const u32 inv = ~rest;
+            p += inv ? static_cast<u32>(__ffs(inv) - 1) : 32u - p;
             bad = 0;
             continue;
           }
-          if (++bad >= pp.hysteresis) {
-            leave = base + k + 1 - static_cast<u64>(pp.hysteresis);
+          // a run of non-hot rows [p, p + z): the middle ends at the row that
+          // brings the count to H (the row-by-row rule ++bad >= H)
+          u32 z = rest ? static_cast<u32>(__ffs(rest) - 1) : 32u - p;
+          if (z > cnt - p) z = cnt - p;
+          const long long t = H - bad - 1 > 0 ? H - bad - 1 : 0;
+          if (t < static_cast<long long>(z)) {
+            leave = static_cast<u64>(static_cast<long long>(base + p) + t + 1 - H);
             break;
           }
+          bad += z;
+          p += z;
         }
       }
       leave = __shfl_sync(FULL, leave, 0);

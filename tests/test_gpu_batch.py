@@ -204,3 +204,40 @@ def test_host_outputs_mode_checked():
     specs = [engine.SimSpec.from_scenario(s, population=pop) for s in config.c4_sweep(4)]
     with pytest.raises(Exception):
         engine.Batch(specs, host_outputs=3)
+
+
+def test_device_phases_match_host_classifier_over_params():
+    # coop_phases (run-by-run scan of the ballot words) against the host
+    # classifier kvg_classify_phases, itself pinned to the reference goldens
+    # (tests/test_config.py), over thresholds and hysteresis lengths 1-100
+    import ctypes as C
+    import random
+    rng = random.Random(7)
+    pop = engine.Population(config.c1_toy().workload, 42)
+    scen = config.c4_sweep(256)
+    for s in scen:
+        s.engine.sat_threshold = rng.choice([0.3, 0.5, 0.8, 0.95])
+        s.engine.hit_threshold = rng.choice([0.2, 0.5, 0.9, 1.0])
+        s.engine.hysteresis = rng.choice([1, 2, 3, 5, 17, 40, 100])
+    specs = [engine.SimSpec.from_scenario(s, population=pop) for s in scen]
+    b = engine.Batch(specs, verify=False, host_outputs=True)
+    b.run()
+    res = b.results_raw()
+    seen = set()
+    for i, s in enumerate(scen):
+        tr = b.trace(i)
+        rows = (abi.TraceRow * max(1, len(tr)))()
+        for k, r in enumerate(tr):
+            rows[k] = abi.TraceRow(**r)
+        out = (abi.PhaseLabel * 3)()
+        n = C.c_size_t()
+        pp = s.engine.to_abi().phases
+        assert engine.lib().kvg_classify_phases(rows, len(tr), res[i].makespan, C.byref(pp), out,
+                                                3, C.byref(n)) == 0
+        want = [(out[k].phase, out[k].start, out[k].end) for k in range(n.value)]
+        got = [(res[i].phases[k].phase, res[i].phases[k].start, res[i].phases[k].end)
+               for k in range(res[i].n_phases)]
+        assert got == want, (i, s.engine.hysteresis, got, want)
+        seen.add(len(want))
+    b.close()
+    assert len(seen) >= 2  # the cases cover more than one phase shape
