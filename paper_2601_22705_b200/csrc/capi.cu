@@ -107,7 +107,11 @@ size_t hot_smem_bytes(u64 n, bool big) {
 size_t hot_smem(u64 n, bool big = false) {
   if (!big) return n > 128 ? 0 : hot_smem_bytes(n, false);
   const size_t b = hot_smem_bytes(n, true);
-  return b <= kBigSmemMax ? b : 0;
+  if (b <= kBigSmemMax) return b;
+  // too big as a whole: the ready bitmaps alone (leader.cuh engine_body)
+  const u64 nwords = (n + 31) / 32;
+  const size_t bm = (nwords + (nwords + 31) / 32) * 4;
+  return bm <= kBigSmemMax ? bm : 0;
 }
 
 // Big-kernel offload sims also keep the tree's walk mirror (tree.cuh tw) in

@@ -274,6 +274,43 @@ __device__ KVG_READY_FN u32 ready_next(const SimDev& D, const Lead& L, u32 from)
   return NIL;
 }
 
+// ready_next for the one-CTA-per-SM kernels (dispatch's member walk): the
+// same answer, the second-level words read four at a time (C5: 64 words,
+// the walk between sparse ready agents was ~18 % of the leader's samples).
+// Separate from ready_next so the sweep kernel's inlined copies stay as small.
+__device__ __forceinline__ u32 ready_next_wide(const SimDev& D, const Lead& L, u32 from) {
+  if (from >= L.n) return NIL;
+  const u32 w = from >> 5;
+  const u32 bits = L.rbits[w] & (~0u << (from & 31));
+  if (bits) return (w << 5) + __ffs(bits) - 1;
+  const u32 w1 = w + 1;
+  if (w1 >= L.nwords) return NIL;
+  const u32 n1 = (L.nwords + 31) >> 5;
+  const bool al = (reinterpret_cast<uintptr_t>(L.rl1) & 15) == 0;
+  u32 j = w1 >> 5;
+  u32 m = L.rl1[j] & (~0u << (w1 & 31));
+  while (!m && j + 1 < n1) {
+    ++j;
+    if (al && (j & 3) == 0 && j + 4 <= n1) {
+      const uint4 q = *reinterpret_cast<const uint4*>(L.rl1 + j);
+      if (q.x) m = q.x;
+      else if (q.y) { m = q.y; j += 1; }
+      else if (q.z) { m = q.z; j += 2; }
+      else if (q.w) { m = q.w; j += 3; }
+      else j += 3;
+    } else {
+      m = L.rl1[j];
+    }
+  }
+  if (!m) return NIL;
+  const u32 ww = (j << 5) + __ffs(m) - 1;
+  return (ww << 5) + __ffs(L.rbits[ww]) - 1;
+}
+template <bool kWide>
+__device__ __forceinline__ u32 ready_next_k(const SimDev& D, const Lead& L, u32 from) {
+  return kWide ? ready_next_wide(D, L, from) : ready_next(D, L, from);
+}
+
 // AgentRecord::set_state (workload.cpp:130-137)
 __device__ KVG_MID_FN void set_state(const SimDev& D, Lead& L, u32 id, uint8_t s) {
   AgentDev& a = L.ag[id];
@@ -1560,6 +1597,7 @@ __device__ __noinline__ bool offload_step(const SimDev& D, Lead& L, Op& op) {
 // PH_M_MATCHED .. PH_M_RESTORED, straight through: no cooperative op is ever
 // needed in chain mode, so the member does not return to the phase dispatch
 // between them.
+template <bool kBig>
 __device__ __forceinline__ void chain_member(const SimDev& D, Lead& L) {
   const u64 f = L.m_f;
   const u64 matched = f * L.ps;
@@ -1625,7 +1663,7 @@ __device__ __forceinline__ void chain_member(const SimDev& D, Lead& L) {
     ++L.stall_streak;
     log_rec(D, L, KVG_LOG_INSERT, L.m_id, 0, 0);
   }
-  L.m_next = ready_next(D, L, L.m_id + 1);
+  L.m_next = ready_next_k<kBig>(D, L, L.m_id + 1);
 }
 
 // dispatch_batch's end (engine.cpp:317-332): the batch wall starts at
@@ -1673,7 +1711,7 @@ __device__ __forceinline__ void batch_end(const SimDev& D, Lead& L) {
 // true when it posted a cooperative op (the caller returns to the CTA);
 // otherwise L.phase says where to go on (PH_EVENT after an inline batch end in
 // chain mode; a member phase in table / verify mode).
-template <bool kOff, bool kChain>
+template <bool kOff, bool kChain, bool kBig = false>
 __device__ __forceinline__ bool member_loop(const SimDev& D, Lead& L, Op& op) {
   for (;;) {  // chain mode: whole member attempts inline, one after another
   const u32 id = L.m_next;
@@ -1716,7 +1754,7 @@ __device__ __forceinline__ bool member_loop(const SimDev& D, Lead& L, Op& op) {
   L.lazy_sh = L.m_now;
   ch_remove(L, id);  // its path is pinned from the match on
   if (kChain || L.chain) {
-    chain_member(D, L);
+    chain_member<kBig>(D, L);
     if (L.status == KVG_ERR_STATE) break;
     continue;  // the next member
   }
@@ -1818,11 +1856,11 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.batch_n = 0;
           L.stall_streak = 0;
           L.b_wall = L.b_total = 0.0;
-          L.m_next = ready_next(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
+          L.m_next = ready_next_k<kBig>(D, L, 0);  // dispatch_batch (engine.cpp:305-333)
           L.phase = PH_MEMBER;
           if (kChain || L.chain) {  // members and the batch end inline, then this loop
             PROF_MARK(L, 25);
-            const bool posted = member_loop<kOff, kChain>(D, L, op);
+            const bool posted = member_loop<kOff, kChain, kBig>(D, L, op);
             PROF_MARK(L, PH_EVENT);
             if (posted) return;
             if (L.phase == PH_EVENT) continue;
@@ -1932,7 +1970,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
           L.phase = PH_O_MEMBER;
           continue;
         }
-        if (member_loop<kOff, kChain>(D, L, op)) return;
+        if (member_loop<kOff, kChain, kBig>(D, L, op)) return;
         continue;
       }
       case PH_M_MATCHED: {
@@ -2550,6 +2588,15 @@ __device__ __forceinline__ void engine_body(const SimDev* __restrict__ sims) {
       L.gring = D.gring;
       L.rbits = D.rbits;
       L.rl1 = D.rl1;
+      // a one-CTA-per-SM simulation too big for shared memory (C5: 65,536
+      // agents) still keeps its ready bitmaps there (8.4 KB): dispatch walks
+      // them for every member (capi.cu hot_smem sizes the same bytes)
+      const size_t bm = static_cast<size_t>(nwords + (nwords + 31) / 32) * sizeof(u32);
+      if (kLru && n > 0 && bm <= dyn_bytes) {
+        L.rbits = reinterpret_cast<u32*>(dyn);
+        L.rl1 = L.rbits + nwords;
+        used = (bm + 15) / 16 * 16;
+      }
     }
     // offload: the tree's walk mirror takes the rest (capi.cu big_smem)
     const size_t room = used < dyn_bytes ? (dyn_bytes - used) / kTWalkSmemBytes : 0;

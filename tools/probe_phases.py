@@ -24,6 +24,10 @@ elif which == "c2":
     specs = [engine.SimSpec.from_scenario(config.c2_qwen("aimd"))]
 elif which == "c5":
     specs = [engine.SimSpec.from_scenario(config.c5_stress("aimd"))]
+elif which == "c5h":  # the bench's C5 line: full size to a 5e4 s horizon
+    s = config.c5_stress("aimd")
+    s.engine.horizon = 5e4
+    specs = [engine.SimSpec.from_scenario(s)]
 elif which.startswith("c5s"):  # scaled C5 shape: c5s<agents>
     ag = int(which[3:])
     s = config.c5_stress("aimd", agents=ag, capacity=1)
