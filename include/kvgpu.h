@@ -520,6 +520,14 @@ KVG_API kvg_status kvg_cache_match_batch(kvg_cache* c, const uint32_t* agents,
  * of the last grid-wide eviction. */
 KVG_API kvg_status kvg_cache_last_ms(const kvg_cache* c, double* ms, uint32_t* grid_blocks);
 
+/* Test hook: the engine's ready-set walk (the smallest ready agent id >= from,
+ * or 0xffffffff) in both device forms — the sweep kernel's and the
+ * one-CTA-per-SM kernels' — over a caller's bitmap of n agents: rbits (one bit
+ * per agent) and rl1 (one bit per non-empty rbits word). */
+KVG_API kvg_status kvg_check_ready_next(int device, const uint32_t* rbits, const uint32_t* rl1,
+                                        uint32_t n, const uint32_t* from, uint32_t nq,
+                                        uint32_t* out_narrow, uint32_t* out_wide);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -30,6 +30,12 @@ using kvg::u32;
 using kvg::u64;
 using kvg_host::set_error;
 
+namespace kvg_engine_cfg {  // engine.cu
+cudaError_t check_ready_next(const unsigned* rbits, const unsigned* rl1, unsigned n,
+                             const unsigned* from, unsigned nq, unsigned* out_narrow,
+                             unsigned* out_wide);
+}
+
 namespace {
 
 #define CUDA_TRY(expr)                                                              \
@@ -651,3 +657,32 @@ KVG_API void kvg_cache_free(kvg_cache* c) {
 }
 
 }  // extern "C"
+
+extern "C" {
+KVG_API kvg_status kvg_check_ready_next(int device, const uint32_t* rbits, const uint32_t* rl1,
+                                        uint32_t n, const uint32_t* from, uint32_t nq,
+                                        uint32_t* out_narrow, uint32_t* out_wide) {
+  if (rbits == nullptr || rl1 == nullptr || from == nullptr || out_narrow == nullptr ||
+      out_wide == nullptr || n == 0)
+    return (kvg_status)set_error(KVG_ERR_CONFIG, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  const size_t nw = (n + 31) / 32, n1 = (nw + 31) / 32;
+  unsigned *d = nullptr;
+  const size_t words = nw + n1 + 3 * static_cast<size_t>(nq) + 4;
+  CUDA_TRY(cudaMalloc(&d, words * 4));
+  unsigned* d_rb = d;
+  unsigned* d_r1 = d + ((nw + 3) & ~size_t(3));  // 16 B aligned, as in the engine's layouts
+  unsigned* d_from = d_r1 + n1;
+  unsigned* d_on = d_from + nq;
+  unsigned* d_ow = d_on + nq;
+  cudaError_t e = cudaMemcpy(d_rb, rbits, nw * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_r1, rl1, n1 * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d_from, from, size_t(nq) * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = kvg_engine_cfg::check_ready_next(d_rb, d_r1, n, d_from, nq, d_on, d_ow);
+  if (e == cudaSuccess) e = cudaMemcpy(out_narrow, d_on, size_t(nq) * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(out_wide, d_ow, size_t(nq) * 4, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return (kvg_status)set_error(KVG_ERR_CUDA, cudaGetErrorString(e));
+  return KVG_OK;
+}
+}

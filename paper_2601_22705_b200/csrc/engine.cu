@@ -857,6 +857,35 @@ __global__ void __launch_bounds__(256) pack_traces(const SimDev* __restrict__ si
 
 #include "grid.cuh"
 
+namespace kvg {
+// Test hook (kvg_check_ready_next): both forms of the ready-set walk over a
+// caller's two-level bitmap, one query per thread.
+__global__ void ready_probe_kernel(const u32* rbits, const u32* rl1, u32 n, const u32* from,
+                                   u32 nq, u32* out_narrow, u32* out_wide) {
+  Lead L;
+  L.n = n;
+  L.nwords = (n + 31) / 32;
+  L.rbits = const_cast<u32*>(rbits);
+  L.rl1 = const_cast<u32*>(rl1);
+  SimDev D;
+  for (u32 q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    out_narrow[q] = ready_next(D, L, from[q]);
+    out_wide[q] = ready_next_wide(D, L, from[q]);
+  }
+}
+}  // namespace kvg
+
+namespace kvg_engine_cfg {
+cudaError_t check_ready_next(const unsigned* rbits, const unsigned* rl1, unsigned n,
+                             const unsigned* from, unsigned nq, unsigned* out_narrow,
+                             unsigned* out_wide) {
+  const unsigned nblocks = (nq + 255) / 256 < 1024 ? (nq + 255) / 256 : 1024;
+  kvg::ready_probe_kernel<<<nblocks ? nblocks : 1, 256>>>(rbits, rl1, n, from, nq, out_narrow,
+                                                          out_wide);
+  return cudaGetLastError();
+}
+}  // namespace kvg_engine_cfg
+
 #ifdef KVG_GRID_PROF
 extern "C" __attribute__((visibility("default"))) int kvg_debug_gprof(unsigned long long* out) {
   cudaMemcpyFromSymbol(out, kvg::g_gprof, sizeof(kvg::g_gprof));
