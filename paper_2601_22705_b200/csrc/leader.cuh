@@ -1004,8 +1004,8 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   const u32 kind = L.kind;
   const double usage = static_cast<double>(L.used) / L.capacity_d;
   const double decay = L.decay, interval = L.interval;
-  const u64 pending = static_cast<u64>(L.pend_size) + L.paus_size;
-  const u64 dec = L.decoded_cum, rec = L.rec_cum;
+  // (the row's pending / decoded / recompute counts are read from Lead at
+  // each row: held in registers across the loop they spill at 72)
   const u64 trace_cap = D.trace_cap;
   const kvg_controller_config c = L.cfg;
   const bool offload_h = kHoist ? L.offload : false;
@@ -1070,9 +1070,9 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
                        : kind == KVG_POLICY_UNCONTROLLED ? static_cast<double>(L.n)
                                                          : static_cast<double>(L.cap);
         row.active = act;
-        row.pending = pending;
-        row.decoded_cum = dec;
-        row.recompute_cum = rec;
+        row.pending = static_cast<u64>(L.pend_size) + L.paus_size;
+        row.decoded_cum = L.decoded_cum;
+        row.recompute_cum = L.rec_cum;
         row.transfers = (kHoist ? offload_h : L.offload) ? x_in_flight(D, L, clock) : 0;
         row.hit_matched = m;
         row.hit_requested = r;
