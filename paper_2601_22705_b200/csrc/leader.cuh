@@ -1015,8 +1015,8 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   const u64 cap_h = kHoist ? static_cast<u64>(L.cap) : 0;
   // evolving state
   double clock = L.clock, tick_t = L.tick_t, adm_t = L.adm_t;
-  double hit_m = L.hit_m, hit_r = L.hit_r, window = L.window, su = L.su, sh = L.sh;
-  int have_s = L.have_s, tick_on = L.tick_on, adm_on = L.adm_on;
+  double hit_m = L.hit_m, hit_r = L.hit_r, window = L.window;
+  int tick_on = L.tick_on, adm_on = L.adm_on;  // (smoothing state: read / written in place)
   u64 ord = L.ord, tick_o = L.tick_o, adm_o = L.adm_o, events = L.events, ticks = L.ticks;
   unsigned long long n_trace = L.n_trace;
   for (;;) {
@@ -1042,13 +1042,13 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
       if (kind == KVG_POLICY_AIMD) {
         double u = usage, h = hit;
         if (c.signal_smoothing > 0) {
-          if (have_s) {
-            u = c.signal_smoothing * su + (1 - c.signal_smoothing) * usage;
-            h = c.signal_smoothing * sh + (1 - c.signal_smoothing) * hit;
+          if (L.have_s) {
+            u = c.signal_smoothing * L.su + (1 - c.signal_smoothing) * usage;
+            h = c.signal_smoothing * L.sh + (1 - c.signal_smoothing) * hit;
           }
-          su = u;
-          sh = h;
-          have_s = 1;
+          L.su = u;
+          L.sh = h;
+          L.have_s = 1;
         }
         double w = window;
         if (u < c.u_low)
@@ -1121,9 +1121,6 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   L.hit_m = hit_m;
   L.hit_r = hit_r;
   L.window = window;
-  L.su = su;
-  L.sh = sh;
-  L.have_s = have_s;
   L.tick_on = tick_on;
   L.adm_on = adm_on;
   L.ord = ord;
