@@ -1017,7 +1017,10 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   double clock = L.clock, tick_t = L.tick_t, adm_t = L.adm_t;
   double hit_m = L.hit_m, hit_r = L.hit_r, window = L.window;
   int tick_on = L.tick_on, adm_on = L.adm_on;  // (smoothing state: read / written in place)
-  u64 ord = L.ord, tick_o = L.tick_o, adm_o = L.adm_o, events = L.events, ticks = L.ticks;
+  // the scheduled slots' ordinals are stored in place; event and tick counts
+  // are kept as 32-bit deltas (registers are what the sweep kernel lacks)
+  u64 ord = L.ord;
+  u32 d_events = 0, d_ticks = 0;
   unsigned long long n_trace = L.n_trace;
   for (;;) {
     // next housekeeping event, if it precedes every agent event (rank 0)
@@ -1038,7 +1041,7 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
       tick_on = 0;
       const double m = hit_m, r = hit_r;
       const double hit = r > 0 ? m / r : 1.0;
-      ++ticks;  // Controller::update_window
+      ++d_ticks;  // Controller::update_window
       if (kind == KVG_POLICY_AIMD) {
         double u = usage, h = hit;
         if (c.signal_smoothing > 0) {
@@ -1082,13 +1085,13 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
       hit_r = r * decay;
       tick_on = 1;
       tick_t = clock + interval;
-      tick_o = ord++;
+      L.tick_o = ord++;
       if (!(adm_on && adm_t == clock)) {  // schedule_admission
         if (adm_on) break;                // cannot happen; general path reports it
         adm_on = 1;
         adm_t = clock;
-        adm_o = ord++;
-        ++events;
+        L.adm_o = ord++;
+        ++d_events;
         // the admission check just scheduled is the very next event (agent
         // events are later than this tick and, unless clock + interval
         // rounds to clock, so is the next tick): a no-op check is taken here
@@ -1098,11 +1101,11 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
                                                     : kHoist ? cap_h : static_cast<u64>(L.cap);
         if (tick_t > clock && nready0 && !(act < limit && admit_src)) {
           adm_on = 0;
-          ++events;
+          ++d_events;
         }
         continue;
       }
-      ++events;
+      ++d_events;
     } else {
       const u64 limit = kind == KVG_POLICY_UNCONTROLLED ? ~0ull
                         : kind == KVG_POLICY_AIMD ? static_cast<u64>(floor(window))
@@ -1112,7 +1115,7 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
       if (!noop) break;  // the general path runs the real admission pass
       clock = bt;
       adm_on = 0;
-      ++events;
+      ++d_events;
     }
   }
   L.clock = clock;
@@ -1124,10 +1127,8 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
   L.tick_on = tick_on;
   L.adm_on = adm_on;
   L.ord = ord;
-  L.tick_o = tick_o;
-  L.adm_o = adm_o;
-  L.events = events;
-  L.ticks = ticks;
+  L.events += d_events;
+  L.ticks += d_ticks;
   L.n_trace = n_trace;
 }
 
