@@ -1137,8 +1137,12 @@ __device__ __forceinline__ void fast_housekeeping(const SimDev& D, Lead& L) {
 // pending in front of it (the steady state between agent events). Smoothed
 // signals (an EMA chain per tick) and offload mode (a link-queue purge per
 // tick) stay on the scalar path.
+template <bool kOff>
 __device__ __forceinline__ bool ticks_apply(const Lead& L) {
-  if (L.offload || L.status != KVG_OK || L.finished == L.n || !L.tick_on || L.adm_on) return false;
+  // (checked every event-loop turn: the usual exit, a pending admission
+  // check, first; the offload flag only where the tier is compiled in)
+  if (L.adm_on || !L.tick_on || L.status != KVG_OK || L.finished == L.n) return false;
+  if (kOff && L.offload) return false;
   if (L.kind == KVG_POLICY_AIMD && L.cfg.signal_smoothing > 0) return false;
   const double t_agent = L.hsize > 0 ? L.heap[0].t : __longlong_as_double(0x7ff0000000000000ll);
   return L.tick_t < t_agent && !(L.tick_t > L.horizon) &&
@@ -1786,7 +1790,7 @@ __device__ void leader_step(const SimDev& D, Lead& L, Op& op) {
             return;
           }
         }
-        if (ticks_apply(L)) {  // pipelined ticks on warp 0, then back here
+        if (ticks_apply<kOff>(L)) {  // pipelined ticks on warp 0, then back here
           op.kind = OP_TICKS;
           return;
         }
