@@ -1682,11 +1682,16 @@ __device__ __forceinline__ void batch_end(const SimDev& D, Lead& L) {
     const double share = total > 0 ? wall / total : 0.0;
     const bool group = !(kOff && L.offload) && nb >= L.group_min;
     u32 tail = ring_at(L.gr_head, L.gr_n, L.n);
+    // the ledger sums in registers across the members (same additions in
+    // the same order; through Lead each would be a shared-memory round trip,
+    // reloaded after every member read through the generic batch pointer)
+    double lf = L.ledger.prefill_fresh, lr = L.ledger.prefill_recompute,
+           ld = L.ledger.decode;
     for (u32 i = 0; i < nb; ++i) {
       const Member& m = D.batch[i];
-      L.ledger.prefill_fresh += share * m.f;
-      L.ledger.prefill_recompute += share * m.r;
-      L.ledger.decode += share * m.d;
+      lf += share * m.f;
+      lr += share * m.r;
+      ld += share * m.d;
       if (!group) {
         sched_agent(D, L, m.id, start + wall, EV_GEN);
         continue;
@@ -1700,6 +1705,9 @@ __device__ __forceinline__ void batch_end(const SimDev& D, Lead& L) {
       L.gring[tail] = m.id;
       tail = ring_at(tail, 1, L.n);
     }
+    L.ledger.prefill_fresh = lf;
+    L.ledger.prefill_recompute = lr;
+    L.ledger.decode = ld;
     if (group) {
       L.gr_n += nb;
       heap_push(L, HeapEnt{start + wall, (L.ord << kKeyShift) | kGroupFlag | nb});
